@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""bench.py — time-to-eps of MB-VI on BASELINE config 2 (B200, sm_100a).
+
+Workload (BASELINE.json configs[1], the metric's own config, fits one GPU):
+random dense MDP |S| = 10 000, |A| = 16, gamma = 0.99, P stored fp32
+(6.4 GB, > L2), fp64 accumulation and V, eps = 1e-6, V0 = 0.
+
+One STEP = one complete MB-VI solve to eps at the headline batch size b
+(default 1000): every sweep's partition draw, all batches with their
+interim-V reads and barriers, residual and stop test, V/pi outputs — all of
+SURVEY 8(a) a1-a5, a8 — in one persistent kernel launch.
+value = state-action backups per second = sweeps * |S| * |A| / time.
+
+Also reported: the roofline of the solver kernel (algorithmic HBM bytes per
+launch / event-timed launch duration vs MEASURED_PEAKS.json), time-to-eps
+for every b in {1, 64, 1000, 10000} (Gauss-Seidel -> Bellman), the e2e number
+through the C ABI with host buffers, and the CPU oracle baseline.
+
+  python bench.py [--gpus N --steps K --warmup W --b B]
+  python bench.py --impl reference   # the CPU oracle arm (host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "state-action backups/sec (HBM GB/s vs peak) and time-to-ε vs batch size, 1/2/4/8 B200"
+UNIT = "state-action backups/s"
+N_STATES, N_ACTIONS, GAMMA, EPS, INST_SEED = 10_000, 16, 0.99, 1e-6, 1
+WORKLOAD = ("BASELINE config 2: random dense MDP |S|=10000 |A|=16 gamma=0.99, MB-VI to eps=1e-6 "
+            "(residual stop), V0=0, P fp32 (6.4 GB) + fp64 accumulation/V")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algo_bytes_per_sweep(n, A, psz, b):
+    """P + c + V read/write (+ the 4n-byte permutation when b < n)."""
+    return n * A * n * psz + n * A * psz + 2 * n * 8 + (4 * n if b < n else 0)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.idx, self.p = idx, None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out = self.p.communicate(timeout=5)[0]
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle
+def oracle_sample(seconds_target=12.0, n_rows=200):
+    """The oracle as it stands (single-threaded C, fp64, sequential sums) on a
+    bounded sample of the config-2 workload: full Bellman backups
+    (16 actions x 10^4 successors) of `n_rows` states of the instance, repeated
+    until ~seconds_target of CPU time.  Returns (backups/s, cores, sample)."""
+    import numpy as np
+
+    import gen
+    import oracle
+    Ph, ch = gen.dense(N_STATES, N_ACTIONS, INST_SEED, rows=(0, n_rows))
+    V = np.random.default_rng(0).random(N_STATES) * 50
+    done, t0 = 0, time.perf_counter()
+    while True:
+        for s in range(n_rows):
+            oracle.backup_dense_row(Ph[s], ch[s], GAMMA, V)
+        done += n_rows
+        el = time.perf_counter() - t0
+        if el >= seconds_target:
+            break
+    rate = done * N_ACTIONS / el
+    return rate, 1, (f"oracle.backup_dense_row (single thread) over states 0..{n_rows - 1} of the config-2 "
+                     f"instance, {done} state backups x 16 actions x 10^4 successors in {el:.1f} s")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import gen
+    import oracle
+    n_rows = 64
+    Ph, ch = gen.dense(N_STATES, N_ACTIONS, INST_SEED, rows=(0, n_rows))
+    V = np.random.default_rng(0).random(N_STATES) * 50
+
+    def step():
+        for s in range(n_rows):
+            oracle.backup_dense_row(Ph[s], ch[s], GAMMA, V)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = args.steps * n_rows * N_ACTIONS / el
+    sample = (f"each step = oracle Bellman backups of {n_rows} states (x16 actions x 10^4 successors) of the "
+              f"config-2 instance, single thread")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "b": args.b, "parallelism": "cpu1"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--b", type=int, default=1000)
+    ap.add_argument("--impl", default="rmb", choices=["rmb", "reference"])
+    ap.add_argument("--no-bsweep", action="store_true", help="skip the per-b time-to-eps table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_2110_02901_b200 as rmb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # each rank solves its own instance (replicas)
+    P, c = rmb.generate_dense(N_STATES, N_ACTIONS, INST_SEED + rank)
+    prob = rmb.Problem.dense(P, c, GAMMA)
+    V = torch.zeros(N_STATES, dtype=torch.float64, device=dev)
+    pi = torch.zeros(N_STATES, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+
+    def solve(b, seed=0):
+        return prob.vi(b, seed=seed, eps=EPS, max_sweeps=200_000, V=V, pi=pi, v0_zero=True)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        solve(args.b, seed=w)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sweeps = 0
+    kernel_s = 0.0
+    launches = 0
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for s in range(args.steps):
+            sol = solve(args.b, seed=100 + s)
+            sweeps += sol.stats.sweeps
+            kernel_s += sol.stats.seconds
+            launches += prob.last_launch_count()
+            flush.zero_()  # L2 flush between timed solves (P is > L2 anyway)
+        ev1.record(stream)
+        barrier()
+    t = ev0.elapsed_time(ev1) / 1e3
+    tt = torch.tensor([t, sweeps], dtype=torch.float64, device=dev)
+    if dist:
+        tmax = tt.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tot = tt.clone()
+        dist.all_reduce(tot[1:], op=dist.ReduceOp.SUM)
+        t, sweeps_all = float(tmax[0]), float(tot[1])
+    else:
+        sweeps_all = sweeps
+    value = sweeps_all * N_STATES * N_ACTIONS / t
+
+    peak, peak_src = peaks()
+    bps = algo_bytes_per_sweep(N_STATES, N_ACTIONS, 4, args.b)
+    achieved = sweeps * bps / kernel_s / 1e9  # per launch = whole solve kernel
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "b": args.b, "sweeps_per_solve": sweeps / args.steps,
+                   "l2": "inputs larger than L2 (P 6.4 GB) + 256 MB flush between solves",
+                   "parallelism": f"replicas{world}" if world > 1 else "dp1"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_src, "kernel": "dense_solver_kernel<float,4>",
+                     "algorithmic_bytes_per_sweep": bps},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and not args.no_bsweep:
+        table = []
+        for b in (1, 64, 1000, 10_000):
+            sol = solve(b, seed=7)
+            st = sol.stats
+            bb = algo_bytes_per_sweep(N_STATES, N_ACTIONS, 4, b)
+            table.append({"b": b, "sweeps": st.sweeps, "batches_per_sweep": -(-N_STATES // b),
+                          "time_to_eps_ms": st.seconds * 1e3,
+                          "us_per_batch": st.seconds / max(1, st.batches) * 1e6,
+                          "backups_per_s": st.sweeps * N_STATES * N_ACTIONS / st.seconds,
+                          "GB_per_s": st.sweeps * bb / st.seconds / 1e9})
+        result["time_to_eps_vs_b"] = table
+
+    if rank == 0 and not args.no_e2e:
+        # e2e through the C ABI with HOST buffers: H2D of P, c inside the timed region
+        Ph = torch.empty(P.shape, dtype=P.dtype, pin_memory=True)
+        ch = torch.empty(c.shape, dtype=c.dtype, pin_memory=True)
+        Ph.copy_(P)
+        ch.copy_(c)
+        Vh = np.zeros(N_STATES)
+        pih = np.zeros(N_STATES, np.int32)
+        del prob
+        torch.cuda.empty_cache()
+        del P
+        torch.cuda.empty_cache()
+
+        def e2e_step(seed):
+            p2 = rmb.Problem.dense(Ph, ch, GAMMA)
+            sol = p2.vi(args.b, seed=seed, eps=EPS, max_sweeps=200_000, V=Vh, pi=pih, v0_zero=True)
+            p2.close()
+            return sol.stats.sweeps
+
+        e2e_step(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sw = 0
+        ksteps = max(1, min(args.steps, 3))
+        for s in range(ksteps):
+            sw += e2e_step(100 + s)
+        te = time.perf_counter() - t0
+        result["e2e"] = {"value": sw * N_STATES * N_ACTIONS / te, "unit": UNIT,
+                         "h2d_bytes_per_step": int(Ph.numel() * 4 + ch.numel() * 4),
+                         "d2h_bytes_per_step": int(N_STATES * 8 + N_STATES * 4 + 8 * sw / ksteps),
+                         "steps": ksteps, "path": "rmb_create_dense(host P,c) + rmb_vi(host V,pi) + rmb_destroy"}
+
+    if rank == 0 and not args.no_cpu:
+        rate, cores, sample = oracle_sample()
+        result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

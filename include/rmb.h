@@ -1,0 +1,193 @@
+/*
+ * rmb.h — C ABI of the B200-native randomized mini-batch DP library.
+ *
+ * Method: the randomized mini-batch operator of arXiv 2110.02901
+ * (Gargiani, Martinelli, Ruts Martinez, Lygeros), Sec. III:
+ *   B_b J(i)      = min_u [ g(i,u) + a sum_{j in S\M(i)} p_ij(u) J(j)
+ *                                  + a sum_{j in M(i)}   p_ij(u) B_b J(j) ]   (Eq. 12)
+ *   B_{mu,b} J(i) = the same with u = mu(i)                                  (Eq. 13)
+ * where M(i) is the set of states in earlier batches of size b (Eq. M(i),
+ * P:L163-166) after a random re-indexing drawn before every operator
+ * application.  b = |S| gives the Bellman operator T, b = 1
+ * the Gauss-Seidel operator F.  MB-VI and MB-MPI (Alg. 1
+ * P:L103-131) apply it until the sup-norm residual falls below eps.
+ *
+ * Notation: b = batch size (the paper's m), m = MPI
+ * evaluation sweeps per outer iteration (the paper's K), gamma = alpha,
+ * c(s,a) = g(i,u), V = J, pi = mu.
+ *
+ * Conventions for every entry point:
+ *   - all sizes are int64_t; states are 0-based;
+ *   - P, c, row_ptr/col/val, V and pi may be DEVICE pointers or HOST
+ *     pointers (pageable or pinned); the library inspects each pointer
+ *     (cudaPointerGetAttributes) and stages host buffers through device
+ *     memory it owns, copying results back before returning;
+ *   - every call returns only after its results are complete and, for host
+ *     outputs, copied back (the stream given at create is synchronised);
+ *   - no call aborts the process: errors are returned as rmb_status and a
+ *     human-readable message is available from rmb_last_error() (per thread).
+ *   - one handle is used by one host thread at a time.
+ */
+#ifndef RMB_H
+#define RMB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rmb_problem_s* rmb_problem; /* opaque */
+
+typedef enum {
+    RMB_OK = 0,
+    RMB_ERR_INVALID_ARG = 1,   /* argument check failed; no device work was done          */
+    RMB_ERR_INVALID_MDP = 2,   /* RMB_VALIDATE: a row does not sum to 1, a column is out
+                                  of range, or a cost is not finite */
+    RMB_ERR_NOT_CONVERGED = 3, /* max sweeps / outer iterations reached; V, pi, trace valid */
+    RMB_ERR_NONFINITE = 4,     /* a backup produced inf/nan; the solve stopped there        */
+    RMB_ERR_CUDA = 5,          /* a CUDA runtime error (message in rmb_last_error)          */
+    RMB_ERR_NCCL = 6,          /* reserved: multi-GPU exchange error                        */
+    RMB_ERR_OOM = 7,           /* device or host allocation failed                          */
+    RMB_ERR_UNSUPPORTED = 8    /* a valid request outside this build's supported envelope   */
+} rmb_status;
+
+typedef enum { RMB_F32 = 0, RMB_F64 = 1 } rmb_dtype;
+
+/* Problem description: the tuple (S, U, P, g, alpha) of P:L37 with a uniform
+ * action count (state-dependent U(i) is encoded by duplicating an admissible
+ * action's row; the lowest-index tie-break makes that exact). */
+typedef struct {
+    int64_t n_states;   /* |S| >= 1                                                  */
+    int32_t n_actions;  /* |A| >= 1                                                  */
+    double gamma;       /* discount alpha in (0,1)                                   */
+    rmb_dtype p_dtype;  /* storage type of P (or CSR val) and c                      */
+    rmb_dtype v_dtype;  /* storage type of V: RMB_F64 only in this build             */
+    int64_t row_begin;  /* owned states [row_begin,row_end); 0 and n_states on 1 GPU  */
+    int64_t row_end;
+    void* nccl_comm;    /* reserved for the multi-GPU exchange; must be NULL         */
+    void* stream;       /* cudaStream_t used for all work of this handle (NULL = legacy default) */
+} rmb_desc;
+
+/* flags */
+#define RMB_ORDER_IDENTITY 0x1u /* no shuffle: ascending order (the paper's Sec. III analysis) */
+#define RMB_V0_ZERO 0x2u        /* ignore V's content on entry and start from V0 = 0        */
+#define RMB_PI_GIVEN 0x4u       /* rmb_mpi: pi holds the initial policy (else pi_0 = greedy(V0))     */
+#define RMB_VALIDATE 0x8u       /* rmb_create_*: check the MDP on device (RMB_ERR_INVALID_MDP)       */
+
+/* Create a handle over a DENSE MDP.
+ *   P: [n][A][n] row-major, P[(s*A + a)*n + j] = p(j | s, a), dtype desc->p_dtype.
+ *   c: [n][A], c[s*A + a] = stage cost, same dtype.
+ * Device pointers are BORROWED (must outlive the handle; never copied).
+ * Host pointers are copied once into owned device memory.
+ * The library allocates its workspace here and in the first solve.
+ * Errors: INVALID_ARG (sizes, gamma, dtype, NULL pointers), INVALID_MDP
+ * (with RMB_VALIDATE), OOM, CUDA. */
+rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, uint32_t flags,
+                            rmb_problem* out);
+
+/* Create a handle over a SPARSE MDP in CSR form over rows r = s*A + a.
+ *   row_ptr: int64 [n*A + 1], row_ptr[0] = 0, nondecreasing;
+ *   col:     int32 [nnz] successor state ids in [0, n);
+ *   val:     [nnz] probabilities (p_dtype);  c: [n][A] costs (p_dtype).
+ * A fixed-stride row_ptr (row_ptr[r] = r*K) is detected and served by the
+ * ELL kernel.  Ownership and errors as rmb_create_dense. */
+rmb_status rmb_create_csr(const rmb_desc* desc, const int64_t* row_ptr, const int32_t* col,
+                          const void* val, const void* c, uint32_t flags, rmb_problem* out);
+
+typedef struct {
+    int64_t sweeps;        /* operator applications done (VI sweeps or MPI evaluation sweeps) */
+    int64_t batches;       /* batches processed                                              */
+    int64_t outer_iters;   /* MPI outer iterations (0 for VI)                                */
+    double final_residual; /* VI: last r_k; MPI: last ||TV - V||_inf                         */
+    double seconds;        /* device time of the solve (CUDA events)                         */
+    int32_t converged;     /* 1 if the stopping test passed                                  */
+    int32_t status;        /* the rmb_status returned                                        */
+} rmb_stats;
+
+/* MB-VI: V <- V0 (V's content, or 0 with RMB_V0_ZERO); for sweeps
+ * k = 1, 2, ...: draw the partition of sweep k (seed, k), apply B_b, record
+ * r_k = ||V_k - V_{k-1}||_inf; stop at the first r_k <= eps.
+ *   b in [1, n]; eps > 0; max_sweeps >= 1.
+ *   V: [n] float64 in/out.  pi: [n] int32 out (the argmin of each state's
+ *   final-sweep backup).  trace: HOST [max_sweeps] or NULL (r_k, k = 1..).
+ *   stats: HOST or NULL.
+ * Returns OK, NOT_CONVERGED (outputs valid), NONFINITE, or an error. */
+rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t max_sweeps,
+                  uint32_t flags, void* V, int32_t* pi, double* trace, rmb_stats* stats);
+
+/* MB-MPI: Algorithm 1 with B_{pi,b} evaluation sweeps and warm
+ * start.  pi_0 = greedy(V0) unless RMB_PI_GIVEN.  Each outer
+ * iteration: m evaluation sweeps (each draws its own partition, sweep
+ * counter k continues across outer iterations), then the improvement
+ * pi' = argmin_a Q(s,a) over all states (no V write) with
+ * changed = #{pi' != pi} and r_T = ||TV - V||_inf; stop when changed == 0
+ * and r_T <= eps.
+ *   trace: HOST [max_outer*(m+1)] or NULL: trace[o*(m+1)+e] = residual of
+ *          evaluation sweep e of outer o, trace[o*(m+1)+m] = r_T.
+ *   changed: HOST [max_outer] or NULL.
+ * Returns as rmb_vi. */
+rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double eps, int64_t max_outer,
+                   uint32_t flags, void* V, int32_t* pi, double* trace, int64_t* changed,
+                   rmb_stats* stats);
+
+/* One application of B_b (pi_or_null == NULL) or B_{pi,b} with the
+ * partition of sweep number `sweep` (>= 1): V_out = B V_in.  V_in and V_out
+ * may alias.  argmin_out ([n] int32, may be NULL) receives the argmin (or
+ * pi).  resid_out (HOST, may be NULL) receives ||V_out - V_in||_inf. */
+rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uint32_t flags,
+                     const int32_t* pi_or_null, const void* V_in, void* V_out, int32_t* argmin_out,
+                     double* resid_out);
+
+/* Policy improvement of Algorithm 1 alone: pi <- greedy(V)
+ * (lowest index on ties), *changed = #{states whose action changed},
+ * *bellman_resid = ||TV - V||_inf.  pi: [n] int32 in/out.  Outputs HOST or NULL. */
+rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellman_resid, int64_t* changed);
+
+/* Host-side partition generator: perm[p] = pi_sweep(p),
+ * the state processed at position p of operator application `sweep`;
+ * batch t = positions [t*b, min(n,(t+1)*b)).  perm: HOST [n] uint32.
+ * flags: RMB_ORDER_IDENTITY gives the identity. */
+rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm);
+
+/* The same permutation evaluated by the device kernel the solver uses
+ * (perm: DEVICE [n] uint32) — exposed for parity tests. */
+rmb_status rmb_partition_device(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm,
+                                void* stream);
+
+/* Synthetic instance generators (gen/rmb_gen.h), evaluated on device.
+ * All output pointers are DEVICE pointers of the documented sizes.
+ *   kind 0 = dense random, 1 = dense dyadic: P [n][A][n], c [n][A];
+ *   rows [s0, s1) only (pass 0, n for the whole instance; P/c then hold
+ *   (s1-s0) states).                                                      */
+rmb_status rmb_generate_dense(int32_t kind, uint64_t seed, int64_t n, int32_t A, int64_t s0, int64_t s1,
+                              rmb_dtype dtype, void* P, void* c, void* stream);
+/* sparse random, K successors per (s,a): row_ptr [(s1-s0)*A+1], col/val [(s1-s0)*A*K], c [(s1-s0)*A] */
+rmb_status rmb_generate_sparse(uint64_t seed, int64_t n, int32_t A, int32_t K, int64_t s0, int64_t s1,
+                               rmb_dtype dtype, int64_t* row_ptr, int32_t* col, void* val, void* c,
+                               void* stream);
+/* N x N slip gridworld, A = 4, ELL width 5: row_ptr [(s1-s0)*4+1], col/val [(s1-s0)*20], c [(s1-s0)*4] */
+rmb_status rmb_generate_grid(int64_t N, int64_t s0, int64_t s1, rmb_dtype dtype, int64_t* row_ptr,
+                             int32_t* col, void* val, void* c, void* stream);
+
+/* Kernel launches issued by the last solve/apply/improve call on this handle
+ * (evidence for bench.py's gpu_launches). */
+int64_t rmb_last_launch_count(rmb_problem h);
+
+/* Phase breakdown of the last solve as seen by CTA 0 of the persistent
+ * kernel (globaltimer): ns4[0] compute (streaming P), ns4[1] waiting in grid
+ * barriers, ns4[2] combine/patch, ns4[3] number of grid barriers.
+ * ns4: HOST [4] int64. */
+rmb_status rmb_last_phase_times(rmb_problem h, int64_t* ns4);
+
+/* Destroy the handle and free its workspace (borrowed buffers untouched). */
+rmb_status rmb_destroy(rmb_problem h);
+
+const char* rmb_status_string(rmb_status s);
+const char* rmb_last_error(void);   /* thread-local, "" if none */
+const char* rmb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RMB_H */

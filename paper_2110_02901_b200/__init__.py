@@ -1,0 +1,339 @@
+"""paper_2110_02901_b200 — B200-native randomized mini-batch dynamic programming.
+
+Thin ctypes binding over librmb.so (include/rmb.h).  Argument marshalling
+only: every step of the method (partition, batched backups, residuals, stop
+test, policy improvement) runs in the library's sm_100a CUDA kernels.  PyTorch
+supplies device memory and streams.  There is no CPU fallback: if librmb.so is
+missing or fails to load, every call raises.
+
+    import paper_2110_02901_b200 as rmb
+    P, c = rmb.generate_dense(n=10_000, A=16, seed=1)          # on cuda
+    prob = rmb.Problem.dense(P, c, gamma=0.99)
+    out = prob.vi(b=1000, seed=0, eps=1e-6)                      # MB-VI
+    out = prob.mpi(b=1000, m=10, seed=0, eps=1e-6)               # MB-MPI (Alg. 1)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librmb.so")
+
+# status codes (include/rmb.h)
+OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(9)
+F32, F64 = 0, 1
+ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE = 0x1, 0x2, 0x4, 0x8
+
+_lib = None
+
+
+class RmbError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("n_states", ctypes.c_int64), ("n_actions", ctypes.c_int32), ("gamma", ctypes.c_double),
+                ("p_dtype", ctypes.c_int), ("v_dtype", ctypes.c_int), ("row_begin", ctypes.c_int64),
+                ("row_end", ctypes.c_int64), ("nccl_comm", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_int64), ("batches", ctypes.c_int64), ("outer_iters", ctypes.c_int64),
+                ("final_residual", ctypes.c_double), ("seconds", ctypes.c_double),
+                ("converged", ctypes.c_int32), ("status", ctypes.c_int32)]
+
+
+_SIGS = {
+    "rmb_create_dense": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+                          ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "rmb_create_csr": ([ctypes.POINTER(_Desc), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                        ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "rmb_vi": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int64,
+                ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)],
+               ctypes.c_int),
+    "rmb_mpi": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double,
+                 ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                 ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
+    "rmb_apply": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                   ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "rmb_improve": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                     ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "rmb_partition": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p],
+                      ctypes.c_int),
+    "rmb_partition_device": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32,
+                              ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_generate_dense": ([ctypes.c_int32, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64,
+                            ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+                           ctypes.c_int),
+    "rmb_generate_sparse": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                             ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_generate_grid": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_last_launch_count": ([ctypes.c_void_p], ctypes.c_int64),
+    "rmb_last_phase_times": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "rmb_status_string": ([ctypes.c_int], ctypes.c_char_p),
+    "rmb_last_error": ([], ctypes.c_char_p),
+    "rmb_version": ([], ctypes.c_char_p),
+}
+
+
+def lib():
+    """Load librmb.so (building it first if the sources are newer). Raises if unavailable."""
+    global _lib
+    if _lib is None:
+        from . import _build
+        if _build.needs_build():
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"librmb.so not found at {LIB_PATH}; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _status_name(s):
+    try:
+        return lib().rmb_status_string(s).decode()
+    except Exception:
+        return str(s)
+
+
+def _check(status, ok=(OK,)):
+    if status not in ok:
+        raise RmbError(status, lib().rmb_last_error().decode())
+    return status
+
+
+# ------------------------------------------------------------------ buffers
+def _ptr(x):
+    """Raw address of a torch tensor / numpy array (host or device), or None."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return ctypes.c_void_p(x.ctypes.data)
+    assert x.is_contiguous()
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def _dtype_code(x):
+    import torch
+    dt = x.dtype
+    if dt in (np.float32, torch.float32):
+        return F32
+    if dt in (np.float64, torch.float64):
+        return F64
+    raise TypeError(f"P/c must be float32 or float64, got {dt}")
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        if not torch.cuda.is_available():
+            return None
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+@dataclass
+class Solution:
+    V: object
+    pi: object
+    trace: np.ndarray
+    status: int
+    stats: Stats
+    changed: np.ndarray | None = None
+
+    @property
+    def converged(self):
+        return self.status == OK
+
+
+class Problem:
+    """A handle over an MDP (S, U, P, g, alpha) living on the GPU."""
+
+    def __init__(self, handle, n, A, gamma, keep):
+        self._h = handle
+        self.n, self.A, self.gamma = n, A, gamma
+        self._keep = keep  # borrowed buffers must outlive the handle
+
+    # ------------------------------------------------------------ creation
+    @classmethod
+    def dense(cls, P, c, gamma, stream=None, validate=False):
+        """P: [n][A][n], c: [n][A] (float32/float64, torch cuda/cpu or numpy)."""
+        n, A, n2 = P.shape
+        assert n == n2 and tuple(c.shape) == (n, A) and c.dtype == P.dtype
+        d = _Desc(n, A, float(gamma), _dtype_code(P), F64, 0, n, None, _stream_ptr(stream))
+        h = ctypes.c_void_p()
+        _check(lib().rmb_create_dense(ctypes.byref(d), _ptr(P), _ptr(c), VALIDATE if validate else 0,
+                                      ctypes.byref(h)))
+        return cls(h, n, A, float(gamma), (P, c))
+
+    @classmethod
+    def csr(cls, n, A, row_ptr, col, val, c, gamma, stream=None, validate=False):
+        """CSR over rows r = s*A + a: row_ptr int64 [n*A+1], col int32, val float."""
+        d = _Desc(n, A, float(gamma), _dtype_code(val), F64, 0, n, None, _stream_ptr(stream))
+        h = ctypes.c_void_p()
+        _check(lib().rmb_create_csr(ctypes.byref(d), _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(c),
+                                    VALIDATE if validate else 0, ctypes.byref(h)))
+        return cls(h, n, A, float(gamma), (row_ptr, col, val, c))
+
+    def close(self):
+        if self._h:
+            lib().rmb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -------------------------------------------------------------- solves
+    def _vp(self, V, pi, device):
+        import torch
+        if V is None:
+            V = torch.zeros(self.n, dtype=torch.float64, device=device)
+        if pi is None:
+            pi = torch.zeros(self.n, dtype=torch.int32, device=device)
+        return V, pi
+
+    def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
+           device="cuda"):
+        """MB-VI: V, pi updated in place (torch cuda/cpu or numpy)."""
+        V, pi = self._vp(V, pi, device)
+        tr = np.zeros(max_sweeps)
+        st = Stats()
+        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+        s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
+        _check(s, (OK, NOT_CONVERGED, NONFINITE))
+        return Solution(V, pi, tr[: st.sweeps], s, st)
+
+    def mpi(self, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
+            v0_zero=False, device="cuda"):
+        """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start."""
+        V, pi = self._vp(V, pi, device)
+        tr = np.zeros(max_outer * (m + 1))
+        ch = np.zeros(max_outer, dtype=np.int64)
+        st = Stats()
+        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+        s = lib().rmb_mpi(self._h, b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi), _ptr(tr), _ptr(ch),
+                          ctypes.byref(st))
+        _check(s, (OK, NOT_CONVERGED, NONFINITE))
+        o = st.outer_iters
+        return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
+
+    def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False):
+        """One application of B_b (pi None) or B_{pi,b}: returns (V_out, argmin, residual)."""
+        import torch
+        if V_out is None:
+            V_out = torch.empty_like(V_in) if not isinstance(V_in, np.ndarray) else np.empty_like(V_in)
+        if argmin is None:
+            argmin = (torch.empty(self.n, dtype=torch.int32, device=V_out.device)
+                      if not isinstance(V_out, np.ndarray) else np.empty(self.n, np.int32))
+        r = ctypes.c_double()
+        s = lib().rmb_apply(self._h, b, seed, sweep, ORDER_IDENTITY if identity else 0, _ptr(pi), _ptr(V_in),
+                            _ptr(V_out), _ptr(argmin), ctypes.byref(r))
+        _check(s, (OK, NONFINITE))
+        return V_out, argmin, r.value
+
+    def improve(self, V, pi):
+        """Policy improvement (Alg. 1): pi in place; returns (pi, ||TV-V||, changed)."""
+        r, ch = ctypes.c_double(), ctypes.c_int64()
+        s = lib().rmb_improve(self._h, _ptr(V), _ptr(pi), ctypes.byref(r), ctypes.byref(ch))
+        _check(s, (OK, NONFINITE))
+        return pi, r.value, ch.value
+
+    def last_launch_count(self):
+        return int(lib().rmb_last_launch_count(self._h))
+
+    def last_phase_times(self):
+        """(compute_ns, barrier_ns, combine_ns, n_barriers) of the last solve, CTA 0's view."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(lib().rmb_last_phase_times(self._h, _ptr(out)))
+        return tuple(int(x) for x in out)
+
+
+# ---------------------------------------------------------- free functions
+def partition(n, seed, sweep, identity=False):
+    """Host-side partition generator: perm[p] = pi_sweep(p) (numpy uint32)."""
+    out = np.empty(n, dtype=np.uint32)
+    _check(lib().rmb_partition(n, seed, sweep, ORDER_IDENTITY if identity else 0, _ptr(out)))
+    return out
+
+
+def partition_device(n, seed, sweep, identity=False, stream=None):
+    """The solver's device permutation kernel, into a new cuda uint32-as-int32 tensor."""
+    import torch
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    _check(lib().rmb_partition_device(n, seed, sweep, ORDER_IDENTITY if identity else 0, _ptr(out),
+                                      _stream_ptr(stream)))
+    return out
+
+
+def generate_dense(n, A, seed, kind="random", dtype=None, rows=None, device="cuda", stream=None):
+    """Dense instance (gen/rmb_gen.h) generated on device: P [rows][A][n], c [rows][A]."""
+    import torch
+    dtype = dtype or torch.float32
+    s0, s1 = rows if rows is not None else (0, n)
+    P = torch.empty((s1 - s0, A, n), dtype=dtype, device=device)
+    c = torch.empty((s1 - s0, A), dtype=dtype, device=device)
+    code = F32 if dtype == torch.float32 else F64
+    _check(lib().rmb_generate_dense({"random": 0, "dyadic": 1}[kind], seed, n, A, s0, s1, code, _ptr(P), _ptr(c),
+                                    _stream_ptr(stream)))
+    return P, c
+
+
+def generate_sparse(n, A, K, seed, dtype=None, rows=None, device="cuda", stream=None):
+    import torch
+    dtype = dtype or torch.float32
+    s0, s1 = rows if rows is not None else (0, n)
+    nr = (s1 - s0) * A
+    rp = torch.empty(nr + 1, dtype=torch.int64, device=device)
+    col = torch.empty(nr * K, dtype=torch.int32, device=device)
+    val = torch.empty(nr * K, dtype=dtype, device=device)
+    c = torch.empty((s1 - s0, A), dtype=dtype, device=device)
+    code = F32 if dtype == torch.float32 else F64
+    _check(lib().rmb_generate_sparse(seed, n, A, K, s0, s1, code, _ptr(rp), _ptr(col), _ptr(val), _ptr(c),
+                                     _stream_ptr(stream)))
+    return rp, col, val, c
+
+
+def generate_grid(N, dtype=None, rows=None, device="cuda", stream=None):
+    import torch
+    dtype = dtype or torch.float32
+    s0, s1 = rows if rows is not None else (0, N * N)
+    nr = (s1 - s0) * 4
+    rp = torch.empty(nr + 1, dtype=torch.int64, device=device)
+    col = torch.empty(nr * 5, dtype=torch.int32, device=device)
+    val = torch.empty(nr * 5, dtype=dtype, device=device)
+    c = torch.empty((s1 - s0, 4), dtype=dtype, device=device)
+    code = F32 if dtype == torch.float32 else F64
+    _check(lib().rmb_generate_grid(N, s0, s1, code, _ptr(rp), _ptr(col), _ptr(val), _ptr(c), _stream_ptr(stream)))
+    return rp, col, val, c
+
+
+def version():
+    return lib().rmb_version().decode()

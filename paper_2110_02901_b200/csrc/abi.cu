@@ -1,0 +1,526 @@
+// abi.cu — the extern "C" boundary (include/rmb.h): argument checks, host
+// buffer staging, workspace, dispatch to the dense / sparse solvers.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+#include "partition.cuh"
+
+namespace rmb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static rmb_status fail(rmb_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+static rmb_status cuda_fail(cudaError_t e, const char* where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) return RMB_ERR_OOM;
+    return RMB_ERR_CUDA;
+}
+
+// true for device (or managed) memory; false for pageable / pinned host memory
+static bool is_device_ptr(const void* p)
+{
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Returns a device view of `p` (size bytes): p itself, or an owned copy.
+static rmb_status device_view(Problem& pr, const void* p, size_t bytes, const void** out, const char* what)
+{
+    if (is_device_ptr(p)) {
+        *out = p;
+        return RMB_OK;
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    pr.owned.push_back(d);
+    e = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    *out = d;
+    return RMB_OK;
+}
+
+static rmb_status check_desc(const rmb_desc* d)
+{
+    if (!d) return fail(RMB_ERR_INVALID_ARG, "desc is NULL");
+    if (d->n_states < 1 || d->n_states > 0x7fffffffLL) return fail(RMB_ERR_INVALID_ARG, "n_states out of [1, 2^31)");
+    if (d->n_actions < 1) return fail(RMB_ERR_INVALID_ARG, "n_actions < 1");
+    if (!(d->gamma > 0.0 && d->gamma < 1.0)) return fail(RMB_ERR_INVALID_ARG, "gamma not in (0,1)");
+    if (d->p_dtype != RMB_F32 && d->p_dtype != RMB_F64) return fail(RMB_ERR_INVALID_ARG, "bad p_dtype");
+    if (d->v_dtype != RMB_F64) return fail(RMB_ERR_INVALID_ARG, "v_dtype must be RMB_F64 in this build");
+    if (!(d->row_begin == 0 && d->row_end == d->n_states))
+        return fail(RMB_ERR_UNSUPPORTED, "row sharding (row_begin/row_end != 0/n) is not in this build");
+    if (d->nccl_comm) return fail(RMB_ERR_UNSUPPORTED, "nccl_comm must be NULL in this build");
+    return RMB_OK;
+}
+
+static rmb_status init_problem(Problem& pr, const rmb_desc* d)
+{
+    pr.n = d->n_states;
+    pr.A = d->n_actions;
+    pr.gamma = d->gamma;
+    pr.pdt = d->p_dtype;
+    pr.stream = (cudaStream_t)d->stream;
+    cudaError_t e = cudaGetDevice(&pr.device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int v = 0;
+    e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, pr.device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    pr.num_sms = v;
+    e = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr.device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    pr.smem_optin = (size_t)v;
+    return RMB_OK;
+}
+
+static void free_problem(Problem* pr)
+{
+    if (!pr) return;
+    for (void* p : pr->owned) cudaFree(p);
+    pr->perm.release();
+    pr->part.release();
+    pr->ctrl.release();
+    pr->trace.release();
+    pr->chg.release();
+    pr->vstage.release();
+    pr->pistage.release();
+    pr->aux.release();
+    delete pr;
+}
+
+static rmb_status validate_mdp(Problem& pr)
+{
+    if (pr.aux.ensure(256) != cudaSuccess) return fail(RMB_ERR_OOM, "validate: allocation failed");
+    int* bad = static_cast<int*>(pr.aux.p);
+    cudaError_t e = launch_validate(pr, bad, pr.stream);
+    int h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "validate");
+    if (h) {
+        std::string m = "invalid MDP:";
+        if (h & 1) m += " a row of P does not sum to 1;";
+        if (h & 2) m += " a successor index is out of range;";
+        if (h & 4) m += " a probability or cost is not finite / not in [0,1];";
+        return fail(RMB_ERR_INVALID_MDP, m);
+    }
+    return RMB_OK;
+}
+
+static rmb_status solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t tl, long long* chg_dev,
+                        int64_t cl, SolveResult* res)
+{
+    return pr.dense ? dense_solve(pr, rq, trace_dev, tl, chg_dev, cl, res)
+                    : sparse_solve(pr, rq, trace_dev, tl, chg_dev, cl, res);
+}
+
+// Stage V (and optionally pi) to device.  Returns device pointers.
+struct Staged {
+    double* V = nullptr;
+    int32_t* pi = nullptr;
+    bool v_host = false, pi_host = false;
+};
+
+static rmb_status stage_in(Problem& pr, void* V, int32_t* pi, bool v_zero, bool copy_pi_in, Staged& s)
+{
+    const size_t vb = (size_t)pr.n * 8, pb = (size_t)pr.n * 4;
+    cudaError_t e = cudaSuccess;
+    if (is_device_ptr(V)) {
+        s.V = static_cast<double*>(V);
+    } else {
+        if (pr.vstage.ensure(vb) != cudaSuccess) return fail(RMB_ERR_OOM, "V staging allocation failed");
+        s.V = static_cast<double*>(pr.vstage.p);
+        s.v_host = true;
+        if (!v_zero) e = cudaMemcpyAsync(s.V, V, vb, cudaMemcpyHostToDevice, pr.stream);
+    }
+    if (e == cudaSuccess && v_zero) e = cudaMemsetAsync(s.V, 0, vb, pr.stream);
+    if (pi) {
+        if (is_device_ptr(pi)) {
+            s.pi = pi;
+        } else {
+            if (pr.pistage.ensure(pb) != cudaSuccess) return fail(RMB_ERR_OOM, "pi staging allocation failed");
+            s.pi = static_cast<int32_t*>(pr.pistage.p);
+            s.pi_host = true;
+            if (e == cudaSuccess && copy_pi_in) e = cudaMemcpyAsync(s.pi, pi, pb, cudaMemcpyHostToDevice, pr.stream);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "stage in");
+    return RMB_OK;
+}
+
+static rmb_status stage_out(Problem& pr, void* V, int32_t* pi, const Staged& s)
+{
+    cudaError_t e = cudaSuccess;
+    if (s.v_host) e = cudaMemcpyAsync(V, s.V, (size_t)pr.n * 8, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess && s.pi_host && pi)
+        e = cudaMemcpyAsync(pi, s.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "stage out");
+    return RMB_OK;
+}
+
+static rmb_status copy_trace(Problem& pr, double* host, const double* dev, int64_t cnt)
+{
+    if (!host || cnt <= 0) return RMB_OK;
+    cudaError_t e = cudaMemcpyAsync(host, dev, (size_t)cnt * 8, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "trace copy");
+    return RMB_OK;
+}
+
+static void fill_stats(rmb_stats* st, const SolveResult& r, rmb_status s)
+{
+    if (!st) return;
+    st->sweeps = r.sweeps;
+    st->batches = r.batches;
+    st->outer_iters = r.outer;
+    st->final_residual = r.final_resid;
+    st->seconds = r.ms * 1e-3;
+    st->converged = r.status == RMB_OK;
+    st->status = s;
+}
+
+}  // namespace rmb
+
+using namespace rmb;
+
+// ===================================================================== ABI
+extern "C" {
+
+const char* rmb_version(void) { return "rmb 0.1 (sm_100a)"; }
+
+const char* rmb_last_error(void) { return g_err.c_str(); }
+
+const char* rmb_status_string(rmb_status s)
+{
+    switch (s) {
+    case RMB_OK: return "RMB_OK";
+    case RMB_ERR_INVALID_ARG: return "RMB_ERR_INVALID_ARG";
+    case RMB_ERR_INVALID_MDP: return "RMB_ERR_INVALID_MDP";
+    case RMB_ERR_NOT_CONVERGED: return "RMB_ERR_NOT_CONVERGED";
+    case RMB_ERR_NONFINITE: return "RMB_ERR_NONFINITE";
+    case RMB_ERR_CUDA: return "RMB_ERR_CUDA";
+    case RMB_ERR_NCCL: return "RMB_ERR_NCCL";
+    case RMB_ERR_OOM: return "RMB_ERR_OOM";
+    case RMB_ERR_UNSUPPORTED: return "RMB_ERR_UNSUPPORTED";
+    }
+    return "RMB_ERR_UNKNOWN";
+}
+
+rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, uint32_t flags, rmb_problem* out)
+{
+    g_err.clear();
+    if (!out) return fail(RMB_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    rmb_status s = check_desc(desc);
+    if (s != RMB_OK) return s;
+    if (!P || !c) return fail(RMB_ERR_INVALID_ARG, "P or c is NULL");
+    Problem* pr = new Problem();
+    s = init_problem(*pr, desc);
+    const size_t psz = desc->p_dtype == RMB_F32 ? 4 : 8;
+    const size_t pbytes = (size_t)pr->n * pr->A * pr->n * psz;
+    if (s == RMB_OK) s = device_view(*pr, P, pbytes, &pr->P, "copy P to device");
+    if (s == RMB_OK) s = device_view(*pr, c, (size_t)pr->n * pr->A * psz, &pr->c, "copy c to device");
+    pr->dense = true;
+    if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
+    if (s != RMB_OK) {
+        free_problem(pr);
+        return s;
+    }
+    *out = reinterpret_cast<rmb_problem>(pr);
+    return RMB_OK;
+}
+
+rmb_status rmb_create_csr(const rmb_desc* desc, const int64_t* row_ptr, const int32_t* col, const void* val,
+                          const void* c, uint32_t flags, rmb_problem* out)
+{
+    g_err.clear();
+    if (!out) return fail(RMB_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    rmb_status s = check_desc(desc);
+    if (s != RMB_OK) return s;
+    if (!row_ptr || !col || !val || !c) return fail(RMB_ERR_INVALID_ARG, "row_ptr, col, val or c is NULL");
+    Problem* pr = new Problem();
+    s = init_problem(*pr, desc);
+    pr->dense = false;
+    const int64_t rows = pr->n * pr->A;
+    const size_t psz = desc->p_dtype == RMB_F32 ? 4 : 8;
+    // row_ptr is inspected on the host (nnz, fixed stride -> ELL)
+    std::vector<int64_t> rp;
+    if (s == RMB_OK) {
+        rp.resize((size_t)rows + 1);
+        cudaError_t e = cudaMemcpy(rp.data(), row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyDefault);
+        if (e != cudaSuccess) s = cuda_fail(e, "read row_ptr");
+    }
+    if (s == RMB_OK) {
+        if (rp[0] != 0) s = fail(RMB_ERR_INVALID_ARG, "row_ptr[0] != 0");
+        for (int64_t r = 0; s == RMB_OK && r < rows; ++r)
+            if (rp[r + 1] < rp[r]) s = fail(RMB_ERR_INVALID_ARG, "row_ptr is not nondecreasing");
+    }
+    if (s == RMB_OK) {
+        pr->nnz = rp[rows];
+        const int64_t K = rows > 0 ? rp[1] - rp[0] : 0;
+        bool ell = K > 0;
+        for (int64_t r = 0; ell && r <= rows; ++r) ell = rp[r] == r * K;
+        pr->ell_K = ell ? (int)K : 0;
+    }
+    if (s == RMB_OK) s = device_view(*pr, row_ptr, (rows + 1) * sizeof(int64_t), (const void**)&pr->row_ptr, "copy row_ptr");
+    if (s == RMB_OK) s = device_view(*pr, col, (size_t)pr->nnz * 4, (const void**)&pr->col, "copy col");
+    if (s == RMB_OK) s = device_view(*pr, val, (size_t)pr->nnz * psz, &pr->val, "copy val");
+    if (s == RMB_OK) s = device_view(*pr, c, (size_t)rows * psz, &pr->c, "copy c");
+    if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
+    if (s != RMB_OK) {
+        free_problem(pr);
+        return s;
+    }
+    *out = reinterpret_cast<rmb_problem>(pr);
+    return RMB_OK;
+}
+
+rmb_status rmb_destroy(rmb_problem h)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem* pr = reinterpret_cast<Problem*>(h);
+    cudaStreamSynchronize(pr->stream);
+    free_problem(pr);
+    return RMB_OK;
+}
+
+int64_t rmb_last_launch_count(rmb_problem h)
+{
+    return h ? reinterpret_cast<Problem*>(h)->last_launches : 0;
+}
+
+rmb_status rmb_last_phase_times(rmb_problem h, int64_t* ns4)
+{
+    if (!h || !ns4) return fail(RMB_ERR_INVALID_ARG, "handle or ns4 is NULL");
+    const Problem* pr = reinterpret_cast<const Problem*>(h);
+    for (int i = 0; i < 4; ++i) ns4[i] = pr->prof[i];
+    return RMB_OK;
+}
+
+rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t max_sweeps, uint32_t flags, void* V,
+                  int32_t* pi, double* trace, rmb_stats* stats)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (b < 1 || b > pr.n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
+    if (!(eps > 0.0) || !std::isfinite(eps)) return fail(RMB_ERR_INVALID_ARG, "eps must be finite and > 0");
+    if (max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "max_sweeps < 1");
+    if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    Staged sg;
+    rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, false, sg);
+    if (s != RMB_OK) return s;
+    if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
+    SolveRequest rq;
+    rq.mode = MODE_VI;
+    rq.b = b;
+    rq.seed = seed;
+    rq.k0 = 1;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = eps;
+    rq.max_iter = max_sweeps;
+    rq.V = sg.V;
+    rq.pi = sg.pi;
+    SolveResult r;
+    s = solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
+    if (s != RMB_OK) return s;
+    s = stage_out(pr, V, pi, sg);
+    if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.sweeps);
+    if (s != RMB_OK) return s;
+    rmb_status ret = (rmb_status)r.status;
+    if (ret == RMB_ERR_NOT_CONVERGED) g_err = "max_sweeps reached before r_k <= eps";
+    if (ret == RMB_ERR_NONFINITE) g_err = "a backup produced a non-finite value";
+    fill_stats(stats, r, ret);
+    return ret;
+}
+
+rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double eps, int64_t max_outer, uint32_t flags,
+                   void* V, int32_t* pi, double* trace, int64_t* changed, rmb_stats* stats)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (b < 1 || b > pr.n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
+    if (m < 1) return fail(RMB_ERR_INVALID_ARG, "m < 1");
+    if (!(eps > 0.0) || !std::isfinite(eps)) return fail(RMB_ERR_INVALID_ARG, "eps must be finite and > 0");
+    if (max_outer < 1) return fail(RMB_ERR_INVALID_ARG, "max_outer < 1");
+    if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    const bool pi_given = flags & RMB_PI_GIVEN;
+    Staged sg;
+    rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
+    if (s != RMB_OK) return s;
+    if (pi_given) {  // validate the given policy on the host side of the copy
+        std::vector<int32_t> hp((size_t)pr.n);
+        cudaError_t e = cudaMemcpyAsync(hp.data(), sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+        if (e != cudaSuccess) return cuda_fail(e, "read pi");
+        for (int32_t a : hp)
+            if (a < 0 || a >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
+    }
+    const int64_t tl = max_outer * (int64_t)(m + 1);
+    if (pr.trace.ensure((size_t)tl * 8) != cudaSuccess || pr.chg.ensure((size_t)max_outer * 8) != cudaSuccess)
+        return fail(RMB_ERR_OOM, "trace allocation failed");
+    SolveRequest rq;
+    rq.mode = MODE_MPI;
+    rq.b = b;
+    rq.msweeps = m;
+    rq.seed = seed;
+    rq.k0 = 1;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = eps;
+    rq.max_iter = max_outer;
+    rq.pi_given = pi_given;
+    rq.V = sg.V;
+    rq.pi = sg.pi;
+    SolveResult r;
+    s = solve(pr, rq, static_cast<double*>(pr.trace.p), tl, static_cast<long long*>(pr.chg.p), max_outer, &r);
+    if (s != RMB_OK) return s;
+    s = stage_out(pr, V, pi, sg);
+    if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.outer * (int64_t)(m + 1));
+    if (s == RMB_OK && changed && r.outer > 0) {
+        cudaError_t e = cudaMemcpy(changed, pr.chg.p, (size_t)r.outer * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) s = cuda_fail(e, "changed copy");
+    }
+    if (s != RMB_OK) return s;
+    rmb_status ret = (rmb_status)r.status;
+    if (ret == RMB_ERR_NOT_CONVERGED) g_err = "max_outer reached before the policy was stable with ||TV-V|| <= eps";
+    if (ret == RMB_ERR_NONFINITE) g_err = "a backup produced a non-finite value";
+    fill_stats(stats, r, ret);
+    return ret;
+}
+
+rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uint32_t flags, const int32_t* pi_or_null,
+                     const void* V_in, void* V_out, int32_t* argmin_out, double* resid_out)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (b < 1 || b > pr.n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
+    if (sweep < 1) return fail(RMB_ERR_INVALID_ARG, "sweep < 1");
+    if (!V_in || !V_out) return fail(RMB_ERR_INVALID_ARG, "V_in or V_out is NULL");
+    const size_t vb = (size_t)pr.n * 8, pb = (size_t)pr.n * 4;
+    cudaError_t e = cudaSuccess;
+    // working V on device: V_out if device, else staging
+    const bool out_dev = is_device_ptr(V_out);
+    double* Vw;
+    if (out_dev) {
+        Vw = static_cast<double*>(V_out);
+    } else {
+        if (pr.vstage.ensure(vb) != cudaSuccess) return fail(RMB_ERR_OOM, "V staging allocation failed");
+        Vw = static_cast<double*>(pr.vstage.p);
+    }
+    if (V_in != (const void*)Vw) e = cudaMemcpyAsync(Vw, V_in, vb, cudaMemcpyDefault, pr.stream);
+    // policy / argmin buffer on device
+    if (pr.pistage.ensure(pb) != cudaSuccess) return fail(RMB_ERR_OOM, "pi staging allocation failed");
+    int32_t* pw = nullptr;
+    if (pi_or_null) {
+        if (is_device_ptr(pi_or_null)) {
+            pw = const_cast<int32_t*>(pi_or_null);
+        } else {
+            pw = static_cast<int32_t*>(pr.pistage.p);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(pw, pi_or_null, pb, cudaMemcpyHostToDevice, pr.stream);
+        }
+    } else if (argmin_out) {
+        pw = is_device_ptr(argmin_out) ? argmin_out : static_cast<int32_t*>(pr.pistage.p);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rmb_apply staging");
+    if (pr.trace.ensure(64) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
+    SolveRequest rq;
+    rq.mode = pi_or_null ? MODE_APPLY_PI : MODE_APPLY;
+    rq.b = b;
+    rq.seed = seed;
+    rq.k0 = sweep;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = -1.0;
+    rq.max_iter = 1;
+    rq.V = Vw;
+    rq.pi = pw;
+    SolveResult r;
+    rmb_status s = solve(pr, rq, static_cast<double*>(pr.trace.p), 1, nullptr, 0, &r);
+    if (s != RMB_OK) return s;
+    if (!out_dev) e = cudaMemcpyAsync(V_out, Vw, vb, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess && argmin_out && argmin_out != pw)
+        e = cudaMemcpyAsync(argmin_out, pw, pb, cudaMemcpyDefault, pr.stream);
+    double rr = 0.0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&rr, pr.trace.p, 8, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "rmb_apply copy out");
+    if (resid_out) *resid_out = rr;
+    if (r.status == RMB_ERR_NONFINITE) g_err = "a backup produced a non-finite value";
+    return (rmb_status)r.status;
+}
+
+rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellman_resid, int64_t* changed)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    Staged sg;
+    rmb_status s = stage_in(pr, const_cast<void*>(V), pi, false, true, sg);
+    if (s != RMB_OK) return s;
+    if (pr.trace.ensure(64) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
+    SolveRequest rq;
+    rq.mode = MODE_IMPROVE;
+    rq.b = pr.n;
+    rq.identity = true;
+    rq.V = sg.V;
+    rq.pi = sg.pi;
+    SolveResult r;
+    s = solve(pr, rq, static_cast<double*>(pr.trace.p), 1, nullptr, 0, &r);
+    if (s != RMB_OK) return s;
+    cudaError_t e = cudaSuccess;
+    if (sg.pi_host) e = cudaMemcpyAsync(pi, sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "rmb_improve copy out");
+    if (bellman_resid) *bellman_resid = r.final_resid;
+    if (changed) *changed = r.changed;
+    return (rmb_status)r.status;
+}
+
+rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm)
+{
+    g_err.clear();
+    if (n < 1 || n > 0xffffffffLL || !perm) return fail(RMB_ERR_INVALID_ARG, "n out of range or perm NULL");
+    if (flags & RMB_ORDER_IDENTITY) {
+        for (int64_t p = 0; p < n; ++p) perm[p] = (uint32_t)p;
+        return RMB_OK;
+    }
+    Permutation pm;
+    pm.init(n, seed, sweep);
+    for (int64_t p = 0; p < n; ++p) perm[p] = (uint32_t)pm((uint64_t)p);
+    return RMB_OK;
+}
+
+rmb_status rmb_partition_device(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm, void* stream)
+{
+    g_err.clear();
+    if (n < 1 || n > 0xffffffffLL || !perm) return fail(RMB_ERR_INVALID_ARG, "n out of range or perm NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = launch_partition(n, seed, sweep, flags & RMB_ORDER_IDENTITY, perm, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "rmb_partition_device");
+    return RMB_OK;
+}
+
+}  // extern "C"

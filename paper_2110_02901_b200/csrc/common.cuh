@@ -1,0 +1,122 @@
+// common.cuh — device helpers shared by the rmb kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rmb {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- loads
+// P rows are streamed exactly once per sweep: bypass L1 allocation.
+__device__ __forceinline__ float4 ld_stream(const float4* p)
+{
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p)
+{
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float ld_stream(const float* p)
+{
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ld_stream(const double* p)
+{
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
+// ------------------------------------------------------------ grid barrier
+// Sense-free monotonic barrier for a co-resident (cooperative) grid.
+// bar[0] = arrival counter, bar[32] = released epoch (separate 256-B lines).
+// Both zeroed by the host before the launch; each CTA keeps its own epoch.
+struct GridBarrier {
+    unsigned long long* arrive;
+    unsigned long long* release;
+    unsigned long long epoch;
+    unsigned long long nblocks;
+    int* error_flag;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Hang guard: a barrier that waits more than 30 s means a broken grid
+// (not all CTAs resident); trap instead of wedging the GPU.
+__device__ __forceinline__ void grid_sync(GridBarrier& g)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        g.epoch += 1;
+        const unsigned long long target = g.epoch * g.nblocks;
+        __threadfence();
+        unsigned long long v = atomicAdd(g.arrive, 1ULL) + 1ULL;
+        if (v == target) {
+            st_release_gpu(g.release, g.epoch);
+        } else {
+            unsigned long long t0 = 0;
+            unsigned spins = 0;
+            while (ld_acquire_gpu(g.release) < g.epoch) {
+                if (++spins == 4096u) {
+                    spins = 0;
+                    unsigned long long t = globaltimer_ns();
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > 30ull * 1000000000ull) {
+                        atomicExch(g.error_flag, 1);
+                        __trap();
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// (value, index) argmin within aligned groups of G lanes; ties -> lower index.
+template <int G>
+__device__ __forceinline__ void group_argmin(double& v, int& a)
+{
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int oa = __shfl_xor_sync(0xffffffffu, a, o);
+        if (ov < v || (ov == v && oa < a)) {
+            v = ov;
+            a = oa;
+        }
+    }
+}
+
+}  // namespace rmb

@@ -1,0 +1,734 @@
+// dense.cu — persistent sm_100a solver for DENSE MDPs (P [n][A][n]).
+//
+// One cooperative launch runs a whole MB-VI or MB-MPI solve (PAPER.md P:L186,
+// Alg. 1): every batch, every sweep and the stopping test, with no
+// host round trip.  Design:
+//
+//  * Each CTA (one per SM, 512 threads) keeps the interim value function V
+//    (fp64) resident in shared memory for the whole solve, plus pi for MPI.
+//  * Batch t of sweep k = positions [t*b, min(n,(t+1)*b)) of the permutation
+//    pi_k (partition.cuh; perm of sweep k+1 is generated during sweep k).
+//  * COMPUTE: the batch's rows are cut into items (state, 4 actions, column
+//    chunk); items are dealt to CTAs round-robin (per-SM balance within one
+//    item) and to warps through a shared-memory counter.  A warp streams its
+//    4 P-row chunks with 128-bit L1::no_allocate loads (each P byte read once
+//    per sweep) and dots them with the smem V in fp64.
+//      - C == 1 (rows not split): the warp finishes the backup itself:
+//        Q = c + gamma * dot per action, and writes the group's (min Q, argmin).
+//      - C > 1 (small b, rows split to fill 148 SMs): fp64 partial sums per
+//        (state, action, chunk).
+//  * BARRIER: one grid barrier per batch ("the batch is written back before
+//    the next batch starts").
+//  * COMBINE: per state, sum partials in chunk order / take the min over the
+//    action groups in order (lowest index on exact ties), residual |Q - V_old|
+//    and the smem patch of V.  Small partial volumes: every CTA reduces all
+//    states itself (redundant, no second barrier).  Large: CTA x reduces the
+//    states i = x mod grid into a list, a second barrier, every CTA patches.
+//    Every CTA ends each batch with an identical V, residual and stop decision.
+//  * Reads within a batch see only pre-batch values (Eq. 12: S \ M(i) with J,
+//    M(i) with B J): smem V is patched only after the batch's barrier.
+//  * Reduction order is a function of (n, b, mode) only: bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+#include "partition.cuh"
+
+namespace rmb {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / kWarp;
+constexpr int kAG = 4;                     // actions per compute item (min modes)
+constexpr int64_t kRedundantMax = 8192;    // doubles of batch partials reduced by every CTA
+
+struct Plan {
+    int Lc;         // chunk length (elements)
+    int C;          // chunks per row
+    int redundant;  // 1: every CTA reduces every state (single barrier)
+};
+
+struct DenseArgs {
+    const void* P;
+    const void* c;
+    int64_t n;
+    int A;
+    double gamma;
+    double* V;
+    int32_t* pi;
+    int64_t b;
+    uint64_t seed;
+    int64_t k0;
+    int identity;
+    int mode;
+    int pi_given;
+    double eps;
+    int64_t max_iter;
+    int msweeps;
+    Plan plan[3];        // 0 = B_b sweep, 1 = B_{pi,b} sweep, 2 = improvement
+    int64_t imp_sub;     // improvement sub-batch (states)
+    uint32_t* perm;      // 3 * n (triple-buffered by sweep index)
+    double* part;        // 2 * part_stride
+    int64_t part_stride;
+    double* lval;        // distributed-combine list: value per batch position
+    int32_t* larg;       //                           argmin per batch position
+    unsigned long long* bar;
+    int* err;
+    double* trace;
+    int64_t trace_len;
+    long long* chg;
+    int64_t chg_len;
+    long long* out;
+    unsigned int* wctr;  // [2] work-stealing counters (phase parity)
+    int64_t qs_cap;      // doubles of smem scratch for S-mode reductions
+    int64_t qs_off;      // byte offset of that scratch in dynamic smem
+    long long* prof;     // [0] compute ns, [1] barrier ns, [2] combine ns, [3] barriers (CTA 0)
+};
+
+// ---------------------------------------------------------------- loads
+template <typename PT, int VE>
+struct Vec;
+template <>
+struct Vec<float, 4> {
+    using T = float4;
+    __device__ static __forceinline__ void get(const T& x, double (&d)[4])
+    {
+        d[0] = x.x, d[1] = x.y, d[2] = x.z, d[3] = x.w;
+    }
+};
+template <>
+struct Vec<double, 2> {
+    using T = double2;
+    __device__ static __forceinline__ void get(const T& x, double (&d)[2]) { d[0] = x.x, d[1] = x.y; }
+};
+template <>
+struct Vec<float, 1> {
+    using T = float;
+    __device__ static __forceinline__ void get(const T& x, double (&d)[1]) { d[0] = x; }
+};
+template <>
+struct Vec<double, 1> {
+    using T = double;
+    __device__ static __forceinline__ void get(const T& x, double (&d)[1]) { d[0] = x; }
+};
+
+template <int VE>
+__device__ __forceinline__ void load_v(const double* Vs, int64_t j, double (&v)[VE])
+{
+    if constexpr (VE == 4) {
+        const double2 a = *reinterpret_cast<const double2*>(Vs + j);
+        const double2 b = *reinterpret_cast<const double2*>(Vs + j + 2);
+        v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    } else if constexpr (VE == 2) {
+        const double2 a = *reinterpret_cast<const double2*>(Vs + j);
+        v[0] = a.x, v[1] = a.y;
+    } else {
+        v[0] = Vs[j];
+    }
+}
+
+// acc[g] += sum_{j in [j0,j1)} P_row_g[j] * Vs[j], lane-strided over VE-vectors,
+// in increasing j order per lane (fixed order -> reproducible).
+template <typename PT, int VE, int NG, int U>
+__device__ __forceinline__ void dot_rows(const PT* __restrict__ row0, int64_t n, int na, int64_t j0,
+                                         int64_t j1, const double* Vs, int lane, double (&acc)[NG])
+{
+    using VT = typename Vec<PT, VE>::T;
+    const int64_t nvec = (j1 - j0) / VE;  // j0, j1 multiples of VE
+    const VT* rows[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) rows[g] = reinterpret_cast<const VT*>(row0 + (int64_t)g * n + j0);
+    for (int64_t v = lane; v < nvec; v += kWarp * U) {
+        VT x[U][NG];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vv = v + (int64_t)kWarp * u;
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                if (g < na && vv < nvec) x[u][g] = ld_stream(rows[g] + vv);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vv = v + (int64_t)kWarp * u;
+            if (vv < nvec) {
+                double vs[VE];
+                load_v<VE>(Vs, j0 + vv * VE, vs);
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (g < na) {
+                        double p[VE];
+                        Vec<PT, VE>::get(x[u][g], p);
+#pragma unroll
+                        for (int e = 0; e < VE; ++e) acc[g] = fma(p[e], vs[e], acc[g]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <typename PT>
+__device__ __forceinline__ double load_cost(const DenseArgs& a, int64_t idx)
+{
+    return (double)__ldg(static_cast<const PT*>(a.c) + idx);
+}
+
+// ------------------------------------------------------------ compute phase
+// EVAL: rows (s, pi(s)); else rows (s, a) for all a in groups of kAG.
+// states: perm[lo + i] (perm != null) or lo + i; i < cnt.
+// Output layout (per batch position i):
+//   C == 1, EVAL: part[i] = Q                  (per_state = 1)
+//   C == 1, min : part[2(i*NAG+ag)+{0,1}] = (min Q over the group, argmin)   (2*NAG)
+//   C >  1, EVAL: part[i*C + ch]               (C)
+//   C >  1, min : part[(i*A + a)*C + ch]       (A*C)
+template <typename PT, int VE, bool EVAL>
+__device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
+                              int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
+{
+    const int lane = threadIdx.x & 31;
+    const int C = pl.C;
+    const int64_t Lc = pl.Lc;
+    const int NAG = EVAL ? 1 : (a.A + kAG - 1) / kAG;
+    const int64_t per_state = (int64_t)NAG * C;
+    const int64_t items = cnt * per_state;
+    const PT* P = static_cast<const PT*>(a.P);
+    constexpr int NG = EVAL ? 1 : kAG;
+    constexpr int U = EVAL ? 8 : 2;
+    // dynamic work stealing over the whole grid (balances SMs whose HBM share
+    // differs); the next item index is fetched while the current one streams
+    auto grab = [&]() -> int64_t {
+        unsigned int r = 0;
+        if (lane == 0) r = atomicAdd(ctr, 1u);
+        return (int64_t)__shfl_sync(0xffffffffu, r, 0);
+    };
+    int64_t it = grab();
+    while (it < items) {
+        const int64_t it_next = grab();
+        const int64_t i = it / per_state;
+        const int rr = (int)(it - i * per_state);
+        const int ag = rr / C;
+        const int ch = rr - ag * C;
+        const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+        const int a0 = EVAL ? pis[s] : ag * kAG;
+        const int na = EVAL ? 1 : min(kAG, a.A - a0);
+        const int64_t j0 = (int64_t)ch * Lc;
+        const int64_t j1 = min(a.n, j0 + Lc);
+        double acc[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) acc[g] = 0.0;
+        dot_rows<PT, VE, NG, U>(P + ((int64_t)s * a.A + a0) * a.n, a.n, na, j0, j1, Vs, lane, acc);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) acc[g] = warp_sum(acc[g]);
+        if (C == 1) {
+            if (lane == 0) {
+                if (EVAL) {
+                    part[i] = load_cost<PT>(a, s * a.A + a0) + a.gamma * acc[0];
+                } else {
+                    double best = 0.0;
+                    int barg = a0;
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        if (g < na) {
+                            const double Q = load_cost<PT>(a, s * a.A + a0 + g) + a.gamma * acc[g];
+                            if (g == 0 || Q < best) best = Q, barg = a0 + g;
+                        }
+                    }
+                    part[2 * (i * NAG + ag)] = best;
+                    part[2 * (i * NAG + ag) + 1] = (double)barg;
+                }
+            }
+        } else if (EVAL) {
+            if (lane == 0) part[i * C + ch] = acc[0];
+        } else {
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                if (lane == g && g < na) part[(i * a.A + a0 + g) * C + ch] = acc[g];
+        }
+        it = it_next;
+    }
+}
+
+struct PhaseAcc {
+    double rmax;
+    int bad;
+    long long changed;
+};
+
+// ------------------------------------------------- per-state reductions
+// F-mode (C == 1): one thread per state.
+template <bool EVAL>
+__device__ __forceinline__ void reduce_state_F(const DenseArgs& a, const double* part, int64_t i, double& best,
+                                               int& barg)
+{
+    if (EVAL) {
+        best = __ldcg(part + i);
+        barg = -1;
+        return;
+    }
+    const int NAG = (a.A + kAG - 1) / kAG;
+    const double2* pp = reinterpret_cast<const double2*>(part) + i * NAG;
+    best = 0.0;
+    barg = 0;
+    for (int ag = 0; ag < NAG; ++ag) {
+        const double2 q = __ldcg(pp + ag);
+        if (ag == 0 || q.x < best) best = q.x, barg = (int)q.y;
+    }
+}
+
+// S-mode (C > 1): the CTA reduces the states i = first + k*step (k < m):
+// warp per (state, action) sums its C partials (lane-strided, then a fixed
+// butterfly), Q = c + gamma*sum goes to smem Qs, then a thread per state takes
+// the argmin over actions in index order (lowest index on ties).  sink(i, s,
+// v, arg) is called by exactly one thread per state.
+template <typename PT, bool EVAL, typename Sink>
+__device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double* part, int C, const uint32_t* perm,
+                                                int64_t lo, int64_t cnt, int64_t first, int64_t step,
+                                                const int32_t* pis, double* Qs, Sink&& sink)
+{
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int Ae = EVAL ? 1 : a.A;
+    if (first >= cnt) return;
+    const int64_t m_all = (cnt - first + step - 1) / step;
+    const int64_t per_round = max((int64_t)1, a.qs_cap / Ae);
+    for (int64_t k0 = 0; k0 < m_all; k0 += per_round) {
+        const int64_t m = min(per_round, m_all - k0);
+        for (int64_t q = warp; q < m * Ae; q += kWarps) {
+            const int64_t kk = q / Ae;
+            const int ai = (int)(q - kk * Ae);
+            const int64_t i = first + (k0 + kk) * step;
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+            const int act = EVAL ? pis[s] : ai;
+            const double* pp = part + (EVAL ? i : i * a.A + act) * C;
+            double sum = 0.0;
+            for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + ch);
+            sum = warp_sum(sum);
+            if (lane == 0) Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
+        }
+        __syncthreads();
+        for (int64_t kk = threadIdx.x; kk < m; kk += kThreads) {
+            const int64_t i = first + (k0 + kk) * step;
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+            double best = Qs[kk * Ae];
+            int barg = EVAL ? pis[s] : 0;
+            if (!EVAL)
+                for (int act = 1; act < a.A; ++act) {
+                    const double Q = Qs[kk * Ae + act];
+                    if (Q < best) best = Q, barg = act;
+                }
+            sink(i, s, best, barg);
+        }
+        __syncthreads();
+    }
+}
+
+// Apply a state's new value to this CTA's smem copy (KIND 0: B_b, 1: B_pi,b,
+// 2: improvement).  CTA 0 also writes the global outputs.
+template <int KIND>
+__device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int32_t* pis, int64_t s, double v, int arg,
+                                            PhaseAcc& acc)
+{
+    const double old = Vs[s];
+    acc.rmax = fmax(acc.rmax, fabs(v - old));
+    acc.bad |= !isfinite(v);
+    const bool writer = blockIdx.x == 0;
+    if (KIND == 2) {
+        acc.changed += (arg != pis[s]);
+        pis[s] = arg;
+        if (writer) a.pi[s] = arg;
+    } else {
+        Vs[s] = v;
+        if (writer) {
+            a.V[s] = v;
+            if (KIND == 0 && a.pi) a.pi[s] = arg;
+        }
+    }
+}
+
+struct Ctx {
+    GridBarrier g;
+    long long phase;  // running compute/combine phase counter (partial buffer parity)
+    int64_t batches;
+    unsigned long long t_mark;
+    long long t_comp, t_bar, t_comb, n_bar;
+};
+
+__device__ __forceinline__ void prof_mark(Ctx& x, long long* slot)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long t = globaltimer_ns();
+        *slot += (long long)(t - x.t_mark);
+        x.t_mark = t;
+    }
+}
+
+__device__ __forceinline__ void timed_sync(Ctx& x)
+{
+    prof_mark(x, &x.t_comp);
+    grid_sync(x.g);
+    prof_mark(x, &x.t_bar);
+    x.n_bar++;
+}
+
+// One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
+template <typename PT, int VE, int KIND>
+__device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
+                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
+{
+    constexpr bool EVAL = KIND == 1;
+    double* part = a.part + (x.phase & 1) * a.part_stride;
+    // the other parity's work counter was last used before the previous
+    // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
+    compute_phase<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+    if (fill_next_k > 0) {  // next sweep's order, off the critical path
+        Permutation pm;
+        pm.init(a.n, a.seed, fill_next_k);
+        uint32_t* dst = a.perm + (fill_next_k % 3) * a.n;
+        const int64_t stride = (int64_t)gridDim.x * kThreads;
+        for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < a.n; p += stride)
+            dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+    timed_sync(x);
+    const bool F = pl.C == 1;
+    auto patch = [&](int64_t, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, s, v, arg, acc); };
+    auto to_list = [&](int64_t i, int64_t, double v, int arg) {
+        a.lval[i] = v;
+        a.larg[i] = arg;
+    };
+    if (pl.redundant) {
+        if (F) {
+            for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
+                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                double v;
+                int arg;
+                reduce_state_F<EVAL>(a, part, i, v, arg);
+                patch_state<KIND>(a, Vs, pis, s, v, arg, acc);
+            }
+        } else {
+            reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, 0, 1, pis, Qs, patch);
+        }
+    } else {
+        // distributed: CTA x reduces states i = x mod grid into the list
+        const int64_t G = gridDim.x;
+        if (F) {
+            for (int64_t i = blockIdx.x + (int64_t)threadIdx.x * G; i < cnt; i += (int64_t)kThreads * G) {
+                double v;
+                int arg;
+                reduce_state_F<EVAL>(a, part, i, v, arg);
+                a.lval[i] = v;
+                a.larg[i] = arg;
+            }
+        } else {
+            reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, blockIdx.x, G, pis, Qs, to_list);
+        }
+        timed_sync(x);
+        for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+            patch_state<KIND>(a, Vs, pis, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
+        }
+    }
+    __syncthreads();
+    prof_mark(x, &x.t_comb);
+    ++x.phase;
+}
+
+// block-wide reduction of a PhaseAcc; every thread receives the result
+__device__ PhaseAcc block_reduce(PhaseAcc v)
+{
+    __shared__ double sd[kWarps];
+    __shared__ int si[kWarps];
+    __shared__ long long sl[kWarps];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.rmax = fmax(v.rmax, __shfl_xor_sync(0xffffffffu, v.rmax, o));
+        v.bad |= __shfl_xor_sync(0xffffffffu, v.bad, o);
+        v.changed += __shfl_xor_sync(0xffffffffu, v.changed, o);
+    }
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sd[w] = v.rmax, si[w] = v.bad, sl[w] = v.changed;
+    __syncthreads();
+    PhaseAcc r{0.0, 0, 0};
+    for (int k = 0; k < kWarps; ++k) r.rmax = fmax(r.rmax, sd[k]), r.bad |= si[k], r.changed += sl[k];
+    __syncthreads();
+    return r;
+}
+
+// One application of B_b (EVAL = false) or B_{pi,b} (EVAL = true), sweep k.
+template <typename PT, int VE, bool EVAL>
+__device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, int64_t k, double* Qs)
+{
+    const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
+    const Plan& pl = a.plan[EVAL ? 1 : 0];
+    PhaseAcc acc{0.0, 0, 0};
+    for (int64_t lo = 0; lo < a.n; lo += a.b) {
+        const int64_t cnt = min(a.b, a.n - lo);
+        run_batch<PT, VE, EVAL ? 1 : 0>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
+                                         (lo == 0 && !a.identity) ? k + 1 : 0);
+        ++x.batches;
+    }
+    return block_reduce(acc);
+}
+
+template <typename PT, int VE>
+__device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, double* Qs)
+{
+    PhaseAcc acc{0.0, 0, 0};
+    for (int64_t lo = 0; lo < a.n; lo += a.imp_sub) {
+        const int64_t cnt = min(a.imp_sub, a.n - lo);
+        run_batch<PT, VE, 2>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
+    }
+    return block_reduce(acc);
+}
+
+template <typename PT, int VE>
+__global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* Vs = reinterpret_cast<double*>(smem_raw);
+    const int64_t n_pad = (a.n + 1) & ~int64_t(1);
+    int32_t* pis = reinterpret_cast<int32_t*>(Vs + n_pad);
+    double* Qs = reinterpret_cast<double*>(smem_raw + a.qs_off);
+    const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE;
+
+    for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
+        Vs[j] = a.V[j];
+        if (need_pi) pis[j] = a.pi[j];
+    }
+    Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
+    if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
+    if (!a.identity && a.mode != MODE_IMPROVE) {
+        Permutation pm;
+        pm.init(a.n, a.seed, a.k0);
+        uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
+        for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < a.n; p += (int64_t)gridDim.x * kThreads)
+            dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+    timed_sync(x);  // perm of the first sweep visible; also orders the smem loads
+
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    long long status = RMB_ERR_NOT_CONVERGED;
+    int64_t k = a.k0, it = 0, outer = 0;
+    long long changed = 0;
+    double last = 0.0;
+
+    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
+        const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
+        while (it < iters) {
+            PhaseAcc r = a.mode == MODE_APPLY_PI ? run_sweep<PT, VE, true>(a, x, Vs, pis, k, Qs)
+                                                 : run_sweep<PT, VE, false>(a, x, Vs, pis, k, Qs);
+            if (lead && it < a.trace_len) a.trace[it] = r.rmax;
+            ++it;
+            ++k;
+            last = r.rmax;
+            if (r.bad) { status = RMB_ERR_NONFINITE; break; }
+            if (a.eps >= 0.0 && r.rmax <= a.eps) { status = RMB_OK; break; }
+        }
+        if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+    } else if (a.mode == MODE_IMPROVE) {
+        PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+        last = r.rmax;
+        changed = r.changed;
+        status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
+    } else {  // MODE_MPI
+        bool bad = false;
+        if (!a.pi_given) {
+            PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+            bad = r.bad;
+        }
+        while (!bad && outer < a.max_iter) {
+            const int64_t row = outer * (a.msweeps + 1);
+            for (int e = 0; e < a.msweeps && !bad; ++e) {
+                PhaseAcc r = run_sweep<PT, VE, true>(a, x, Vs, pis, k, Qs);
+                if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
+                ++k;
+                ++it;
+                bad = r.bad;
+            }
+            if (bad) { ++outer; break; }
+            PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+            if (lead && row + a.msweeps < a.trace_len) a.trace[row + a.msweeps] = r.rmax;
+            if (lead && outer < a.chg_len) a.chg[outer] = r.changed;
+            ++outer;
+            last = r.rmax;
+            changed = r.changed;
+            if (r.bad) { bad = true; break; }
+            if (r.changed == 0 && r.rmax <= a.eps) { status = RMB_OK; break; }
+        }
+        if (bad) status = RMB_ERR_NONFINITE;
+    }
+    if (lead) {
+        a.out[OUT_SWEEPS] = it;
+        a.out[OUT_OUTER] = outer;
+        a.out[OUT_STATUS] = status;
+        a.out[OUT_RESID_BITS] = __double_as_longlong(last);
+        a.out[OUT_BATCHES] = x.batches;
+        a.out[OUT_CHANGED] = changed;
+        a.prof[0] = x.t_comp;
+        a.prof[1] = x.t_bar;
+        a.prof[2] = x.t_comb;
+        a.prof[3] = x.n_bar;
+    }
+}
+
+// ------------------------------------------------------------------ host
+// rows = (states per batch) x (items per state before chunking)
+static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_eff, int VE, int num_sms,
+                        bool allow_split)
+{
+    const int64_t rows = cnt * groups_per_state;
+    const int64_t unit = (int64_t)kWarp * VE;
+    const int64_t maxC = std::max<int64_t>(1, (n + unit - 1) / unit);
+    int64_t c = 1;
+    // >= 16 items per SM keeps the per-SM imbalance of the round-robin deal
+    // small; below that, split rows into column chunks (up to ~32 per SM)
+    if (allow_split && rows < 16LL * num_sms) c = (32LL * num_sms + rows - 1) / rows;
+    c = std::min(std::max<int64_t>(c, 1), maxC);
+    int64_t L = (n + c - 1) / c;
+    L = (L + unit - 1) / unit * unit;
+    Plan p;
+    p.Lc = (int)L;
+    p.C = (int)((n + L - 1) / L);
+    const int64_t per_state = p.C == 1 ? (A_eff == 1 ? 1 : 2 * groups_per_state) : (int64_t)A_eff * p.C;
+    p.redundant = cnt * per_state <= kRedundantMax ? 1 : 0;
+    return p;
+}
+
+static int64_t plan_doubles(const Plan& p, int64_t cnt, int64_t groups_per_state, int A_eff)
+{
+    return p.C == 1 ? cnt * (A_eff == 1 ? 1 : 2 * groups_per_state) : cnt * A_eff * p.C;
+}
+
+template <typename PT, int VE>
+static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaStream_t st)
+{
+    auto kern = dense_solver_kernel<PT, VE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    void* args[] = {const_cast<DenseArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, st);
+}
+
+rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                       long long* chg_dev, int64_t chg_len, SolveResult* res)
+{
+    const int64_t n = pr.n;
+    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
+    int VE = 16 / psz;
+    if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
+    const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE;
+    const int64_t n_pad = (n + 1) & ~int64_t(1);
+    const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
+    if (smem_v + 2048 > pr.smem_optin) {
+        set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
+                  " B of shared memory for V (limit " + std::to_string(pr.smem_optin) +
+                  "); column panels for larger dense n are not in this build");
+        return RMB_ERR_UNSUPPORTED;
+    }
+
+    DenseArgs a{};
+    a.P = pr.P;
+    a.c = pr.c;
+    a.n = n;
+    a.A = pr.A;
+    a.gamma = pr.gamma;
+    a.V = rq.V;
+    a.pi = rq.pi;
+    a.b = rq.b;
+    a.seed = rq.seed;
+    a.k0 = rq.k0;
+    a.identity = rq.identity ? 1 : 0;
+    a.mode = rq.mode;
+    a.pi_given = rq.pi_given ? 1 : 0;
+    a.eps = rq.eps;
+    a.max_iter = rq.max_iter;
+    a.msweeps = rq.msweeps;
+    const int64_t NAG = (pr.A + kAG - 1) / kAG;
+    const int sms = pr.num_sms;
+    // smem scratch for split-row (S-mode) reductions: up to 32 KB after V / pi
+    a.qs_off = (int64_t)smem_v;
+    a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 2048) / 8);
+    const size_t smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
+    const bool split_ok = a.qs_cap >= pr.A;  // else every row stays whole (C = 1)
+    a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok);
+    a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok);
+    // improvement (no V write): as few sub-batches as a bounded scratch allows
+    a.imp_sub = n * NAG * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(std::min<int64_t>(n, rq.b), (int64_t(1) << 21) / NAG);
+    a.plan[2] = plan_chunks(n, a.imp_sub, NAG, pr.A, VE, sms, split_ok);
+    const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
+                                              plan_doubles(a.plan[1], rq.b, 1, 1),
+                                              plan_doubles(a.plan[2], a.imp_sub, NAG, pr.A)});
+    a.part_stride = (stride + 31) / 32 * 32;
+    const int64_t lcap = std::max<int64_t>(rq.b, a.imp_sub);
+
+    cudaStream_t st = pr.stream;
+    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess ||
+        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)lcap * 12 + 64) != cudaSuccess ||
+        pr.ctrl.ensure(4096) != cudaSuccess) {
+        set_error("dense solver: workspace allocation failed");
+        return RMB_ERR_OOM;
+    }
+    a.perm = static_cast<uint32_t*>(pr.perm.p);
+    a.part = static_cast<double*>(pr.part.p);
+    a.lval = a.part + 2 * a.part_stride;
+    a.larg = reinterpret_cast<int32_t*>(a.lval + lcap);
+    unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
+    a.bar = ctrl;                                      // [0], [32]
+    a.err = reinterpret_cast<int*>(ctrl + 64);         // [64]
+    a.out = reinterpret_cast<long long*>(ctrl + 128);  // [128..136)
+    a.prof = reinterpret_cast<long long*>(ctrl + 192); // [192..196)
+    a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256); // [256]
+    a.trace = trace_dev;
+    a.trace_len = trace_len;
+    a.chg = chg_dev;
+    a.chg_len = chg_len;
+
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    if (ce == cudaSuccess) {
+        if (pr.pdt == RMB_F32)
+            ce = VE == 4 ? launch_typed<float, 4>(a, smem, sms, st) : launch_typed<float, 1>(a, smem, sms, st);
+        else
+            ce = VE == 2 ? launch_typed<double, 2>(a, smem, sms, st) : launch_typed<double, 1>(a, smem, sms, st);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
+    long long out[OUT_N + 8] = {0};
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) {
+        set_error(std::string("dense solver: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    res->sweeps = out[OUT_SWEEPS];
+    res->outer = out[OUT_OUTER];
+    res->status = (int)out[OUT_STATUS];
+    double d;
+    memcpy(&d, &out[OUT_RESID_BITS], 8);
+    res->final_resid = d;
+    res->batches = out[OUT_BATCHES];
+    res->changed = out[OUT_CHANGED];
+    res->ms = ms;
+    res->launches = 1;
+    for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
+    pr.last_launches = 1;
+    return RMB_OK;
+}
+
+}  // namespace rmb

@@ -1,0 +1,115 @@
+// internal.h — library-internal types shared by the ABI layer and kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rmb.h"
+
+namespace rmb {
+
+enum Mode : int {
+    MODE_VI = 0,       // MB-VI: sweeps of B_b to r_k <= eps
+    MODE_MPI = 1,      // MB-MPI: Algorithm 1 with B_{pi,b} evaluation
+    MODE_APPLY = 2,    // one application of B_b
+    MODE_APPLY_PI = 3, // one application of B_{pi,b}
+    MODE_IMPROVE = 4,  // one policy improvement (greedy, ||TV-V||, changed)
+};
+
+// Device-side result block written by the solver kernels (long long[8]).
+enum OutSlot : int {
+    OUT_SWEEPS = 0,
+    OUT_OUTER = 1,
+    OUT_STATUS = 2,
+    OUT_RESID_BITS = 3,
+    OUT_BATCHES = 4,
+    OUT_CHANGED = 5,
+    OUT_N = 8
+};
+
+struct SolveRequest {
+    int mode = MODE_VI;
+    int64_t b = 1;
+    uint64_t seed = 0;
+    int64_t k0 = 1;          // first sweep index
+    bool identity = false;   // RMB_ORDER_IDENTITY
+    double eps = -1.0;       // < 0: no convergence test
+    int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
+    int msweeps = 1;         // MPI evaluation sweeps per outer iteration
+    bool pi_given = false;
+    double* V = nullptr;     // device [n]
+    int32_t* pi = nullptr;   // device [n] (may be null for APPLY)
+};
+
+struct SolveResult {
+    int64_t sweeps = 0, outer = 0, batches = 0, changed = 0;
+    int status = RMB_OK;
+    double final_resid = 0.0;
+    float ms = 0.f;
+    int launches = 0;
+};
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need)
+    {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Problem {
+    int64_t n = 0;
+    int A = 0;
+    double gamma = 0.0;
+    rmb_dtype pdt = RMB_F32;
+    bool dense = true;
+    // device views (borrowed or owned)
+    const void* P = nullptr;
+    const void* c = nullptr;
+    const int64_t* row_ptr = nullptr;
+    const int32_t* col = nullptr;
+    const void* val = nullptr;
+    int64_t nnz = 0;
+    int ell_K = 0;  // > 0: fixed-stride rows (ELL)
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    int num_sms = 0;
+    size_t smem_optin = 0;
+    std::vector<void*> owned;  // host-staged inputs
+    // workspace
+    DevBuf perm, part, ctrl, trace, chg, vstage, pistage, aux;
+    int64_t last_launches = 0;
+    long long prof[4] = {0, 0, 0, 0};  // last solve: compute / barrier / combine ns (CTA 0), barriers
+};
+
+// dense.cu
+rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                       long long* chg_dev, int64_t chg_len, SolveResult* res);
+// sparse.cu
+rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                        long long* chg_dev, int64_t chg_len, SolveResult* res);
+// gen_kernels.cu
+cudaError_t launch_partition(int64_t n, uint64_t seed, int64_t sweep, bool identity, uint32_t* perm,
+                             cudaStream_t st);
+cudaError_t launch_validate(const Problem& pr, int* bad_dev, cudaStream_t st);
+
+// abi.cu
+void set_error(const std::string& msg);
+
+}  // namespace rmb

@@ -1,0 +1,277 @@
+"""GPU parity: the sm_100a dense path (through the C ABI) vs the CPU oracle.
+
+Tolerances: both sides accumulate in fp64 but in
+different orders, so V agrees to ~n*u*|V|; we require
+  single application: |V_gpu - V_or| <= 1e-11 * max(1, |V|_inf)
+  full solves:        |V_gpu - V_or| <= 1e-9  * max(1, |V|_inf)   (north_star)
+  residual traces:    same bound per sweep, same number of sweeps
+  policies:           bit-exact wherever the oracle's Q-gap exceeds 1e-6 * scale
+  dyadic instances:   bit-exact (every product and sum is exact in fp64)
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+import paper_2110_02901_b200 as rmb
+
+pytestmark = pytest.mark.gpu
+
+
+def tdev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def make(n, A, seed, dtype=np.float64, kind="random", gamma=0.9):
+    P, c = gen.dense(n, A, seed, kind=kind, dtype=dtype)
+    m = oracle.MDP(n, A, gamma, c, P=P)
+    prob = rmb.Problem.dense(tdev(P), tdev(c), gamma)
+    return m, prob, P, c
+
+
+def qgap(m, V):
+    Q = m.c.astype(np.float64) + m.gamma * np.einsum("saj,j->sa", m.to_dense64(), V)
+    if m.A == 1:
+        return np.full(m.n, np.inf)
+    s = np.sort(Q, 1)
+    return (s[:, 1] - s[:, 0]) / np.maximum(1.0, np.abs(s[:, 0]))
+
+
+def assert_close(a, b, rel):
+    scale = max(1.0, float(np.abs(b).max()))
+    assert np.abs(np.asarray(a) - np.asarray(b)).max() <= rel * scale, np.abs(np.asarray(a) - np.asarray(b)).max()
+
+
+# ------------------------------------------------------------ partition
+@pytest.mark.parametrize("n,seed,k", [(1, 0, 1), (3, 1, 2), (50, 42, 7), (10_000, 5, 100), (1_000_000, 7, 3)])
+def test_device_partition_matches_oracle(n, seed, k):
+    d = rmb.partition_device(n, seed, k).cpu().numpy().view(np.uint32)
+    assert np.array_equal(d, oracle.partition(n, seed, k))
+
+
+# ----------------------------------------------------------- generators
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("kind", ["random", "dyadic"])
+def test_device_dense_generator_is_bitwise_host(dtype, kind):
+    Pd, cd = rmb.generate_dense(77, 5, 3, kind=kind, dtype=dtype)
+    Ph, ch = gen.dense(77, 5, 3, kind=kind, dtype=np.float32 if dtype == torch.float32 else np.float64)
+    assert np.array_equal(Pd.cpu().numpy(), Ph) and np.array_equal(cd.cpu().numpy(), ch)
+    Pr, cr = rmb.generate_dense(77, 5, 3, kind=kind, dtype=dtype, rows=(10, 20))
+    assert np.array_equal(Pr.cpu().numpy(), Ph[10:20])
+
+
+def test_device_sparse_and_grid_generators_are_bitwise_host():
+    out = rmb.generate_sparse(500, 8, 32, 9)
+    ref = gen.sparse(500, 8, 32, 9)
+    for a, b in zip(out, ref):
+        assert np.array_equal(a.cpu().numpy(), b)
+    out = rmb.generate_grid(13, dtype=torch.float64)
+    ref = gen.grid(13, dtype=np.float64)
+    for a, b in zip(out, ref):
+        assert np.array_equal(a.cpu().numpy(), b)
+
+
+# ----------------------------------------------------- single application
+CASES = [  # n, A, b, dtype, identity
+    (1, 1, 1, np.float64, False),
+    (2, 3, 1, np.float32, True),
+    (50, 4, 10, np.float64, False),
+    (50, 4, 7, np.float32, False),       # n % 4 != 0 -> scalar loads
+    (257, 5, 1, np.float32, False),      # ragged everything, A % 4 != 0
+    (257, 6, 19, np.float64, False),
+    (600, 16, 600, np.float32, False),   # Bellman T
+    (600, 16, 64, np.float32, False),
+    (1000, 40, 33, np.float32, False),   # A > 32
+    (2048, 8, 1, np.float32, True),      # Gauss-Seidel F, ascending
+    (4096, 3, 4096, np.float64, False),
+]
+
+
+@pytest.mark.parametrize("n,A,b,dtype,identity", CASES)
+@pytest.mark.parametrize("policy", [False, True])
+def test_apply_matches_oracle(n, A, b, dtype, identity, policy):
+    m, prob, P, c = make(n, A, seed=n + A, dtype=dtype)
+    rng = np.random.default_rng(n)
+    V0 = rng.standard_normal(n) * 3
+    pi = rng.integers(0, A, n).astype(np.int32) if policy else None
+    sweep = 5
+    Vg, argg, rg = prob.apply(b, 11, sweep, tdev(V0), pi=tdev(pi) if policy else None, identity=identity)
+    perm = oracle.partition(n, 11, sweep, identity=identity)
+    Vo, argo, ro = oracle.sweep(m, V0, b, perm, pi)
+    assert_close(Vg.cpu().numpy(), Vo, 1e-11)
+    assert abs(rg - ro) <= 1e-11 * max(1.0, np.abs(Vo).max())
+    mask = qgap(m, Vo) > 1e-6
+    assert np.array_equal(argg.cpu().numpy()[mask], argo[mask])
+
+
+@pytest.mark.parametrize("b", [1, 3, 8, 13])
+def test_dyadic_instance_is_bitwise(b):
+    n, A = 13, 3
+    m, prob, P, c = make(n, A, seed=4, kind="dyadic", gamma=0.5)
+    V = torch.zeros(n, dtype=torch.float64, device="cuda")
+    Vo = np.zeros(n)
+    # each batch can add 3 fraction bits (gamma/4 = 1/8) to the values it reads:
+    # stay within 45 bits so every product and sum is exact in fp64
+    T = -(-n // b)
+    for k in range(1, max(1, 45 // (3 * T)) + 1):
+        V, arg, r = prob.apply(b, 2, k, V)
+        Vo, argo, ro = oracle.sweep(m, Vo, b, oracle.partition(n, 2, k))
+        assert np.array_equal(V.cpu().numpy(), Vo) and r == ro
+        assert np.array_equal(arg.cpu().numpy(), argo)
+
+
+def test_spec_chain_worked_example():
+    # two-state chain, gamma 0.5, J = (4,4)
+    P = np.array([[[1.0, 0.0]], [[1.0, 0.0]]])
+    c = np.array([[0.0], [1.0]])
+    prob = rmb.Problem.dense(tdev(P), tdev(c), 0.5)
+    J = tdev(np.array([4.0, 4.0]))
+    assert prob.apply(2, 0, 1, J, identity=True)[0].tolist() == [2.0, 3.0]
+    assert prob.apply(1, 0, 1, J, identity=True)[0].tolist() == [2.0, 2.0]
+
+
+# ------------------------------------------------------------- solves
+def test_config1_vi_parity():
+    # BASELINE config 1: dense 50 x 4, gamma 0.9, b = 10, eps 1e-6, fp64
+    m, prob, P, c = make(50, 4, seed=1)
+    for seed in range(3):
+        sol = prob.vi(10, seed=seed, eps=1e-6)
+        ref = oracle.vi(m, 10, seed=seed, eps=1e-6)
+        assert sol.status == rmb.OK and sol.stats.sweeps == ref.sweeps
+        assert_close(sol.trace, ref.trace, 1e-9)
+        assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+        assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
+
+
+@pytest.mark.parametrize("b", [1, 64, 1000, 2000])
+def test_config2_shape_vi_parity_scaled(b):
+    """Config 2 shape (|A| = 16, gamma 0.99, fp32 P) at n = 2000, 40 sweeps."""
+    n, A = 2000, 16
+    m, prob, P, c = make(n, A, seed=2, dtype=np.float32, gamma=0.99)
+    sol = prob.vi(b, seed=3, eps=1e-6, max_sweeps=40)
+    ref = oracle.vi(m, b, seed=3, eps=1e-6, max_sweeps=40)
+    assert sol.status == rmb.NOT_CONVERGED and ref.status == oracle.NOT_CONVERGED
+    assert_close(sol.trace, ref.trace, 1e-10)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-10)
+    mask = qgap(m, ref.V) > 1e-6
+    assert np.array_equal(sol.pi.cpu().numpy()[mask], ref.pi[mask])
+
+
+def test_vi_to_convergence_small_b_sweep():
+    n, A = 300, 8
+    m, prob, P, c = make(n, A, seed=5, dtype=np.float32, gamma=0.95)
+    for b in (1, 37, 300):
+        sol = prob.vi(b, seed=1, eps=1e-8)
+        ref = oracle.vi(m, b, seed=1, eps=1e-8)
+        assert sol.status == rmb.OK
+        assert abs(sol.stats.sweeps - ref.sweeps) <= 1
+        k = min(sol.stats.sweeps, ref.sweeps)
+        assert_close(sol.trace[:k], ref.trace[:k], 1e-9)
+        if sol.stats.sweeps == ref.sweeps:
+            assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+
+
+@pytest.mark.parametrize("b,msweeps", [(1, 3), (37, 5), (300, 1), (300, 10)])
+def test_mpi_parity(b, msweeps):
+    n, A = 300, 8
+    m, prob, P, c = make(n, A, seed=6, dtype=np.float32, gamma=0.95)
+    sol = prob.mpi(b, msweeps, seed=4, eps=1e-8)
+    ref = oracle.mpi(m, b, msweeps, seed=4, eps=1e-8)
+    assert sol.status == rmb.OK and ref.status == oracle.OK
+    assert sol.stats.outer_iters == ref.outer
+    assert_close(sol.trace, ref.trace, 1e-9)
+    assert np.array_equal(sol.changed, ref.changed)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
+
+
+def test_improve_parity():
+    n, A = 500, 7
+    m, prob, P, c = make(n, A, seed=8, dtype=np.float32)
+    V = np.random.default_rng(1).standard_normal(n)
+    pi0 = np.zeros(n, np.int32)
+    pig = tdev(pi0)
+    _, r, ch = prob.improve(tdev(V), pig)
+    pio, ro, cho = oracle.improve(m, V, pi0)
+    assert np.array_equal(pig.cpu().numpy(), pio) and ch == cho
+    assert abs(r - ro) <= 1e-11 * max(1, np.abs(V).max())
+
+
+# ---------------------------------------------------------- API behaviour
+def test_host_buffers_equal_device_buffers():
+    n, A = 400, 6
+    P, c = gen.dense(n, A, 3, dtype=np.float32)
+    ph = rmb.Problem.dense(P, c, 0.97)                       # host numpy
+    pd = rmb.Problem.dense(tdev(P), tdev(c), 0.97)
+    Vh, pih = np.zeros(n), np.zeros(n, np.int32)
+    sh = ph.vi(17, seed=2, eps=1e-7, V=Vh, pi=pih)
+    sd = pd.vi(17, seed=2, eps=1e-7)
+    assert np.array_equal(Vh, sd.V.cpu().numpy()) and np.array_equal(pih, sd.pi.cpu().numpy())
+    assert np.array_equal(sh.trace, sd.trace)
+
+
+def test_bitwise_reproducible():
+    n, A = 1500, 16
+    m, prob, P, c = make(n, A, seed=9, dtype=np.float32, gamma=0.99)
+    a = prob.vi(50, seed=1, eps=1e-6, max_sweeps=30)
+    b = prob.vi(50, seed=1, eps=1e-6, max_sweeps=30)
+    assert np.array_equal(a.V.cpu().numpy(), b.V.cpu().numpy()) and np.array_equal(a.trace, b.trace)
+
+
+def test_errors():
+    n, A = 20, 2
+    m, prob, P, c = make(n, A, seed=1)
+    with pytest.raises(rmb.RmbError) as e:
+        prob.vi(0)
+    assert e.value.status == rmb.INVALID_ARG
+    with pytest.raises(rmb.RmbError):
+        prob.vi(n + 1)
+    with pytest.raises(rmb.RmbError):
+        prob.mpi(5, 0)
+    cbad = c.copy()
+    cbad[3, :] = np.inf          # every action infinite -> V(3) = inf (min ignores a single inf)
+    bad = rmb.Problem.dense(tdev(P), tdev(cbad), 0.9)
+    sol = bad.vi(5, eps=1e-6, max_sweeps=10)
+    assert sol.status == rmb.NONFINITE
+    with pytest.raises(rmb.RmbError) as e:
+        rmb.Problem.dense(tdev(P * 1.01), tdev(c), 0.9, validate=True)
+    assert e.value.status == rmb.INVALID_MDP
+
+
+def test_single_state_closed_form():
+    prob = rmb.Problem.dense(tdev(np.ones((1, 1, 1))), tdev(np.array([[1.0]])), 0.95)
+    sol = prob.vi(1, eps=1e-6)
+    K = sol.stats.sweeps
+    assert 1.0 * 0.95 ** (K - 1) <= 1e-6 < 0.95 ** (K - 2)
+    assert sol.V.item() == pytest.approx((1 - 0.95**K) / 0.05, rel=1e-13)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("b", [1, 64, 1000, 10_000])
+def test_config2_full_size_sampled(b):
+    """BASELINE config 2 at full size (n = 10^4, |A| = 16, fp32 P generated on
+    device), one application at the bench's launch configuration; 64 sampled
+    states recomputed one by one by the oracle from host-generated rows and the
+    interim V (pre/post snapshots assembled with the oracle's partition)."""
+    n, A, gamma = 10_000, 16, 0.99
+    P, c = rmb.generate_dense(n, A, 1)
+    prob = rmb.Problem.dense(P, c, gamma)
+    V0 = np.random.default_rng(0).random(n) * 50
+    V1, arg, r = prob.apply(b, 7, 3, tdev(V0))
+    V1 = V1.cpu().numpy()
+    arg = arg.cpu().numpy()
+    perm = oracle.partition(n, 7, 3)
+    pos = np.empty(n, np.int64)
+    pos[perm] = np.arange(n)
+    rng = np.random.default_rng(b)
+    for s in rng.choice(n, 64, replace=False):
+        t = pos[s] // b
+        earlier = (pos // b) < t
+        Vint = np.where(earlier, V1, V0)
+        Ph, ch = gen.dense(n, A, 1, rows=(s, s + 1))
+        assert np.array_equal(Ph[0], P[s].cpu().numpy())
+        q, a = oracle.backup_dense_row(Ph[0], ch[0], gamma, Vint)
+        assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
+        assert arg[s] == a
+    assert r == pytest.approx(np.abs(V1 - V0).max(), abs=0)
