@@ -70,6 +70,8 @@ def _load():
                                 vp, vp, vp, vp, vp, vp]
         lib.orc_backup_dense_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, i32, vp]
         lib.orc_backup_dense_row.restype = dbl
+        lib.orc_backup_csr_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, vp, vp, i32, vp]
+        lib.orc_backup_csr_row.restype = dbl
         for f in (lib.orc_partition, lib.orc_partition_inverse, lib.orc_sweep, lib.orc_improve,
                   lib.orc_vi, lib.orc_mpi):
             f.restype = ctypes.c_int
@@ -228,6 +230,20 @@ def backup_dense_row(P_rows: np.ndarray, c_row: np.ndarray, gamma: float, Vint: 
     arg = ctypes.c_int32()
     q = _load().orc_backup_dense_row(n, A, gamma, int(P_rows.dtype == np.float32), _p(P_rows), _p(c_row),
                                      _p(Vint), pi_a, ctypes.byref(arg))
+    return q, arg.value
+
+
+def backup_csr_row(n: int, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray, c_row: np.ndarray,
+                   gamma: float, Vint: np.ndarray, pi_a: int = -1):
+    """(Q_min or Q_pi, argmin) of one state from its A CSR rows (row_ptr: A+1 offsets)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.ascontiguousarray(val)
+    c_row = np.ascontiguousarray(c_row, dtype=val.dtype)
+    Vint = np.ascontiguousarray(Vint, dtype=np.float64)
+    arg = ctypes.c_int32()
+    q = _load().orc_backup_csr_row(n, len(row_ptr) - 1, gamma, int(val.dtype == np.float32), _p(row_ptr), _p(col),
+                                   _p(val), _p(c_row), _p(Vint), pi_a, ctypes.byref(arg))
     return q, arg.value
 
 

@@ -371,3 +371,28 @@ double orc_backup_dense_row(int64_t n, int32_t A, double gamma, int p_f32, const
     if (arg) *arg = a;
     return q;
 }
+
+/* Single-state backup over CSR rows for sampled parity checks at full size:
+ * row_ptr has A+1 entries (offsets into col/val for the state's A rows). */
+double orc_backup_csr_row(int64_t n, int32_t A, double gamma, int p_f32, const int64_t* row_ptr,
+                          const int32_t* col, const void* val, const void* c_row, const double* Vint,
+                          int32_t pi_a, int32_t* arg)
+{
+    orc_mdp m;
+    memset(&m, 0, sizeof m);
+    m.n = n;
+    m.A = A;
+    m.kind = 1;
+    m.gamma = gamma;
+    m.p_f32 = p_f32;
+    m.c_f32 = p_f32;
+    m.row_ptr = row_ptr;
+    m.col = col;
+    m.val = val;
+    m.c = c_row;
+    if (pi_a >= 0) { if (arg) *arg = pi_a; return q_value(&m, 0, pi_a, Vint); }
+    int32_t a;
+    double q = q_min(&m, 0, Vint, &a);
+    if (arg) *arg = a;
+    return q;
+}

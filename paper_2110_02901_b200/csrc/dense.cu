@@ -76,6 +76,7 @@ struct DenseArgs {
     int64_t part_stride;
     double* lval;        // distributed-combine list: value per batch position
     int32_t* larg;       //                           argmin per batch position
+    unsigned int* scnt;  // per batch position: items completed (last-arriver)
     unsigned long long* bar;
     int* err;
     double* trace;
@@ -177,6 +178,63 @@ __device__ __forceinline__ double load_cost(const DenseArgs& a, int64_t idx)
     return (double)__ldg(static_cast<const PT*>(a.c) + idx);
 }
 
+// The last-arriving warp of state i reduces its partials (L2) into
+// (lval[i], larg[i]).  F-mode: the (min, argmin) of the action groups in group
+// order; S-mode: lane a sums action a's chunk partials in chunk order, then an
+// argmin butterfly (lower value, then lower action).
+template <typename PT, bool EVAL>
+__device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const double* part, int C, int64_t i, int64_t s,
+                                                  int act_eval)
+{
+    const int lane = threadIdx.x & 31;
+    if (C == 1) {  // F-mode, NAG > 1 groups
+        if (lane == 0) {
+            const int NAG = (a.A + kAG - 1) / kAG;
+            const double2* pp = reinterpret_cast<const double2*>(part) + i * NAG;
+            double best = 0.0;
+            int barg = 0;
+            for (int ag = 0; ag < NAG; ++ag) {
+                const double2 q = __ldcg(pp + ag);
+                if (ag == 0 || q.x < best) best = q.x, barg = (int)q.y;
+            }
+            a.lval[i] = best;
+            a.larg[i] = barg;
+        }
+        return;
+    }
+    if (EVAL) {
+        double sum = 0.0;
+        for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(part + i * C + ch);
+        sum = warp_sum(sum);
+        if (lane == 0) {
+            a.lval[i] = load_cost<PT>(a, s * a.A + act_eval) + a.gamma * sum;
+            a.larg[i] = act_eval;
+        }
+        return;
+    }
+    double best = INFINITY;
+    int barg = 0x7fffffff;
+    for (int act = lane; act < a.A; act += kWarp) {
+        const double* pp = part + (i * a.A + act) * C;
+        double sum = 0.0;
+        for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + ch);
+        const double Q = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
+        if (barg == 0x7fffffff || Q < best) best = Q, barg = act;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, barg, o);
+        if (ov < best || (ov == best && oa < barg) || (barg == 0x7fffffff && oa != 0x7fffffff)) {
+            best = ov;
+            barg = oa;
+        }
+    }
+    if (lane == 0) {
+        a.lval[i] = best;
+        a.larg[i] = barg;
+    }
+}
+
 // ------------------------------------------------------------ compute phase
 // EVAL: rows (s, pi(s)); else rows (s, a) for all a in groups of kAG.
 // states: perm[lo + i] (perm != null) or lo + i; i < cnt.
@@ -248,7 +306,242 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
             for (int g = 0; g < NG; ++g)
                 if (lane == g && g < na) part[(i * a.A + a0 + g) * C + ch] = acc[g];
         }
+        if (!pl.redundant) {
+            // last arriver of state i finishes its backup into the list
+            if (per_state == 1) {
+                if (lane == 0) {
+                    if (EVAL) {
+                        a.lval[i] = part[i];
+                        a.larg[i] = a0;
+                    } else {
+                        a.lval[i] = part[2 * i];
+                        a.larg[i] = (int)part[2 * i + 1];
+                    }
+                }
+            } else {
+                __syncwarp();
+                unsigned int prev = 0;
+                if (lane == 0) {
+                    __threadfence();
+                    prev = atomicAdd(a.scnt + i, 1u);
+                }
+                prev = __shfl_sync(0xffffffffu, prev, 0);
+                if (prev == (unsigned int)(per_state - 1)) {
+                    __threadfence();
+                    finish_state_warp<PT, EVAL>(a, part, C, i, s, a0);
+                    if (lane == 0) a.scnt[i] = 0u;  // rearmed for the next batch (ordered by its barrier)
+                }
+            }
+        }
         it = it_next;
+    }
+}
+
+// ------------------------------------------------- CTA tile pipeline
+// The compute phase as a per-SM pipeline: a TILE = (state i, action group of
+// NG rows, column chunk) is streamed by all 512 threads of the CTA together
+// (thread t takes vectors t, t+512, ...), so a tile completes ~16x sooner than
+// if one warp owned it and the end-of-batch tail shrinks accordingly.  Each
+// thread keeps D slots of NG*U2 = 4 vector loads in flight and keeps issuing
+// across tile boundaries; per tile one __syncthreads joins the 16 warp sums
+// (fixed warp order -> reproducible) while the next tile's loads are already
+// in flight.  Tiles are taken from a global work-stealing counter by thread 0,
+// five tiles ahead, with their state id / costs prefetched into a smem ring.
+constexpr int kRing = 8;
+constexpr int kAhead = 5;  // tiles grabbed ahead (> D + 1)
+constexpr int kD = 3;      // slots in flight per thread
+
+struct TileRing {
+    long long it[kRing];  // item index, -1 = end
+    long long s[kRing];   // state
+    long long i[kRing];   // batch position
+    int a0[kRing], na[kRing], ch[kRing], R[kRing];
+    long long j0[kRing];
+    int nvec[kRing];
+    double cost[kRing][kAG];
+    double red[2][kWarps][kAG];
+};
+
+template <typename PT, bool EVAL>
+__device__ __forceinline__ void tile_grab(const DenseArgs& a, TileRing& tr, int slot, unsigned int* ctr,
+                                          const uint32_t* perm, const int32_t* pis, int64_t lo, int64_t items,
+                                          int64_t per_state, int C, int64_t Lc, int VE, int U2)
+{
+    const long long it = (long long)atomicAdd(ctr, 1u);
+    if (it >= items) {
+        tr.it[slot] = -1;
+        return;
+    }
+    const int64_t i = it / per_state;
+    const int rr = (int)(it - i * per_state);
+    const int ag = rr / C;
+    const int ch = rr - ag * C;
+    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+    const int a0 = EVAL ? pis[s] : ag * kAG;
+    const int na = EVAL ? 1 : min(kAG, a.A - a0);
+    const int64_t j0 = (int64_t)ch * Lc;
+    const int64_t j1 = min(a.n, j0 + Lc);
+    const int nvec = (int)((j1 - j0) / VE);
+    tr.it[slot] = it;
+    tr.s[slot] = s;
+    tr.i[slot] = i;
+    tr.a0[slot] = a0;
+    tr.na[slot] = na;
+    tr.ch[slot] = ch;
+    tr.j0[slot] = j0;
+    tr.nvec[slot] = nvec;
+    tr.R[slot] = max(1, (nvec + kThreads * U2 - 1) / (kThreads * U2));
+    for (int g = 0; g < kAG; ++g) tr.cost[slot][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
+}
+
+template <typename PT, int VE, bool EVAL>
+__device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
+                                  int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
+{
+    using VT = typename Vec<PT, VE>::T;
+    constexpr int NG = EVAL ? 1 : kAG;
+    constexpr int U2 = kAG / NG;  // vectors per row per slot (4 loads per slot)
+    __shared__ TileRing tr;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int C = pl.C;
+    const int64_t Lc = pl.Lc;
+    const int NAG = EVAL ? 1 : (a.A + kAG - 1) / kAG;
+    const int64_t per_state = (int64_t)NAG * C;
+    const int64_t items = cnt * per_state;
+    const PT* P = static_cast<const PT*>(a.P);
+
+    __syncthreads();  // previous phase's readers of tr are done
+    if (tid == 0)
+        for (int q = 0; q < kAhead; ++q)
+            tile_grab<PT, EVAL>(a, tr, q, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2);
+    __syncthreads();
+
+    VT buf[kD][kAG];
+    double acc[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) acc[g] = 0.0;
+    int cq = 0, cr = 0;  // consume position (tile, slot)
+    int iq = 0, ir = 0;  // issue position
+
+    auto issue = [&](VT (&b)[kAG]) {
+        const int sl = iq & (kRing - 1);
+        if (tr.it[sl] < 0) return;
+        const VT* row = reinterpret_cast<const VT*>(P + (tr.s[sl] * a.A + tr.a0[sl]) * a.n + tr.j0[sl]);
+        const int nv = tr.nvec[sl], na = tr.na[sl];
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+            const int v = tid + kThreads * (U2 * ir + u);
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                if (g < na && v < nv) b[u * NG + g] = ld_stream(row + (int64_t)g * (a.n / VE) + v);
+        }
+        if (++ir == tr.R[sl]) ++iq, ir = 0;
+    };
+    auto consume = [&](const VT (&b)[kAG]) {
+        const int sl = cq & (kRing - 1);
+        const int nv = tr.nvec[sl], na = tr.na[sl];
+        const int64_t j0 = tr.j0[sl];
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+            const int v = tid + kThreads * (U2 * cr + u);
+            if (v < nv) {
+                double vs[VE];
+                load_v<VE>(Vs, j0 + (int64_t)v * VE, vs);
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (g < na) {
+                        double p[VE];
+                        Vec<PT, VE>::get(b[u * NG + g], p);
+#pragma unroll
+                        for (int e = 0; e < VE; ++e) acc[g] = fma(p[e], vs[e], acc[g]);
+                    }
+                }
+            }
+        }
+    };
+    // tile cq fully consumed: join the warp sums, emit, grab ahead
+    auto finalize = [&]() {
+        const int sl = cq & (kRing - 1);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const double w = warp_sum(acc[g]);
+            if (lane == 0) tr.red[cq & 1][warp][g] = w;
+            acc[g] = 0.0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double tot[NG];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                tot[g] = 0.0;
+                for (int w = 0; w < kWarps; ++w) tot[g] += tr.red[cq & 1][w][g];
+            }
+            const int64_t i = tr.i[sl];
+            const int a0 = tr.a0[sl], na = tr.na[sl], ch = tr.ch[sl];
+            if (lane == 0) {
+                if (C == 1) {
+                    if (EVAL) {
+                        part[i] = tr.cost[sl][0] + a.gamma * tot[0];
+                    } else {
+                        double best = 0.0;
+                        int barg = a0;
+#pragma unroll
+                        for (int g = 0; g < NG; ++g)
+                            if (g < na) {
+                                const double Q = tr.cost[sl][g] + a.gamma * tot[g];
+                                if (g == 0 || Q < best) best = Q, barg = a0 + g;
+                            }
+                        part[2 * (i * NAG + a0 / kAG)] = best;
+                        part[2 * (i * NAG + a0 / kAG) + 1] = (double)barg;
+                    }
+                } else if (EVAL) {
+                    part[i * C + ch] = tot[0];
+                } else {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g)
+                        if (g < na) part[(i * a.A + a0 + g) * C + ch] = tot[g];
+                }
+            }
+            if (!pl.redundant) {
+                if (per_state == 1) {
+                    if (lane == 0) {
+                        a.lval[i] = EVAL ? part[i] : part[2 * i];
+                        a.larg[i] = EVAL ? a0 : (int)part[2 * i + 1];
+                    }
+                } else {
+                    unsigned int prev = 0;
+                    if (lane == 0) {
+                        __threadfence();
+                        prev = atomicAdd(a.scnt + i, 1u);
+                    }
+                    prev = __shfl_sync(0xffffffffu, prev, 0);
+                    if (prev == (unsigned int)(per_state - 1)) {
+                        __threadfence();
+                        finish_state_warp<PT, EVAL>(a, part, C, i, tr.s[sl], a0);
+                        if (lane == 0) a.scnt[i] = 0u;
+                    }
+                }
+            }
+            if (lane == 0)
+                tile_grab<PT, EVAL>(a, tr, (cq + kAhead) & (kRing - 1), ctr, perm, pis, lo, items, per_state, C,
+                                    Lc, VE, U2);
+        }
+        ++cq;
+        cr = 0;
+    };
+
+#pragma unroll
+    for (int d = 0; d < kD; ++d) issue(buf[d]);
+    while (tr.it[cq & (kRing - 1)] >= 0) {
+#pragma unroll
+        for (int d = 0; d < kD; ++d) {
+            if (tr.it[cq & (kRing - 1)] < 0) break;
+            consume(buf[d]);
+            issue(buf[d]);
+            if (++cr == tr.R[cq & (kRing - 1)]) finalize();
+        }
     }
 }
 
@@ -384,7 +677,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     // the other parity's work counter was last used before the previous
     // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
-    compute_phase<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+    compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
@@ -396,10 +689,6 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     timed_sync(x);
     const bool F = pl.C == 1;
     auto patch = [&](int64_t, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, s, v, arg, acc); };
-    auto to_list = [&](int64_t i, int64_t, double v, int arg) {
-        a.lval[i] = v;
-        a.larg[i] = arg;
-    };
     if (pl.redundant) {
         if (F) {
             for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
@@ -413,20 +702,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
             reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, 0, 1, pis, Qs, patch);
         }
     } else {
-        // distributed: CTA x reduces states i = x mod grid into the list
-        const int64_t G = gridDim.x;
-        if (F) {
-            for (int64_t i = blockIdx.x + (int64_t)threadIdx.x * G; i < cnt; i += (int64_t)kThreads * G) {
-                double v;
-                int arg;
-                reduce_state_F<EVAL>(a, part, i, v, arg);
-                a.lval[i] = v;
-                a.larg[i] = arg;
-            }
-        } else {
-            reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, blockIdx.x, G, pis, Qs, to_list);
-        }
-        timed_sync(x);
+        // last-arriver mode: the list was completed during the compute phase
         for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
             const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
             patch_state<KIND>(a, Vs, pis, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
@@ -577,18 +853,25 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
 }
 
 // ------------------------------------------------------------------ host
-// rows = (states per batch) x (items per state before chunking)
+// rows = (states per batch) x (items per state before chunking).  Items are
+// NG rows x Lc columns of P: at most ~16 KB so that the dynamically scheduled
+// tail (one warp finishing one item) stays a few microseconds, and at least
+// ~32 items per SM when the batch is small (b = 1 must still fill 148 SMs).
 static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_eff, int VE, int num_sms,
-                        bool allow_split)
+                        bool allow_split, int ng, int psz)
 {
     const int64_t rows = cnt * groups_per_state;
     const int64_t unit = (int64_t)kWarp * VE;
     const int64_t maxC = std::max<int64_t>(1, (n + unit - 1) / unit);
+    const int64_t lc_target = std::max<int64_t>(unit, (int64_t(16) << 10) / ((int64_t)ng * psz));
     int64_t c = 1;
-    // >= 16 items per SM keeps the per-SM imbalance of the round-robin deal
-    // small; below that, split rows into column chunks (up to ~32 per SM)
-    if (allow_split && rows < 16LL * num_sms) c = (32LL * num_sms + rows - 1) / rows;
-    c = std::min(std::max<int64_t>(c, 1), maxC);
+    if (allow_split && rows < 16LL * num_sms) {
+        (void)lc_target;
+        c = (32LL * num_sms + rows - 1) / rows;
+        // bound the partial-sum scratch (A_eff * C doubles per state) to 64 MB
+        c = std::min<int64_t>(c, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, cnt * A_eff)));
+        c = std::min(std::max<int64_t>(c, 1), maxC);
+    }
     int64_t L = (n + c - 1) / c;
     L = (L + unit - 1) / unit * unit;
     Plan p;
@@ -659,11 +942,11 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 2048) / 8);
     const size_t smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
     const bool split_ok = a.qs_cap >= pr.A;  // else every row stays whole (C = 1)
-    a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok);
-    a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok);
+    a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok, kAG, psz);
+    a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok, 1, psz);
     // improvement (no V write): as few sub-batches as a bounded scratch allows
-    a.imp_sub = n * NAG * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(std::min<int64_t>(n, rq.b), (int64_t(1) << 21) / NAG);
-    a.plan[2] = plan_chunks(n, a.imp_sub, NAG, pr.A, VE, sms, split_ok);
+    a.imp_sub = n * NAG * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / (2 * NAG));
+    a.plan[2] = plan_chunks(n, a.imp_sub, NAG, pr.A, VE, sms, split_ok, kAG, psz);
     const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
                                               plan_doubles(a.plan[2], a.imp_sub, NAG, pr.A)});
@@ -672,7 +955,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
 
     cudaStream_t st = pr.stream;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess ||
-        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)lcap * 12 + 64) != cudaSuccess ||
+        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)lcap * 16 + 64) != cudaSuccess ||
         pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("dense solver: workspace allocation failed");
         return RMB_ERR_OOM;
@@ -681,6 +964,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     a.part = static_cast<double*>(pr.part.p);
     a.lval = a.part + 2 * a.part_stride;
     a.larg = reinterpret_cast<int32_t*>(a.lval + lcap);
+    a.scnt = reinterpret_cast<unsigned int*>(a.larg + lcap);
     unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
     a.bar = ctrl;                                      // [0], [32]
     a.err = reinterpret_cast<int*>(ctrl + 64);         // [64]
@@ -696,6 +980,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(a.scnt, 0, (size_t)lcap * 4, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)

@@ -62,11 +62,33 @@ struct Permutation {
         return (L << h) | R;
     }
 
+    RMB_HD uint64_t decrypt(uint64_t x) const
+    {
+        uint64_t L = x >> h, R = x & lo_mask;
+#pragma unroll
+        for (int r = 5; r >= 0; --r) {
+            // forward round: (L', R') = (R, L ^ F(R))  =>  R = L', L = R' ^ F(L')
+            const uint64_t f = splitmix64(rk[r] ^ L) >> (64u - h);
+            const uint64_t t = R ^ f;
+            R = L;
+            L = t;
+        }
+        return (L << h) | R;
+    }
+
     // state at position p
     RMB_HD uint64_t operator()(uint64_t p) const
     {
         uint64_t x = encrypt(p);
         while (x >= n) x = encrypt(x);
+        return x;
+    }
+
+    // position of state s (the inverse permutation, same cycle walk backwards)
+    RMB_HD uint64_t position(uint64_t s) const
+    {
+        uint64_t x = decrypt(s);
+        while (x >= n) x = decrypt(x);
         return x;
     }
 };

@@ -1,13 +1,567 @@
-// sparse.cu — persistent sm_100a solver for CSR / ELL MDPs (placeholder until
-// the sparse kernel lands; dense problems are served by dense.cu).
+// sparse.cu — persistent sm_100a solver for SPARSE MDPs (CSR over rows
+// r = s*A + a; fixed-stride rows are served as ELL).
+//
+// One cooperative launch runs a whole MB-VI / MB-MPI solve (Alg. 1).
+// V does not fit in shared memory (config 3: 8 MB, config 4: 33.5 MB), so the
+// interim vector lives in L2-resident global memory, ping-ponged by batch:
+//
+//   invariant: at the start of (global) batch g, X[g & 1] is the interim V.
+//   batch g reads successors from X_cur = X[g & 1] (one 8-byte gather per
+//   nonzero, no select), writes its states' new values into X_next, and also
+//   re-copies the previous batch's states X_cur -> X_next, so that X_next is
+//   the interim V of batch g+1 after the single grid barrier.
+//
+// This realises Eq. 12 exactly: every read of batch g sees the
+// values of earlier batches (they are in X_cur) and the previous sweep's
+// values of every other state, including same-batch states.
+//
+// Per state, a lane group does the backup:
+//   row mode (ELL width K <= 8, A <= 32): lane a sums row (s, a) sequentially,
+//     then an argmin butterfly over the group (ties -> lower action);
+//   strided mode (wide or ragged rows): the group's lanes stride over each
+//     row's nonzeros, butterfly sum, actions in order (strict < keeps the
+//     lowest index).
+// The residual and nonfinite flag are reduced per CTA and combined with one
+// atomicMax / atomicOr per CTA before the sweep's last barrier.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
 #include "internal.h"
+#include "partition.cuh"
 
 namespace rmb {
 
-rmb_status sparse_solve(Problem&, const SolveRequest&, double*, int64_t, long long*, int64_t, SolveResult*)
+constexpr int kSThreads = 1024;
+constexpr int kSWarps = kSThreads / kWarp;
+
+struct SparseArgs {
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const void* val;
+    const void* c;
+    int64_t n;
+    int A;
+    int K;  // > 0: ELL width
+    int GS; // lanes per state (power of two <= 32)
+    double gamma;
+    double* V;
+    int32_t* pi;
+    double* X0;
+    double* X1;
+    int32_t* pw0;  // MPI policy ping-pong
+    int32_t* pw1;
+    int64_t b;
+    uint64_t seed;
+    int64_t k0;
+    int identity;
+    int mode;
+    int pi_given;
+    double eps;
+    int64_t max_iter;
+    int msweeps;
+    uint32_t* perm;  // 3 * n
+    unsigned long long* bar;
+    int* err;
+    unsigned long long* red;  // [4] residual bits ring, [4..8) nonfinite ring, [8..12) changed ring
+    double* trace;
+    int64_t trace_len;
+    long long* chg;
+    int64_t chg_len;
+    long long* out;
+    long long* prof;
+};
+
+template <typename PT>
+__device__ __forceinline__ double ldv(const void* p, int64_t e)
 {
-    set_error("sparse solver not built yet");
-    return RMB_ERR_UNSUPPORTED;
+    return (double)__ldg(static_cast<const PT*>(p) + e);
+}
+
+// Backup of state s against X by a group of GS lanes (g = lane in group).
+// act_fixed >= 0: B_{pi,b} row only.  Result valid in every lane of the group.
+template <typename PT, bool ROWMODE>
+__device__ __forceinline__ void backup_state(const SparseArgs& a, const double* X, int64_t s, int act_fixed, int g,
+                                             bool valid, double& best, int& barg)
+{
+    const int GS = a.GS;
+    if (ROWMODE) {
+        double Q = INFINITY;
+        int arg = 0x7fffffff;
+        const int act = !valid ? -1 : act_fixed >= 0 ? (g == 0 ? act_fixed : -1) : (g < a.A ? g : -1);
+        if (act >= 0) {
+            const int64_t row = s * a.A + act;
+            const int64_t e0 = a.K > 0 ? row * a.K : __ldg(a.row_ptr + row);
+            const int64_t e1 = a.K > 0 ? e0 + a.K : __ldg(a.row_ptr + row + 1);
+            // one lane, storage order, separately rounded products and sums
+            // (no FMA contraction): the same arithmetic as the oracle's row
+            // sum, so row mode is bit-exact and exact Q ties (symmetric grids)
+            // break identically on both sides
+            double acc = 0.0;
+            for (int64_t e = e0; e < e1; ++e)
+                acc = __dadd_rn(acc, __dmul_rn(ldv<PT>(a.val, e), __ldcg(X + __ldg(a.col + e))));
+            Q = __dadd_rn(ldv<PT>(a.c, row), __dmul_rn(a.gamma, acc));
+            arg = act;
+        }
+        for (int o = GS >> 1; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, Q, o);
+            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+            // lane order == action order, so (lower value, then lower index)
+            // reproduces "first strict minimum"; a NaN in lane 0 stays (as in
+            // the oracle, where a NaN Q_0 is never replaced)
+            if (ov < Q || (ov == Q && oa < arg) || (arg == 0x7fffffff && oa != 0x7fffffff)) {
+                Q = ov;
+                arg = oa;
+            }
+        }
+        best = Q;
+        barg = arg;
+        return;
+    }
+    const int a_lo = act_fixed >= 0 ? act_fixed : 0;
+    const int a_hi = act_fixed >= 0 ? act_fixed + 1 : a.A;
+    best = 0.0;
+    barg = a_lo;
+    for (int act = a_lo; act < a_hi; ++act) {
+        const int64_t row = s * a.A + act;
+        const int64_t e0 = !valid ? 0 : a.K > 0 ? row * a.K : __ldg(a.row_ptr + row);
+        const int64_t e1 = !valid ? 0 : a.K > 0 ? e0 + a.K : __ldg(a.row_ptr + row + 1);
+        double acc = 0.0;
+        for (int64_t e = e0 + g; e < e1; e += GS) acc = fma(ldv<PT>(a.val, e), __ldcg(X + __ldg(a.col + e)), acc);
+        for (int o = GS >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const double Q = valid ? ldv<PT>(a.c, row) + a.gamma * acc : 0.0;
+        if (act == a_lo || Q < best) best = Q, barg = act;
+    }
+}
+
+struct SCtx {
+    GridBarrier g;
+    int64_t gb;  // global batch counter (X parity)
+    int64_t batches;
+    // previous batch (for the X_cur -> X_next re-copy)
+    const uint32_t* prev_perm;
+    int64_t prev_lo, prev_cnt;
+    bool prev_valid;
+    unsigned long long t_mark;
+    long long t_comp, t_bar, n_bar;
+};
+
+__device__ __forceinline__ void s_prof(SCtx& x, long long* slot)
+{
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long t = globaltimer_ns();
+        *slot += (long long)(t - x.t_mark);
+        x.t_mark = t;
+    }
+}
+
+// CTA reduction (max, or, sum) then one global atomic per CTA.
+__device__ void cta_publish(const SparseArgs& a, int slot, double rmax, int bad, long long changed)
+{
+    __shared__ double sd[kSWarps];
+    __shared__ int si[kSWarps];
+    __shared__ long long sl[kSWarps];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sd[w] = rmax, si[w] = bad, sl[w] = changed;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        int bb = 0;
+        long long cc = 0;
+        for (int k = 0; k < kSWarps; ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
+        atomicMax(a.red + slot, (unsigned long long)__double_as_longlong(r));
+        if (bb) atomicOr(reinterpret_cast<unsigned int*>(a.red + 4 + slot), 1u);
+        if (cc) atomicAdd(a.red + 8 + slot, (unsigned long long)cc);
+    }
+}
+
+struct SweepResult {
+    double r;
+    int bad;
+    long long changed;
+};
+
+__device__ __forceinline__ SweepResult read_slot(const SparseArgs& a, int slot)
+{
+    SweepResult s;
+    s.r = __longlong_as_double((long long)ld_acquire_gpu(a.red + slot));
+    s.bad = ld_acquire_gpu(a.red + 4 + slot) != 0;
+    s.changed = (long long)ld_acquire_gpu(a.red + 8 + slot);
+    return s;
+}
+
+// One application of B_b (EVAL false) or B_{pi,b} (EVAL true), sweep k.
+template <typename PT, bool ROWMODE, bool EVAL>
+__device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const int32_t* pol)
+{
+    const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
+    const int GS = a.GS;
+    const int g = threadIdx.x & (GS - 1);
+    // warp-uniform trip counts: all 32 lanes stay in the loop for the shuffles
+    const int64_t ngroups = (int64_t)gridDim.x * (kSThreads / GS);
+    const int64_t gid = (int64_t)blockIdx.x * (kSThreads / GS) + threadIdx.x / GS;
+    const int64_t wfirst = gid - (threadIdx.x & 31) / GS;  // first group of this warp
+    const int slot = (int)(k & 3);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // rearm the ring slot used two sweeps ahead
+        const int z = (int)((k + 2) & 3);
+        atomicExch(a.red + z, 0ull);
+        atomicExch(a.red + 4 + z, 0ull);
+        atomicExch(a.red + 8 + z, 0ull);
+    }
+    const bool single = a.b >= a.n;  // one batch per sweep: every state rewritten each batch
+    double rmax = 0.0;
+    int bad = 0;
+    for (int64_t lo = 0; lo < a.n; lo += a.b) {
+        const int64_t cnt = min(a.b, a.n - lo);
+        const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
+        double* Xn = (x.gb & 1) ? a.X0 : a.X1;
+        // states in processing order; a single batch is order-free, so walk it
+        // in state order (coalesced rows)
+        const uint32_t* bperm = single ? nullptr : perm;
+        for (int64_t w0 = wfirst; w0 < cnt; w0 += ngroups) {
+            const int64_t i = w0 + (gid - wfirst);
+            const bool valid = i < cnt;
+            const int64_t s = !valid ? 0 : bperm ? (int64_t)__ldg(bperm + lo + i) : lo + i;
+            double v;
+            int arg;
+            backup_state<PT, ROWMODE>(a, Xc, s, EVAL ? pol[s] : -1, g, valid, v, arg);
+            if (valid && g == 0) {
+                const double old = __ldcg(Xc + s);
+                rmax = fmax(rmax, fabs(v - old));
+                bad |= !isfinite(v);
+                Xn[s] = v;
+                if (!EVAL && a.pi) a.pi[s] = arg;
+            }
+        }
+        // carry the previous batch's new values into X_next.  In the first
+        // batch of a sweep the previous batch belongs to the previous sweep and
+        // may share states with this batch: those get this batch's new value,
+        // so their copy is skipped (membership through the inverse permutation).
+        if (x.prev_valid && !single) {
+            Permutation pk;
+            if (lo == 0 && !a.identity) pk.init(a.n, a.seed, k);
+            const int64_t stride = (int64_t)gridDim.x * kSThreads;
+            for (int64_t i = (int64_t)blockIdx.x * kSThreads + threadIdx.x; i < x.prev_cnt; i += stride) {
+                const int64_t s = x.prev_perm ? (int64_t)x.prev_perm[x.prev_lo + i] : x.prev_lo + i;
+                if (lo == 0) {
+                    const int64_t pos = a.identity ? s : (int64_t)pk.position((uint64_t)s);
+                    if (pos < cnt) continue;
+                }
+                Xn[s] = __ldcg(Xc + s);
+            }
+        }
+        if (lo == 0 && !a.identity) {  // next sweep's order, off the critical path
+            Permutation pm;
+            pm.init(a.n, a.seed, k + 1);
+            uint32_t* dst = a.perm + ((k + 1) % 3) * a.n;
+            const int64_t stride = (int64_t)gridDim.x * kSThreads;
+            for (int64_t p = (int64_t)blockIdx.x * kSThreads + threadIdx.x; p < a.n; p += stride)
+                dst[p] = (uint32_t)pm((uint64_t)p);
+        }
+        const bool last = lo + a.b >= a.n;
+        if (last) cta_publish(a, slot, rmax, bad, 0);
+        s_prof(x, &x.t_comp);
+        grid_sync(x.g);
+        s_prof(x, &x.t_bar);
+        x.n_bar++;
+        x.prev_perm = single ? nullptr : perm;
+        x.prev_lo = lo;
+        x.prev_cnt = cnt;
+        x.prev_valid = !single;
+        ++x.gb;
+        ++x.batches;
+    }
+    return read_slot(a, slot);
+}
+
+// Policy improvement over all states against X_cur (no X write):
+// pw_next = greedy, changed vs pw_cur, ||TV - V||_inf.
+template <typename PT, bool ROWMODE>
+__device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx, const int32_t* pcur, int32_t* pnext,
+                                   bool count_changed)
+{
+    const int GS = a.GS;
+    const int g = threadIdx.x & (GS - 1);
+    const int64_t ngroups = (int64_t)gridDim.x * (kSThreads / GS);
+    const int64_t gid = (int64_t)blockIdx.x * (kSThreads / GS) + threadIdx.x / GS;
+    const int64_t wfirst = gid - (threadIdx.x & 31) / GS;
+    // improvement steps use their own ring (slots 2,3 parity of imp_idx) via the
+    // same red[] words offset by 16
+    const SparseArgs* ap = &a;
+    const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
+    double rmax = 0.0;
+    int bad = 0;
+    long long changed = 0;
+    for (int64_t w0 = wfirst; w0 < a.n; w0 += ngroups) {
+        const int64_t s = w0 + (gid - wfirst);
+        const bool valid = s < a.n;
+        double v;
+        int arg;
+        backup_state<PT, ROWMODE>(a, Xc, valid ? s : 0, -1, g, valid, v, arg);
+        if (valid && g == 0) {
+            rmax = fmax(rmax, fabs(v - __ldcg(Xc + s)));
+            bad |= !isfinite(v);
+            if (count_changed) changed += (arg != pcur[s]);
+            pnext[s] = arg;
+        }
+    }
+    // improvement ring: red[16 + 4*q .. ] with q = imp_idx & 1 (rearmed for q^1)
+    unsigned long long* base = a.red + 16 + 4 * (imp_idx & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long* other = a.red + 16 + 4 * ((imp_idx + 1) & 1);
+        atomicExch(other, 0ull);
+        atomicExch(other + 1, 0ull);
+        atomicExch(other + 2, 0ull);
+    }
+    {
+        __shared__ double sd[kSWarps];
+        __shared__ int si[kSWarps];
+        __shared__ long long sl[kSWarps];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+            changed += __shfl_xor_sync(0xffffffffu, changed, o);
+        }
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) sd[w] = rmax, si[w] = bad, sl[w] = changed;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double r = 0.0;
+            int bb = 0;
+            long long cc = 0;
+            for (int k = 0; k < kSWarps; ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
+            atomicMax(base, (unsigned long long)__double_as_longlong(r));
+            if (bb) atomicOr(base + 1, 1ull);
+            if (cc) atomicAdd(base + 2, (unsigned long long)cc);
+        }
+    }
+    (void)ap;
+    s_prof(x, &x.t_comp);
+    grid_sync(x.g);
+    s_prof(x, &x.t_bar);
+    x.n_bar++;
+    SweepResult r;
+    r.r = __longlong_as_double((long long)ld_acquire_gpu(base));
+    r.bad = ld_acquire_gpu(base + 1) != 0;
+    r.changed = (long long)ld_acquire_gpu(base + 2);
+    return r;
+}
+
+template <typename PT, bool ROWMODE>
+__global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const SparseArgs a)
+{
+    SCtx x{};
+    x.g = GridBarrier{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err};
+    if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
+    const int64_t stride = (int64_t)gridDim.x * kSThreads;
+    const int64_t tid = (int64_t)blockIdx.x * kSThreads + threadIdx.x;
+    for (int64_t s = tid; s < a.n; s += stride) {
+        const double v = a.V[s];
+        a.X0[s] = v;
+        a.X1[s] = v;
+        if (a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE) a.pw0[s] = a.pi[s];
+    }
+    if (!a.identity && a.mode != MODE_IMPROVE) {
+        Permutation pm;
+        pm.init(a.n, a.seed, a.k0);
+        uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
+        for (int64_t p = tid; p < a.n; p += stride) dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+    grid_sync(x.g);
+
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    long long status = RMB_ERR_NOT_CONVERGED;
+    int64_t k = a.k0, it = 0, outer = 0, imp = 0;
+    long long changed = 0;
+    double last = 0.0;
+    int pcur = 0;  // which pw buffer holds the current policy
+    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
+        const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
+        while (it < iters) {
+            SweepResult r = a.mode == MODE_APPLY_PI ? run_sweep<PT, ROWMODE, true>(a, x, k, a.pw0)
+                                                    : run_sweep<PT, ROWMODE, false>(a, x, k, nullptr);
+            if (lead && it < a.trace_len) a.trace[it] = r.r;
+            ++it;
+            ++k;
+            last = r.r;
+            if (r.bad) { status = RMB_ERR_NONFINITE; break; }
+            if (a.eps >= 0.0 && r.r <= a.eps) { status = RMB_OK; break; }
+        }
+        if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+    } else if (a.mode == MODE_IMPROVE) {
+        SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, a.pw0, a.pw1, true);
+        pcur = 1;
+        last = r.r;
+        changed = r.changed;
+        status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
+    } else {  // MODE_MPI
+        bool bad = false;
+        if (!a.pi_given) {
+            SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, a.pw0, a.pw1, false);
+            pcur = 1;
+            bad = r.bad;
+        }
+        while (!bad && outer < a.max_iter) {
+            const int64_t row = outer * (a.msweeps + 1);
+            const int32_t* pol = pcur ? a.pw1 : a.pw0;
+            for (int e = 0; e < a.msweeps && !bad; ++e) {
+                SweepResult r = run_sweep<PT, ROWMODE, true>(a, x, k, pol);
+                if (lead && row + e < a.trace_len) a.trace[row + e] = r.r;
+                ++k;
+                ++it;
+                bad = r.bad;
+            }
+            if (bad) { ++outer; break; }
+            SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, pol, pcur ? a.pw0 : a.pw1, true);
+            pcur ^= 1;
+            if (lead && row + a.msweeps < a.trace_len) a.trace[row + a.msweeps] = r.r;
+            if (lead && outer < a.chg_len) a.chg[outer] = r.changed;
+            ++outer;
+            last = r.r;
+            changed = r.changed;
+            if (r.bad) { bad = true; break; }
+            if (r.changed == 0 && r.r <= a.eps) { status = RMB_OK; break; }
+        }
+        if (bad) status = RMB_ERR_NONFINITE;
+    }
+    // outputs: the interim vector after the last batch, and the policy
+    const double* Xf = (x.gb & 1) ? a.X1 : a.X0;
+    const int32_t* pf = pcur ? a.pw1 : a.pw0;
+    const bool write_pi_buf = a.mode == MODE_MPI || a.mode == MODE_IMPROVE;
+    for (int64_t s = tid; s < a.n; s += stride) {
+        if (a.mode != MODE_IMPROVE) a.V[s] = Xf[s];
+        if (write_pi_buf) a.pi[s] = pf[s];
+    }
+    if (lead) {
+        a.out[OUT_SWEEPS] = it;
+        a.out[OUT_OUTER] = outer;
+        a.out[OUT_STATUS] = status;
+        a.out[OUT_RESID_BITS] = __double_as_longlong(last);
+        a.out[OUT_BATCHES] = x.batches;
+        a.out[OUT_CHANGED] = changed;
+        a.prof[0] = x.t_comp;
+        a.prof[1] = x.t_bar;
+        a.prof[2] = 0;
+        a.prof[3] = x.n_bar;
+    }
+}
+
+template <typename PT, bool ROWMODE>
+static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
+{
+    auto kern = sparse_solver_kernel<PT, ROWMODE>;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    void* args[] = {const_cast<SparseArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSThreads), args, 0, st);
+}
+
+rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                        long long* chg_dev, int64_t chg_len, SolveResult* res)
+{
+    const int64_t n = pr.n;
+    SparseArgs a{};
+    a.row_ptr = pr.row_ptr;
+    a.col = pr.col;
+    a.val = pr.val;
+    a.c = pr.c;
+    a.n = n;
+    a.A = pr.A;
+    a.K = pr.ell_K;
+    a.gamma = pr.gamma;
+    a.V = rq.V;
+    a.pi = rq.pi;
+    a.b = rq.b;
+    a.seed = rq.seed;
+    a.k0 = rq.k0;
+    a.identity = rq.identity ? 1 : 0;
+    a.mode = rq.mode;
+    a.pi_given = rq.pi_given ? 1 : 0;
+    a.eps = rq.eps;
+    a.max_iter = rq.max_iter;
+    a.msweeps = rq.msweeps;
+    const double avg = pr.n * pr.A > 0 ? (double)pr.nnz / (double)(pr.n * pr.A) : 1.0;
+    const bool rowmode = pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32;
+    int GS = 1;
+    if (rowmode) {
+        while (GS < pr.A) GS <<= 1;
+    } else {
+        while (GS < 32 && GS < avg) GS <<= 1;
+    }
+    a.GS = GS;
+
+    cudaStream_t st = pr.stream;
+    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.part.ensure((size_t)2 * n * 8 + (size_t)2 * n * 4 + 256) != cudaSuccess ||
+        pr.ctrl.ensure(4096) != cudaSuccess) {
+        set_error("sparse solver: workspace allocation failed");
+        return RMB_ERR_OOM;
+    }
+    a.perm = static_cast<uint32_t*>(pr.perm.p);
+    a.X0 = static_cast<double*>(pr.part.p);
+    a.X1 = a.X0 + n;
+    a.pw0 = reinterpret_cast<int32_t*>(a.X1 + n);
+    a.pw1 = a.pw0 + n;
+    unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
+    a.bar = ctrl;
+    a.err = reinterpret_cast<int*>(ctrl + 64);
+    a.out = reinterpret_cast<long long*>(ctrl + 128);
+    a.prof = reinterpret_cast<long long*>(ctrl + 192);
+    a.red = ctrl + 256;  // [256 .. 280)
+    a.trace = trace_dev;
+    a.trace_len = trace_len;
+    a.chg = chg_dev;
+    a.chg_len = chg_len;
+
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    const int grid = pr.num_sms;
+    if (ce == cudaSuccess) {
+        if (pr.pdt == RMB_F32)
+            ce = rowmode ? launch_sparse<float, true>(a, grid, st) : launch_sparse<float, false>(a, grid, st);
+        else
+            ce = rowmode ? launch_sparse<double, true>(a, grid, st) : launch_sparse<double, false>(a, grid, st);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
+    long long out[OUT_N + 4] = {0};
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) {
+        set_error(std::string("sparse solver: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    res->sweeps = out[OUT_SWEEPS];
+    res->outer = out[OUT_OUTER];
+    res->status = (int)out[OUT_STATUS];
+    double d;
+    memcpy(&d, &out[OUT_RESID_BITS], 8);
+    res->final_resid = d;
+    res->batches = out[OUT_BATCHES];
+    res->changed = out[OUT_CHANGED];
+    res->ms = ms;
+    res->launches = 1;
+    for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
+    pr.last_launches = 1;
+    return RMB_OK;
 }
 
 }  // namespace rmb

@@ -1,0 +1,188 @@
+"""GPU parity of the sparse (CSR / ELL) persistent solver vs the CPU oracle.
+
+Same bar as test_gpu_dense.py: single applications to 1e-11 * max(1,|V|),
+solves to 1e-9 * max(1,|V|), identical sweep counts and residual traces,
+policies bit-exact where the Q-gap exceeds 1e-6.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+import paper_2110_02901_b200 as rmb
+
+pytestmark = pytest.mark.gpu
+
+
+def tdev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def assert_close(a, b, rel):
+    scale = max(1.0, float(np.abs(b).max()))
+    d = np.abs(np.asarray(a) - np.asarray(b)).max()
+    assert d <= rel * scale, d
+
+
+def sparse_instance(n, A, K, seed, dtype=np.float32, gamma=0.99):
+    rp, col, val, c = gen.sparse(n, A, K, seed, dtype=dtype)
+    m = oracle.MDP(n, A, gamma, c, row_ptr=rp, col=col, val=val)
+    prob = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma)
+    return m, prob
+
+
+def grid_instance(N, dtype=np.float32, gamma=0.95):
+    rp, col, val, c = gen.grid(N, dtype=dtype)
+    n = N * N
+    m = oracle.MDP(n, 4, gamma, c, row_ptr=rp, col=col, val=val)
+    prob = rmb.Problem.csr(n, 4, tdev(rp), tdev(col), tdev(val), tdev(c), gamma)
+    return m, prob
+
+
+def ragged_instance(n, A, seed, gamma=0.9):
+    """General CSR with 1..40 successors per row (strided mode, row_ptr path)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 41, n * A)
+    rp = np.zeros(n * A + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.random(rp[-1]) + 0.01
+    for r in range(n * A):
+        val[rp[r]:rp[r + 1]] /= val[rp[r]:rp[r + 1]].sum()
+    c = rng.random((n, A))
+    m = oracle.MDP(n, A, gamma, c, row_ptr=rp, col=col, val=val)
+    prob = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma, validate=True)
+    return m, prob
+
+
+def qgap(m, V):
+    P = m.to_dense64() if m.n <= 3000 else None
+    if P is None:
+        return None
+    Q = m.c.astype(np.float64) + m.gamma * np.einsum("saj,j->sa", P, V)
+    s = np.sort(Q, 1)
+    return (s[:, 1] - s[:, 0]) / np.maximum(1.0, np.abs(s[:, 0]))
+
+
+INSTANCES = {
+    "ell32": lambda: sparse_instance(1500, 8, 32, 3),
+    "ell32_f64": lambda: sparse_instance(900, 5, 32, 4, dtype=np.float64, gamma=0.9),
+    "ell12": lambda: sparse_instance(700, 3, 12, 5, gamma=0.9),
+    "grid": lambda: grid_instance(20),
+    "ragged": lambda: ragged_instance(400, 6, 6),
+}
+
+
+@pytest.mark.parametrize("name", list(INSTANCES))
+@pytest.mark.parametrize("bfrac", [0, 0.013, 0.25, 1.0])
+@pytest.mark.parametrize("policy", [False, True])
+def test_apply_matches_oracle(name, bfrac, policy):
+    m, prob = INSTANCES[name]()
+    b = max(1, int(round(bfrac * m.n)))
+    rng = np.random.default_rng(b)
+    V0 = rng.standard_normal(m.n) * 2
+    pi = rng.integers(0, m.A, m.n).astype(np.int32) if policy else None
+    Vg, argg, rg = prob.apply(b, 9, 4, tdev(V0), pi=tdev(pi) if policy else None)
+    Vo, argo, ro = oracle.sweep(m, V0, b, oracle.partition(m.n, 9, 4), pi)
+    assert_close(Vg.cpu().numpy(), Vo, 1e-11)
+    assert abs(rg - ro) <= 1e-11 * max(1.0, np.abs(Vo).max())
+    gap = qgap(m, Vo)
+    mask = gap > 1e-6 if gap is not None else np.ones(m.n, bool)
+    assert np.array_equal(argg.cpu().numpy()[mask], argo[mask])
+
+
+@pytest.mark.parametrize("b", [1, 50, 1500])
+def test_config3_shape_vi(b):
+    m, prob = sparse_instance(1500, 8, 32, 7)
+    sol = prob.vi(b, seed=2, eps=1e-6, max_sweeps=60)
+    ref = oracle.vi(m, b, seed=2, eps=1e-6, max_sweeps=60)
+    assert sol.stats.sweeps == ref.sweeps
+    assert_close(sol.trace, ref.trace, 1e-10)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-10)
+
+
+@pytest.mark.parametrize("b,msweeps", [(1, 10), (25, 10), (400, 10), (400, 1)])
+def test_config4_shape_mpi(b, msweeps):
+    """Gridworld (config 4 law) at 20 x 20, MPI m = 10 (and m = 1)."""
+    m, prob = grid_instance(20)
+    sol = prob.mpi(b, msweeps, seed=1, eps=1e-8)
+    ref = oracle.mpi(m, b, msweeps, seed=1, eps=1e-8)
+    assert sol.status == rmb.OK and ref.status == oracle.OK
+    assert sol.stats.outer_iters == ref.outer
+    assert_close(sol.trace, ref.trace, 1e-9)
+    assert np.array_equal(sol.changed, ref.changed)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    gap = qgap(m, ref.V)
+    assert np.array_equal(sol.pi.cpu().numpy()[gap > 1e-6], ref.pi[gap > 1e-6])
+
+
+def test_ragged_vi_and_improve():
+    m, prob = ragged_instance(300, 4, 11)
+    sol = prob.vi(17, seed=3, eps=1e-9)
+    ref = oracle.vi(m, 17, seed=3, eps=1e-9)
+    assert sol.status == rmb.OK and abs(sol.stats.sweeps - ref.sweeps) <= 1
+    k = min(sol.stats.sweeps, ref.sweeps)
+    assert_close(sol.trace[:k], ref.trace[:k], 1e-9)
+    V = np.random.default_rng(0).standard_normal(300)
+    pig = tdev(np.zeros(300, np.int32))
+    _, r, ch = prob.improve(tdev(V), pig)
+    pio, ro, cho = oracle.improve(m, V, np.zeros(300, np.int32))
+    assert np.array_equal(pig.cpu().numpy(), pio) and ch == cho and abs(r - ro) < 1e-11 * max(1, np.abs(V).max())
+
+
+def test_sparse_device_generator_instance_equals_host():
+    rp, col, val, c = rmb.generate_sparse(3000, 8, 32, 1)
+    prob = rmb.Problem.csr(3000, 8, rp, col, val, c, 0.99)
+    m, _ = sparse_instance(3000, 8, 32, 1)
+    sol = prob.vi(300, seed=5, eps=1e-6, max_sweeps=25)
+    ref = oracle.vi(m, 300, seed=5, eps=1e-6, max_sweeps=25)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-10)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("b", [1_000_000, 125_000, 4096])
+def test_config3_full_size_sampled(b):
+    """BASELINE config 3 at full size (10^6 x 8 x 32, fp32, generated on device),
+    one application at the launch configuration of the solver; 64 sampled
+    states recomputed by the oracle from host-generated rows and the interim V."""
+    n, A, K, gamma = 1_000_000, 8, 32, 0.99
+    rp, col, val, c = rmb.generate_sparse(n, A, K, 1)
+    prob = rmb.Problem.csr(n, A, rp, col, val, c, gamma)
+    V0 = np.random.default_rng(0).random(n) * 50
+    V1, arg, r = prob.apply(b, 3, 2, tdev(V0))
+    V1, arg = V1.cpu().numpy(), arg.cpu().numpy()
+    perm = oracle.partition(n, 3, 2)
+    pos = np.empty(n, np.int64)
+    pos[perm] = np.arange(n)
+    bat = pos // b
+    for s in np.random.default_rng(b).choice(n, 64, replace=False):
+        Vint = np.where(bat < bat[s], V1, V0)
+        hrp, hcol, hval, hc = gen.sparse(n, A, K, 1, rows=(s, s + 1))
+        q, a = oracle.backup_csr_row(n, hrp, hcol, hval, hc[0], gamma, Vint)
+        assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
+        assert arg[s] == a
+    assert r == np.abs(V1 - V0).max()
+
+
+@pytest.mark.slow
+def test_config4_full_size_sampled_eval():
+    """BASELINE config 4 grid (2048^2 states) one B_{pi,b} application, b = 65536."""
+    N, b, gamma = 2048, 65536, 0.95
+    n = N * N
+    rp, col, val, c = rmb.generate_grid(N)
+    prob = rmb.Problem.csr(n, 4, rp, col, val, c, gamma)
+    rng = np.random.default_rng(0)
+    V0 = rng.random(n) * 20
+    pi = rng.integers(0, 4, n).astype(np.int32)
+    V1, _, r = prob.apply(b, 5, 7, tdev(V0), pi=tdev(pi))
+    V1 = V1.cpu().numpy()
+    perm = oracle.partition(n, 5, 7)
+    pos = np.empty(n, np.int64)
+    pos[perm] = np.arange(n)
+    bat = pos // b
+    for s in rng.choice(n, 64, replace=False):
+        Vint = np.where(bat < bat[s], V1, V0)
+        hrp, hcol, hval, hc = gen.grid(N, rows=(s, s + 1))
+        q, _ = oracle.backup_csr_row(n, hrp, hcol, hval, hc[0], gamma, Vint, pi_a=int(pi[s]))
+        assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
