@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -50,6 +51,7 @@ struct Plan {
     int Lc;         // chunk length (elements)
     int C;          // chunks per row
     int redundant;  // 1: every CTA reduces every state (single barrier)
+    int cta;        // 1: CTA-cooperative tile pipeline, 0: warp-owned items
 };
 
 struct DenseArgs {
@@ -349,7 +351,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
 // five tiles ahead, with their state id / costs prefetched into a smem ring.
 constexpr int kRing = 8;
 constexpr int kAhead = 5;  // tiles grabbed ahead (> D + 1)
-constexpr int kD = 3;      // slots in flight per thread
+constexpr int kD = 2;      // slots in flight per thread
 
 struct TileRing {
     long long it[kRing];  // item index, -1 = end
@@ -359,41 +361,61 @@ struct TileRing {
     long long j0[kRing];
     int nvec[kRing];
     double cost[kRing][kAG];
-    double red[2][kWarps][kAG];
+    double red[kRing][kWarps][kAG];
+    volatile int ready[kRing];   // tile number whose descriptor the slot holds
+    int arrive[kRing];           // warps done with the slot's tile
 };
 
 template <typename PT, bool EVAL>
-__device__ __forceinline__ void tile_grab(const DenseArgs& a, TileRing& tr, int slot, unsigned int* ctr,
+__device__ __forceinline__ void tile_grab(const DenseArgs& a, TileRing& tr, int q, unsigned int* ctr,
                                           const uint32_t* perm, const int32_t* pis, int64_t lo, int64_t items,
-                                          int64_t per_state, int C, int64_t Lc, int VE, int U2)
+                                          int64_t per_state, int C, int64_t Lc, int VE, int U2,
+                                          long long fixed_it = -1)
 {
-    const long long it = (long long)atomicAdd(ctr, 1u);
+    // Grabs happen in tile order (grab(q) finishes inside epilogue(q-kAhead),
+    // before tile q-kAhead+1 can complete and trigger grab(q+1)), so the item
+    // indices a CTA receives increase with q and "end" is monotone.
+    const int slot = q & (kRing - 1);
+    const long long it = fixed_it >= 0 ? fixed_it : (long long)atomicAdd(ctr, 1u);
     if (it >= items) {
         tr.it[slot] = -1;
-        return;
+    } else {
+        const int64_t i = it / per_state;
+        const int rr = (int)(it - i * per_state);
+        const int ag = rr / C;
+        const int ch = rr - ag * C;
+        const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+        const int a0 = EVAL ? pis[s] : ag * kAG;
+        const int na = EVAL ? 1 : min(kAG, a.A - a0);
+        const int64_t j0 = (int64_t)ch * Lc;
+        const int64_t j1 = min(a.n, j0 + Lc);
+        const int nvec = (int)((j1 - j0) / VE);
+        tr.it[slot] = it;
+        tr.s[slot] = s;
+        tr.i[slot] = i;
+        tr.a0[slot] = a0;
+        tr.na[slot] = na;
+        tr.ch[slot] = ch;
+        tr.j0[slot] = j0;
+        tr.nvec[slot] = nvec;
+        tr.R[slot] = max(1, (nvec + kThreads * U2 - 1) / (kThreads * U2));
+        for (int g = 0; g < kAG; ++g) tr.cost[slot][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
     }
-    const int64_t i = it / per_state;
-    const int rr = (int)(it - i * per_state);
-    const int ag = rr / C;
-    const int ch = rr - ag * C;
-    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-    const int a0 = EVAL ? pis[s] : ag * kAG;
-    const int na = EVAL ? 1 : min(kAG, a.A - a0);
-    const int64_t j0 = (int64_t)ch * Lc;
-    const int64_t j1 = min(a.n, j0 + Lc);
-    const int nvec = (int)((j1 - j0) / VE);
-    tr.it[slot] = it;
-    tr.s[slot] = s;
-    tr.i[slot] = i;
-    tr.a0[slot] = a0;
-    tr.na[slot] = na;
-    tr.ch[slot] = ch;
-    tr.j0[slot] = j0;
-    tr.nvec[slot] = nvec;
-    tr.R[slot] = max(1, (nvec + kThreads * U2 - 1) / (kThreads * U2));
-    for (int g = 0; g < kAG; ++g) tr.cost[slot][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
+    __threadfence_block();
+    tr.ready[slot] = q;
 }
 
+// ------------------------------------------------- CTA tile pipeline
+// A TILE = (state i, group of NG action rows, column chunk) is streamed by all
+// 512 threads of the CTA (thread t takes vectors t, t+512, ...), so it
+// completes ~16x sooner than a warp-owned item and the end-of-batch tail
+// shrinks accordingly.  Each thread keeps kD slots of 4 vector loads in flight
+// and keeps issuing across tile boundaries.  There is no CTA-wide barrier per
+// tile: each warp adds its warp-sum to the tile's smem slot and bumps the
+// slot's arrival counter; the 16th warp to arrive sums the 16 warp partials in
+// warp order (reproducible), emits the tile result, and grabs the tile kAhead
+// positions later from the global work-stealing counter (its dependent loads
+// — state id, costs — land long before anyone needs them).
 template <typename PT, int VE, bool EVAL>
 __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
                                   int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
@@ -411,86 +433,133 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
     const int64_t per_state = (int64_t)NAG * C;
     const int64_t items = cnt * per_state;
     const PT* P = static_cast<const PT*>(a.P);
+    const int64_t rowvec = a.n / VE;  // row stride in vectors
 
-    __syncthreads();  // previous phase's readers of tr are done
-    if (tid == 0)
-        for (int q = 0; q < kAhead; ++q)
-            tile_grab<PT, EVAL>(a, tr, q, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2);
+    __shared__ long long s_base;
+    __syncthreads();  // the previous phase is done with tr
+    if (tid < kRing) {
+        tr.arrive[tid] = 0;
+        tr.ready[tid] = -1;  // stale tile numbers of the previous phase must not match
+    }
+    if (tid == 0) s_base = (long long)atomicAdd(ctr, (unsigned int)kAhead);  // tiles 0..kAhead-1: consecutive items
     __syncthreads();
+    if (lane == 0 && warp < kAhead)
+        tile_grab<PT, EVAL>(a, tr, warp, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2,
+                            s_base + warp < items ? s_base + warp : items);
+    __syncthreads();
+
+    // Readers spin on the slot's ready flag and read the fields with volatile
+    // shared loads (in order per thread); no fence here — a fence would drain
+    // this thread's in-flight P loads at every tile boundary.
+    auto wait_ready = [&](int q) -> int {
+        const int sl = q & (kRing - 1);
+        while (tr.ready[sl] != q) {
+        }
+        return sl;
+    };
+    const volatile TileRing& vt = tr;
+    constexpr int kStep = kThreads * U2;  // vectors per thread-slot advance
+
+    // issue side: per-row running pointers and remaining-vector count
+    const VT* ip[NG];
+    int ileft = 0, ina = 0, islots = 0, iq = 0;
+    bool ilive = false;
+    auto begin_issue = [&](int q) {
+        const int sl = wait_ready(q);
+        ilive = vt.it[sl] >= 0;
+        if (!ilive) return;
+        const VT* row = reinterpret_cast<const VT*>(P + (vt.s[sl] * a.A + vt.a0[sl]) * a.n + vt.j0[sl]) + tid;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) ip[g] = row + (int64_t)g * rowvec;
+        ileft = vt.nvec[sl] - tid;
+        ina = vt.na[sl];
+        islots = vt.R[sl];
+    };
+    // consume side: smem V index and remaining-vector count
+    int cvo = 0, cleft = 0, cna = 0, cslots = 0, cq = 0;
+    bool clive = false;
+    auto begin_consume = [&](int q) {
+        const int sl = wait_ready(q);
+        clive = vt.it[sl] >= 0;
+        if (!clive) return;
+        cvo = (int)vt.j0[sl] + tid * VE;
+        cleft = vt.nvec[sl] - tid;
+        cna = vt.na[sl];
+        cslots = vt.R[sl];
+    };
 
     VT buf[kD][kAG];
     double acc[NG];
 #pragma unroll
     for (int g = 0; g < NG; ++g) acc[g] = 0.0;
-    int cq = 0, cr = 0;  // consume position (tile, slot)
-    int iq = 0, ir = 0;  // issue position
+    begin_issue(0);
+    begin_consume(0);
 
     auto issue = [&](VT (&b)[kAG]) {
-        const int sl = iq & (kRing - 1);
-        if (tr.it[sl] < 0) return;
-        const VT* row = reinterpret_cast<const VT*>(P + (tr.s[sl] * a.A + tr.a0[sl]) * a.n + tr.j0[sl]);
-        const int nv = tr.nvec[sl], na = tr.na[sl];
+        if (!ilive) return;
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
-            const int v = tid + kThreads * (U2 * ir + u);
+            const bool ok = ileft > kThreads * u;
 #pragma unroll
             for (int g = 0; g < NG; ++g)
-                if (g < na && v < nv) b[u * NG + g] = ld_stream(row + (int64_t)g * (a.n / VE) + v);
+                if (ok && g < ina) b[u * NG + g] = ld_stream(ip[g] + kThreads * u);
         }
-        if (++ir == tr.R[sl]) ++iq, ir = 0;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) ip[g] += kStep;
+        ileft -= kStep;
+        if (--islots == 0) begin_issue(++iq);
     };
     auto consume = [&](const VT (&b)[kAG]) {
-        const int sl = cq & (kRing - 1);
-        const int nv = tr.nvec[sl], na = tr.na[sl];
-        const int64_t j0 = tr.j0[sl];
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
-            const int v = tid + kThreads * (U2 * cr + u);
-            if (v < nv) {
+            if (cleft > kThreads * u) {
                 double vs[VE];
-                load_v<VE>(Vs, j0 + (int64_t)v * VE, vs);
+                load_v<VE>(Vs, cvo + kThreads * VE * u, vs);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
-                    if (g < na) {
-                        double p[VE];
-                        Vec<PT, VE>::get(b[u * NG + g], p);
+                    if (g < cna) {
+                        double pv[VE];
+                        Vec<PT, VE>::get(b[u * NG + g], pv);
 #pragma unroll
-                        for (int e = 0; e < VE; ++e) acc[g] = fma(p[e], vs[e], acc[g]);
+                        for (int e = 0; e < VE; ++e) acc[g] = fma(pv[e], vs[e], acc[g]);
                     }
                 }
             }
         }
+        cvo += kStep * VE;
+        cleft -= kStep;
     };
-    // tile cq fully consumed: join the warp sums, emit, grab ahead
     auto finalize = [&]() {
         const int sl = cq & (kRing - 1);
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             const double w = warp_sum(acc[g]);
-            if (lane == 0) tr.red[cq & 1][warp][g] = w;
+            if (lane == 0) tr.red[sl][warp][g] = w;
             acc[g] = 0.0;
         }
-        __syncthreads();
-        if (warp == 0) {
-            double tot[NG];
-#pragma unroll
-            for (int g = 0; g < NG; ++g) {
-                tot[g] = 0.0;
-                for (int w = 0; w < kWarps; ++w) tot[g] += tr.red[cq & 1][w][g];
-            }
-            const int64_t i = tr.i[sl];
-            const int a0 = tr.a0[sl], na = tr.na[sl], ch = tr.ch[sl];
+        // shared-memory stores and atomics of one thread are performed in
+        // order; the last arriver reads the partials with volatile loads
+        int last = 0;
+        if (lane == 0) last = atomicAdd(&tr.arrive[sl], 1) == kWarps - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {  // this warp runs the tile's epilogue
+            const int64_t i = vt.i[sl];
+            const int a0 = vt.a0[sl], na = vt.na[sl], ch = vt.ch[sl];
             if (lane == 0) {
+                double tot[NG];
+                for (int g = 0; g < NG; ++g) {
+                    tot[g] = 0.0;
+                    for (int w = 0; w < kWarps; ++w) tot[g] += vt.red[sl][w][g];
+                }
                 if (C == 1) {
                     if (EVAL) {
-                        part[i] = tr.cost[sl][0] + a.gamma * tot[0];
+                        part[i] = vt.cost[sl][0] + a.gamma * tot[0];
                     } else {
                         double best = 0.0;
                         int barg = a0;
-#pragma unroll
                         for (int g = 0; g < NG; ++g)
                             if (g < na) {
-                                const double Q = tr.cost[sl][g] + a.gamma * tot[g];
+                                const double Q = vt.cost[sl][g] + a.gamma * tot[g];
                                 if (g == 0 || Q < best) best = Q, barg = a0 + g;
                             }
                         part[2 * (i * NAG + a0 / kAG)] = best;
@@ -499,7 +568,6 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
                 } else if (EVAL) {
                     part[i * C + ch] = tot[0];
                 } else {
-#pragma unroll
                     for (int g = 0; g < NG; ++g)
                         if (g < na) part[(i * a.A + a0 + g) * C + ch] = tot[g];
                 }
@@ -519,30 +587,32 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
                     prev = __shfl_sync(0xffffffffu, prev, 0);
                     if (prev == (unsigned int)(per_state - 1)) {
                         __threadfence();
-                        finish_state_warp<PT, EVAL>(a, part, C, i, tr.s[sl], a0);
+                        finish_state_warp<PT, EVAL>(a, part, C, i, vt.s[sl], a0);
                         if (lane == 0) a.scnt[i] = 0u;
                     }
                 }
             }
-            if (lane == 0)
-                tile_grab<PT, EVAL>(a, tr, (cq + kAhead) & (kRing - 1), ctr, perm, pis, lo, items, per_state, C,
-                                    Lc, VE, U2);
+            if (lane == 0) {
+                tr.arrive[sl] = 0;
+                tile_grab<PT, EVAL>(a, tr, cq + kAhead, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2);
+            }
+            __syncwarp();
         }
-        ++cq;
-        cr = 0;
+        begin_consume(++cq);
     };
 
 #pragma unroll
     for (int d = 0; d < kD; ++d) issue(buf[d]);
-    while (tr.it[cq & (kRing - 1)] >= 0) {
+    while (clive) {
 #pragma unroll
         for (int d = 0; d < kD; ++d) {
-            if (tr.it[cq & (kRing - 1)] < 0) break;
+            if (!clive) break;
             consume(buf[d]);
             issue(buf[d]);
-            if (++cr == tr.R[cq & (kRing - 1)]) finalize();
+            if (--cslots == 0) finalize();
         }
     }
+    __syncthreads();  // every tile's epilogue is complete
 }
 
 struct PhaseAcc {
@@ -668,7 +738,7 @@ __device__ __forceinline__ void timed_sync(Ctx& x)
 }
 
 // One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
-template <typename PT, int VE, int KIND>
+template <typename PT, int VE, int KIND, bool CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
                           int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
 {
@@ -677,7 +747,10 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     // the other parity's work counter was last used before the previous
     // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
-    compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+    if constexpr (CTA)
+        compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+    else
+        compute_phase<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
@@ -736,7 +809,7 @@ __device__ PhaseAcc block_reduce(PhaseAcc v)
 }
 
 // One application of B_b (EVAL = false) or B_{pi,b} (EVAL = true), sweep k.
-template <typename PT, int VE, bool EVAL>
+template <typename PT, int VE, bool EVAL, bool CTA>
 __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, int64_t k, double* Qs)
 {
     const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
@@ -744,25 +817,25 @@ __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* p
     PhaseAcc acc{0.0, 0, 0};
     for (int64_t lo = 0; lo < a.n; lo += a.b) {
         const int64_t cnt = min(a.b, a.n - lo);
-        run_batch<PT, VE, EVAL ? 1 : 0>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
+        run_batch<PT, VE, EVAL ? 1 : 0, CTA>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
                                          (lo == 0 && !a.identity) ? k + 1 : 0);
         ++x.batches;
     }
     return block_reduce(acc);
 }
 
-template <typename PT, int VE>
+template <typename PT, int VE, bool CTA>
 __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, double* Qs)
 {
     PhaseAcc acc{0.0, 0, 0};
     for (int64_t lo = 0; lo < a.n; lo += a.imp_sub) {
         const int64_t cnt = min(a.imp_sub, a.n - lo);
-        run_batch<PT, VE, 2>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
+        run_batch<PT, VE, 2, CTA>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
     }
     return block_reduce(acc);
 }
 
-template <typename PT, int VE>
+template <typename PT, int VE, bool CTA>
 __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -796,8 +869,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
         const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
         while (it < iters) {
-            PhaseAcc r = a.mode == MODE_APPLY_PI ? run_sweep<PT, VE, true>(a, x, Vs, pis, k, Qs)
-                                                 : run_sweep<PT, VE, false>(a, x, Vs, pis, k, Qs);
+            PhaseAcc r = a.mode == MODE_APPLY_PI ? run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs)
+                                                 : run_sweep<PT, VE, false, CTA>(a, x, Vs, pis, k, Qs);
             if (lead && it < a.trace_len) a.trace[it] = r.rmax;
             ++it;
             ++k;
@@ -807,27 +880,27 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
         }
         if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
     } else if (a.mode == MODE_IMPROVE) {
-        PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+        PhaseAcc r = run_improve<PT, VE, CTA>(a, x, Vs, pis, Qs);
         last = r.rmax;
         changed = r.changed;
         status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
     } else {  // MODE_MPI
         bool bad = false;
         if (!a.pi_given) {
-            PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+            PhaseAcc r = run_improve<PT, VE, CTA>(a, x, Vs, pis, Qs);
             bad = r.bad;
         }
         while (!bad && outer < a.max_iter) {
             const int64_t row = outer * (a.msweeps + 1);
             for (int e = 0; e < a.msweeps && !bad; ++e) {
-                PhaseAcc r = run_sweep<PT, VE, true>(a, x, Vs, pis, k, Qs);
+                PhaseAcc r = run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
                 ++k;
                 ++it;
                 bad = r.bad;
             }
             if (bad) { ++outer; break; }
-            PhaseAcc r = run_improve<PT, VE>(a, x, Vs, pis, Qs);
+            PhaseAcc r = run_improve<PT, VE, CTA>(a, x, Vs, pis, Qs);
             if (lead && row + a.msweeps < a.trace_len) a.trace[row + a.msweeps] = r.rmax;
             if (lead && outer < a.chg_len) a.chg[outer] = r.changed;
             ++outer;
@@ -865,9 +938,17 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     const int64_t maxC = std::max<int64_t>(1, (n + unit - 1) / unit);
     const int64_t lc_target = std::max<int64_t>(unit, (int64_t(16) << 10) / ((int64_t)ng * psz));
     int64_t c = 1;
+    static const bool use_cta = [] {
+        const char* e = getenv("RMB_DENSE_CTA");
+        return e && e[0] == '1';
+    }();
     if (allow_split && rows < 16LL * num_sms) {
         (void)lc_target;
         c = (32LL * num_sms + rows - 1) / rows;
+        if (use_cta) {  // CTA tiles: at least one full slot (512 threads x 4 vectors) per tile
+            const int64_t min_lc = (int64_t)kThreads * VE * (kAG / ng);
+            c = std::min<int64_t>(c, std::max<int64_t>(1, n / min_lc));
+        }
         // bound the partial-sum scratch (A_eff * C doubles per state) to 64 MB
         c = std::min<int64_t>(c, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, cnt * A_eff)));
         c = std::min(std::max<int64_t>(c, 1), maxC);
@@ -879,6 +960,7 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     p.C = (int)((n + L - 1) / L);
     const int64_t per_state = p.C == 1 ? (A_eff == 1 ? 1 : 2 * groups_per_state) : (int64_t)A_eff * p.C;
     p.redundant = cnt * per_state <= kRedundantMax ? 1 : 0;
+    p.cta = use_cta ? 1 : 0;
     return p;
 }
 
@@ -890,7 +972,7 @@ static int64_t plan_doubles(const Plan& p, int64_t cnt, int64_t groups_per_state
 template <typename PT, int VE>
 static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaStream_t st)
 {
-    auto kern = dense_solver_kernel<PT, VE>;
+    auto kern = a.plan[0].cta ? dense_solver_kernel<PT, VE, true> : dense_solver_kernel<PT, VE, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -911,7 +993,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE;
     const int64_t n_pad = (n + 1) & ~int64_t(1);
     const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
-    if (smem_v + 2048 > pr.smem_optin) {
+    if (smem_v + 12288 > pr.smem_optin) {
         set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
                   " B of shared memory for V (limit " + std::to_string(pr.smem_optin) +
                   "); column panels for larger dense n are not in this build");
@@ -939,7 +1021,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     const int sms = pr.num_sms;
     // smem scratch for split-row (S-mode) reductions: up to 32 KB after V / pi
     a.qs_off = (int64_t)smem_v;
-    a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 2048) / 8);
+    a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 12288) / 8);
     const size_t smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
     const bool split_ok = a.qs_cap >= pr.A;  // else every row stays whole (C = 1)
     a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok, kAG, psz);
