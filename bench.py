@@ -163,6 +163,40 @@ def run_reference(args):
     return 0
 
 
+def other_configs(rmb, torch, dev):
+    """Secondary lines: BASELINE config 3 (sparse 10^6 x 8 x 32, MB-VI b = n/8)
+    and config 4 (2048^2 gridworld, MB-MPI m = 10, b = 65536), one solve each."""
+    out = []
+    n, A, K = 1_000_000, 8, 32
+    rp, col, val, c = rmb.generate_sparse(n, A, K, 1)
+    prob = rmb.Problem.csr(n, A, rp, col, val, c, 0.99)
+    prob.vi(n // 8, seed=0, eps=1e-6, max_sweeps=3)
+    sol = prob.vi(n // 8, seed=0, eps=1e-6, max_sweeps=100_000)
+    st = sol.stats
+    bps = n * A * K * 8 + n * A * 4 + 16 * n
+    out.append({"workload": "config 3: sparse random |S|=1e6 |A|=8 K=32 (ELL fp32), gamma=0.99, MB-VI b=n/8 to eps=1e-6",
+                "status": int(sol.status), "sweeps": st.sweeps, "time_to_eps_ms": st.seconds * 1e3,
+                "backups_per_s": st.sweeps * n * A / st.seconds,
+                "hbm_algorithmic_GB_per_s": st.sweeps * bps / st.seconds / 1e9,
+                "note": "L2-gather bound: one random 8-byte V gather (a 32-byte L2 sector) per nonzero"})
+    del prob, rp, col, val, c
+    torch.cuda.empty_cache()
+    N = 2048
+    n = N * N
+    rp, col, val, c = rmb.generate_grid(N)
+    prob = rmb.Problem.csr(n, 4, rp, col, val, c, 0.95)
+    prob.mpi(65536, 10, seed=0, eps=1e-6, max_outer=2)
+    sol = prob.mpi(65536, 10, seed=0, eps=1e-6, max_outer=100_000)
+    st = sol.stats
+    backups = st.sweeps * n + (st.outer_iters + 1) * n * 4
+    out.append({"workload": "config 4: 2048x2048 slip gridworld, gamma=0.95, MB-MPI m=10 b=65536 to eps=1e-6",
+                "status": int(sol.status), "outer_iterations": st.outer_iters, "eval_sweeps": st.sweeps,
+                "time_to_eps_ms": st.seconds * 1e3, "backups_per_s": backups / st.seconds})
+    del prob, rp, col, val, c
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -174,6 +208,7 @@ def main():
     ap.add_argument("--no-bsweep", action="store_true", help="skip the per-b time-to-eps table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the config 3 / 4 secondary lines")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -241,6 +276,13 @@ def main():
     value = sweeps_all * N_STATES * N_ACTIONS / t
 
     peak, peak_src = peaks()
+    traffic = None
+    try:  # DRAM bytes per sweep of the solver kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_per_sweep"] * sweeps / args.steps  # per launch (= one solve)
+    except Exception:
+        pass
     bps = algo_bytes_per_sweep(N_STATES, N_ACTIONS, 4, args.b)
     achieved = sweeps * bps / kernel_s / 1e9  # per launch = whole solve kernel
     result = {
@@ -251,7 +293,10 @@ def main():
                    "l2": "inputs larger than L2 (P 6.4 GB) + 256 MB flush between solves",
                    "parallelism": f"replicas{world}" if world > 1 else "dp1"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": "dram read+write bytes per launch = per-sweep DRAM bytes of the committed "
+                                     "ncu --set full capture (profiles/ncu_traffic.json) x sweeps per solve",
+                     "achieved_bytes_per_launch": sweeps * bps / args.steps,
                      "peak_source": peak_src, "kernel": "dense_solver_kernel<float,4>",
                      "algorithmic_bytes_per_sweep": bps},
         "gpu_launches": launches,
@@ -302,6 +347,9 @@ def main():
                          "h2d_bytes_per_step": int(Ph.numel() * 4 + ch.numel() * 4),
                          "d2h_bytes_per_step": int(N_STATES * 8 + N_STATES * 4 + 8 * sw / ksteps),
                          "steps": ksteps, "path": "rmb_create_dense(host P,c) + rmb_vi(host V,pi) + rmb_destroy"}
+
+    if rank == 0 and not args.no_other:
+        result["other_configs"] = other_configs(rmb, torch, dev)
 
     if rank == 0 and not args.no_cpu:
         rate, cores, sample = oracle_sample()

@@ -52,6 +52,7 @@ struct Plan {
     int C;          // chunks per row
     int redundant;  // 1: every CTA reduces every state (single barrier)
     int cta;        // 1: CTA-cooperative tile pipeline, 0: warp-owned items
+    int ng;         // action rows per warp item in min modes (4, or 1 for short-tail batches)
 };
 
 struct DenseArgs {
@@ -186,12 +187,12 @@ __device__ __forceinline__ double load_cost(const DenseArgs& a, int64_t idx)
 // argmin butterfly (lower value, then lower action).
 template <typename PT, bool EVAL>
 __device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const double* part, int C, int64_t i, int64_t s,
-                                                  int act_eval)
+                                                  int act_eval, int ng = kAG)
 {
     const int lane = threadIdx.x & 31;
     if (C == 1) {  // F-mode, NAG > 1 groups
         if (lane == 0) {
-            const int NAG = (a.A + kAG - 1) / kAG;
+            const int NAG = (a.A + ng - 1) / ng;
             const double2* pp = reinterpret_cast<const double2*>(part) + i * NAG;
             double best = 0.0;
             int barg = 0;
@@ -245,19 +246,19 @@ __device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const doub
 //   C == 1, min : part[2(i*NAG+ag)+{0,1}] = (min Q over the group, argmin)   (2*NAG)
 //   C >  1, EVAL: part[i*C + ch]               (C)
 //   C >  1, min : part[(i*A + a)*C + ch]       (A*C)
-template <typename PT, int VE, bool EVAL>
+template <typename PT, int VE, bool EVAL, int NGT>
 __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
                               int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
 {
     const int lane = threadIdx.x & 31;
     const int C = pl.C;
     const int64_t Lc = pl.Lc;
-    const int NAG = EVAL ? 1 : (a.A + kAG - 1) / kAG;
+    constexpr int NG = EVAL ? 1 : NGT;
+    const int NAG = EVAL ? 1 : (a.A + NG - 1) / NG;
     const int64_t per_state = (int64_t)NAG * C;
     const int64_t items = cnt * per_state;
     const PT* P = static_cast<const PT*>(a.P);
-    constexpr int NG = EVAL ? 1 : kAG;
-    constexpr int U = EVAL ? 8 : 2;
+    constexpr int U = NG == 1 ? 8 : 2;
     // dynamic work stealing over the whole grid (balances SMs whose HBM share
     // differs); the next item index is fetched while the current one streams
     auto grab = [&]() -> int64_t {
@@ -273,8 +274,8 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
         const int ag = rr / C;
         const int ch = rr - ag * C;
         const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-        const int a0 = EVAL ? pis[s] : ag * kAG;
-        const int na = EVAL ? 1 : min(kAG, a.A - a0);
+        const int a0 = EVAL ? pis[s] : ag * NG;
+        const int na = EVAL ? 1 : min(NG, a.A - a0);
         const int64_t j0 = (int64_t)ch * Lc;
         const int64_t j1 = min(a.n, j0 + Lc);
         double acc[NG];
@@ -330,7 +331,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
                 prev = __shfl_sync(0xffffffffu, prev, 0);
                 if (prev == (unsigned int)(per_state - 1)) {
                     __threadfence();
-                    finish_state_warp<PT, EVAL>(a, part, C, i, s, a0);
+                    finish_state_warp<PT, EVAL>(a, part, C, i, s, a0, NG);
                     if (lane == 0) a.scnt[i] = 0u;  // rearmed for the next batch (ordered by its barrier)
                 }
             }
@@ -350,8 +351,10 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
 // in flight.  Tiles are taken from a global work-stealing counter by thread 0,
 // five tiles ahead, with their state id / costs prefetched into a smem ring.
 constexpr int kRing = 8;
-constexpr int kAhead = 5;  // tiles grabbed ahead (> D + 1)
-constexpr int kD = 2;      // slots in flight per thread
+constexpr int kD = 1;                      // slots in flight per thread
+constexpr int kSlotLoads = 8;              // vector loads per thread per slot
+constexpr int kCW = kWarps - 1;            // streaming warps (warp kCW is the producer)
+constexpr int kCT = kCW * kWarp;           // streaming threads
 
 struct TileRing {
     long long it[kRing];  // item index, -1 = end
@@ -361,68 +364,33 @@ struct TileRing {
     long long j0[kRing];
     int nvec[kRing];
     double cost[kRing][kAG];
-    double red[kRing][kWarps][kAG];
-    volatile int ready[kRing];   // tile number whose descriptor the slot holds
-    int arrive[kRing];           // warps done with the slot's tile
+    double red[kRing][kCW][kAG];
+    volatile int ready[kRing];    // tile number whose descriptor the slot holds
+    volatile int allowed[kRing];  // next tile number the producer may write into the slot
+    int arrive[kRing];            // streaming warps done with the slot's tile
 };
 
-template <typename PT, bool EVAL>
-__device__ __forceinline__ void tile_grab(const DenseArgs& a, TileRing& tr, int q, unsigned int* ctr,
-                                          const uint32_t* perm, const int32_t* pis, int64_t lo, int64_t items,
-                                          int64_t per_state, int C, int64_t Lc, int VE, int U2,
-                                          long long fixed_it = -1)
-{
-    // Grabs happen in tile order (grab(q) finishes inside epilogue(q-kAhead),
-    // before tile q-kAhead+1 can complete and trigger grab(q+1)), so the item
-    // indices a CTA receives increase with q and "end" is monotone.
-    const int slot = q & (kRing - 1);
-    const long long it = fixed_it >= 0 ? fixed_it : (long long)atomicAdd(ctr, 1u);
-    if (it >= items) {
-        tr.it[slot] = -1;
-    } else {
-        const int64_t i = it / per_state;
-        const int rr = (int)(it - i * per_state);
-        const int ag = rr / C;
-        const int ch = rr - ag * C;
-        const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-        const int a0 = EVAL ? pis[s] : ag * kAG;
-        const int na = EVAL ? 1 : min(kAG, a.A - a0);
-        const int64_t j0 = (int64_t)ch * Lc;
-        const int64_t j1 = min(a.n, j0 + Lc);
-        const int nvec = (int)((j1 - j0) / VE);
-        tr.it[slot] = it;
-        tr.s[slot] = s;
-        tr.i[slot] = i;
-        tr.a0[slot] = a0;
-        tr.na[slot] = na;
-        tr.ch[slot] = ch;
-        tr.j0[slot] = j0;
-        tr.nvec[slot] = nvec;
-        tr.R[slot] = max(1, (nvec + kThreads * U2 - 1) / (kThreads * U2));
-        for (int g = 0; g < kAG; ++g) tr.cost[slot][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
-    }
-    __threadfence_block();
-    tr.ready[slot] = q;
-}
-
 // ------------------------------------------------- CTA tile pipeline
-// A TILE = (state i, group of NG action rows, column chunk) is streamed by all
-// 512 threads of the CTA (thread t takes vectors t, t+512, ...), so it
-// completes ~16x sooner than a warp-owned item and the end-of-batch tail
-// shrinks accordingly.  Each thread keeps kD slots of 4 vector loads in flight
-// and keeps issuing across tile boundaries.  There is no CTA-wide barrier per
-// tile: each warp adds its warp-sum to the tile's smem slot and bumps the
-// slot's arrival counter; the 16th warp to arrive sums the 16 warp partials in
-// warp order (reproducible), emits the tile result, and grabs the tile kAhead
-// positions later from the global work-stealing counter (its dependent loads
-// — state id, costs — land long before anyone needs them).
+// A TILE = (state i, group of NG action rows, column chunk) is streamed by the
+// 480 streaming threads of the CTA together (thread t takes vectors t, t+480,
+// ...), so it completes ~15x sooner than a warp-owned item and the end-of-
+// batch tail shrinks accordingly.  Each streaming thread keeps kD slots of 4
+// vector loads in flight and keeps issuing across tile boundaries.
+// Warp specialisation: warp 15 is the PRODUCER — it takes tiles from the
+// global work-stealing counter (one atomic per tile), resolves the state id
+// and costs, and publishes descriptors into a smem ring up to kRing tiles
+// ahead.  Streaming warps never touch global control data: at the end of a
+// tile each adds its warp sum to the tile's smem slot and bumps the arrival
+// counter; the last arriver sums the 15 partials in warp order (reproducible),
+// writes the tile result and frees the ring slot.  No CTA-wide barrier per tile.
 template <typename PT, int VE, bool EVAL>
 __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
                                   int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
 {
     using VT = typename Vec<PT, VE>::T;
     constexpr int NG = EVAL ? 1 : kAG;
-    constexpr int U2 = kAG / NG;  // vectors per row per slot (4 loads per slot)
+    constexpr int U2 = kSlotLoads / NG;  // vectors per row per slot
+    constexpr int kStep = kCT * U2;
     __shared__ TileRing tr;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -435,22 +403,59 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
     const PT* P = static_cast<const PT*>(a.P);
     const int64_t rowvec = a.n / VE;  // row stride in vectors
 
-    __shared__ long long s_base;
     __syncthreads();  // the previous phase is done with tr
     if (tid < kRing) {
         tr.arrive[tid] = 0;
         tr.ready[tid] = -1;  // stale tile numbers of the previous phase must not match
+        tr.allowed[tid] = tid;
     }
-    if (tid == 0) s_base = (long long)atomicAdd(ctr, (unsigned int)kAhead);  // tiles 0..kAhead-1: consecutive items
-    __syncthreads();
-    if (lane == 0 && warp < kAhead)
-        tile_grab<PT, EVAL>(a, tr, warp, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2,
-                            s_base + warp < items ? s_base + warp : items);
     __syncthreads();
 
+    if (warp == kCW) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            for (int q = 0;; ++q) {
+                const int sl = q & (kRing - 1);
+                while (tr.allowed[sl] != q) {
+                }
+                const long long it = (long long)atomicAdd(ctr, 1u);
+                if (it >= items) {
+                    tr.it[sl] = -1;
+                } else {
+                    const int64_t i = it / per_state;
+                    const int rr = (int)(it - i * per_state);
+                    const int ag = rr / C;
+                    const int ch = rr - ag * C;
+                    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                    const int a0 = EVAL ? pis[s] : ag * kAG;
+                    const int na = EVAL ? 1 : min(kAG, a.A - a0);
+                    const int64_t j0 = (int64_t)ch * Lc;
+                    const int64_t j1 = min(a.n, j0 + Lc);
+                    const int nvec = (int)((j1 - j0) / VE);
+                    tr.it[sl] = it;
+                    tr.s[sl] = s;
+                    tr.i[sl] = i;
+                    tr.a0[sl] = a0;
+                    tr.na[sl] = na;
+                    tr.ch[sl] = ch;
+                    tr.j0[sl] = j0;
+                    tr.nvec[sl] = nvec;
+                    tr.R[sl] = max(1, (nvec + kStep - 1) / kStep);
+                    for (int g = 0; g < kAG; ++g) tr.cost[sl][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
+                }
+                __threadfence_block();
+                tr.ready[sl] = q;
+                if (it >= items) break;
+            }
+        }
+        __syncthreads();
+        return;
+    }
+
+    // ------------------------------------------------ streaming warps
     // Readers spin on the slot's ready flag and read the fields with volatile
-    // shared loads (in order per thread); no fence here — a fence would drain
-    // this thread's in-flight P loads at every tile boundary.
+    // shared loads (in order per thread); no fence — a fence would drain this
+    // thread's in-flight P loads at every tile boundary.
     auto wait_ready = [&](int q) -> int {
         const int sl = q & (kRing - 1);
         while (tr.ready[sl] != q) {
@@ -458,9 +463,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         return sl;
     };
     const volatile TileRing& vt = tr;
-    constexpr int kStep = kThreads * U2;  // vectors per thread-slot advance
 
-    // issue side: per-row running pointers and remaining-vector count
     const VT* ip[NG];
     int ileft = 0, ina = 0, islots = 0, iq = 0;
     bool ilive = false;
@@ -475,7 +478,6 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         ina = vt.na[sl];
         islots = vt.R[sl];
     };
-    // consume side: smem V index and remaining-vector count
     int cvo = 0, cleft = 0, cna = 0, cslots = 0, cq = 0;
     bool clive = false;
     auto begin_consume = [&](int q) {
@@ -488,33 +490,33 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         cslots = vt.R[sl];
     };
 
-    VT buf[kD][kAG];
+    VT buf[kD][kSlotLoads];
     double acc[NG];
 #pragma unroll
     for (int g = 0; g < NG; ++g) acc[g] = 0.0;
     begin_issue(0);
     begin_consume(0);
 
-    auto issue = [&](VT (&b)[kAG]) {
+    auto issue = [&](VT (&b)[kSlotLoads]) {
         if (!ilive) return;
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
-            const bool ok = ileft > kThreads * u;
+            const bool ok = ileft > kCT * u;
 #pragma unroll
             for (int g = 0; g < NG; ++g)
-                if (ok && g < ina) b[u * NG + g] = ld_stream(ip[g] + kThreads * u);
+                if (ok && g < ina) b[u * NG + g] = ld_stream(ip[g] + kCT * u);
         }
 #pragma unroll
         for (int g = 0; g < NG; ++g) ip[g] += kStep;
         ileft -= kStep;
         if (--islots == 0) begin_issue(++iq);
     };
-    auto consume = [&](const VT (&b)[kAG]) {
+    auto consume = [&](const VT (&b)[kSlotLoads]) {
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
-            if (cleft > kThreads * u) {
+            if (cleft > kCT * u) {
                 double vs[VE];
-                load_v<VE>(Vs, cvo + kThreads * VE * u, vs);
+                load_v<VE>(Vs, cvo + kCT * VE * u, vs);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     if (g < cna) {
@@ -540,16 +542,16 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         // shared-memory stores and atomics of one thread are performed in
         // order; the last arriver reads the partials with volatile loads
         int last = 0;
-        if (lane == 0) last = atomicAdd(&tr.arrive[sl], 1) == kWarps - 1;
+        if (lane == 0) last = atomicAdd(&tr.arrive[sl], 1) == kCW - 1;
         last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {  // this warp runs the tile's epilogue
+        if (last) {  // this warp runs the tile's (cheap) epilogue
             const int64_t i = vt.i[sl];
             const int a0 = vt.a0[sl], na = vt.na[sl], ch = vt.ch[sl];
             if (lane == 0) {
                 double tot[NG];
                 for (int g = 0; g < NG; ++g) {
                     tot[g] = 0.0;
-                    for (int w = 0; w < kWarps; ++w) tot[g] += vt.red[sl][w][g];
+                    for (int w = 0; w < kCW; ++w) tot[g] += vt.red[sl][w][g];
                 }
                 if (C == 1) {
                     if (EVAL) {
@@ -594,7 +596,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
             }
             if (lane == 0) {
                 tr.arrive[sl] = 0;
-                tile_grab<PT, EVAL>(a, tr, cq + kAhead, ctr, perm, pis, lo, items, per_state, C, Lc, VE, U2);
+                tr.allowed[sl] = cq + kRing;  // the producer may reuse the slot
             }
             __syncwarp();
         }
@@ -612,7 +614,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
             if (--cslots == 0) finalize();
         }
     }
-    __syncthreads();  // every tile's epilogue is complete
+    __syncthreads();  // pairs with the producer's; every epilogue is complete
 }
 
 struct PhaseAcc {
@@ -625,14 +627,14 @@ struct PhaseAcc {
 // F-mode (C == 1): one thread per state.
 template <bool EVAL>
 __device__ __forceinline__ void reduce_state_F(const DenseArgs& a, const double* part, int64_t i, double& best,
-                                               int& barg)
+                                               int& barg, int ng)
 {
     if (EVAL) {
         best = __ldcg(part + i);
         barg = -1;
         return;
     }
-    const int NAG = (a.A + kAG - 1) / kAG;
+    const int NAG = (a.A + ng - 1) / ng;
     const double2* pp = reinterpret_cast<const double2*>(part) + i * NAG;
     best = 0.0;
     barg = 0;
@@ -660,17 +662,31 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
     const int64_t per_round = max((int64_t)1, a.qs_cap / Ae);
     for (int64_t k0 = 0; k0 < m_all; k0 += per_round) {
         const int64_t m = min(per_round, m_all - k0);
-        for (int64_t q = warp; q < m * Ae; q += kWarps) {
-            const int64_t kk = q / Ae;
-            const int ai = (int)(q - kk * Ae);
-            const int64_t i = first + (k0 + kk) * step;
-            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-            const int act = EVAL ? pis[s] : ai;
-            const double* pp = part + (EVAL ? i : i * a.A + act) * C;
-            double sum = 0.0;
-            for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + ch);
-            sum = warp_sum(sum);
-            if (lane == 0) Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
+        if (C <= 8) {  // many short sums: a thread per (state, action), chunk order
+            for (int64_t q = threadIdx.x; q < m * Ae; q += kThreads) {
+                const int64_t kk = q / Ae;
+                const int ai = (int)(q - kk * Ae);
+                const int64_t i = first + (k0 + kk) * step;
+                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                const int act = EVAL ? pis[s] : ai;
+                const double* pp = part + (EVAL ? i : i * a.A + act) * C;
+                double sum = 0.0;
+                for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + ch);
+                Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
+            }
+        } else {       // few long sums: a warp per (state, action)
+            for (int64_t q = warp; q < m * Ae; q += kWarps) {
+                const int64_t kk = q / Ae;
+                const int ai = (int)(q - kk * Ae);
+                const int64_t i = first + (k0 + kk) * step;
+                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                const int act = EVAL ? pis[s] : ai;
+                const double* pp = part + (EVAL ? i : i * a.A + act) * C;
+                double sum = 0.0;
+                for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + ch);
+                sum = warp_sum(sum);
+                if (lane == 0) Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
+            }
         }
         __syncthreads();
         for (int64_t kk = threadIdx.x; kk < m; kk += kThreads) {
@@ -750,7 +766,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     if constexpr (CTA)
         compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     else
-        compute_phase<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+        compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
@@ -768,7 +784,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
                 double v;
                 int arg;
-                reduce_state_F<EVAL>(a, part, i, v, arg);
+                reduce_state_F<EVAL>(a, part, i, v, arg, pl.ng);
                 patch_state<KIND>(a, Vs, pis, s, v, arg, acc);
             }
         } else {
@@ -946,7 +962,7 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
         (void)lc_target;
         c = (32LL * num_sms + rows - 1) / rows;
         if (use_cta) {  // CTA tiles: at least one full slot (512 threads x 4 vectors) per tile
-            const int64_t min_lc = (int64_t)kThreads * VE * (kAG / ng);
+            const int64_t min_lc = (int64_t)kCT * VE * (kSlotLoads / ng);
             c = std::min<int64_t>(c, std::max<int64_t>(1, n / min_lc));
         }
         // bound the partial-sum scratch (A_eff * C doubles per state) to 64 MB
@@ -1017,21 +1033,28 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
-    const int64_t NAG = (pr.A + kAG - 1) / kAG;
     const int sms = pr.num_sms;
+    // min-mode items are groups of kAG action rows (single-row items were
+    // measured slower at b = 1000: 4x the smem V traffic and per-item atomics)
+    const int ng_b = kAG;
+    const int64_t NAG = (pr.A + ng_b - 1) / ng_b;
     // smem scratch for split-row (S-mode) reductions: up to 32 KB after V / pi
     a.qs_off = (int64_t)smem_v;
     a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 12288) / 8);
     const size_t smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
     const bool split_ok = a.qs_cap >= pr.A;  // else every row stays whole (C = 1)
-    a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok, kAG, psz);
+    a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok, ng_b, psz);
+    a.plan[0].ng = ng_b;
     a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok, 1, psz);
+    a.plan[1].ng = 1;
     // improvement (no V write): as few sub-batches as a bounded scratch allows
-    a.imp_sub = n * NAG * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / (2 * NAG));
-    a.plan[2] = plan_chunks(n, a.imp_sub, NAG, pr.A, VE, sms, split_ok, kAG, psz);
+    const int64_t NAG4 = (pr.A + kAG - 1) / kAG;
+    a.imp_sub = n * NAG4 * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / (2 * NAG4));
+    a.plan[2] = plan_chunks(n, a.imp_sub, NAG4, pr.A, VE, sms, split_ok, kAG, psz);
+    a.plan[2].ng = kAG;
     const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
-                                              plan_doubles(a.plan[2], a.imp_sub, NAG, pr.A)});
+                                              plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A)});
     a.part_stride = (stride + 31) / 32 * 32;
     const int64_t lcap = std::max<int64_t>(rq.b, a.imp_sub);
 

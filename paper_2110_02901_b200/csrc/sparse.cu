@@ -35,7 +35,7 @@
 
 namespace rmb {
 
-constexpr int kSThreads = 1024;
+constexpr int kSThreads = 512;
 constexpr int kSWarps = kSThreads / kWarp;
 
 struct SparseArgs {
@@ -46,7 +46,8 @@ struct SparseArgs {
     int64_t n;
     int A;
     int K;  // > 0: ELL width
-    int GS; // lanes per state (power of two <= 32)
+    int GS; // lanes per state in min modes (power of two <= 32)
+    int GSE;  // lanes per state in B_{pi,b} sweeps
     double gamma;
     double* V;
     int32_t* pi;
@@ -81,14 +82,63 @@ __device__ __forceinline__ double ldv(const void* p, int64_t e)
     return (double)__ldg(static_cast<const PT*>(p) + e);
 }
 
-// Backup of state s against X by a group of GS lanes (g = lane in group).
-// act_fixed >= 0: B_{pi,b} row only.  Result valid in every lane of the group.
-template <typename PT, bool ROWMODE>
-__device__ __forceinline__ void backup_state(const SparseArgs& a, const double* X, int64_t s, int act_fixed, int g,
-                                             bool valid, double& best, int& barg)
+// Layout modes of the sparse backup (chosen on the host from the CSR shape).
+enum SMode : int {
+    SM_STRIDED = 0,  // general CSR: group lanes stride over each row, actions in turn
+    SM_ROW = 1,      // ELL, K <= 8: a lane per action row (bit-exact with the oracle)
+    SM_VEC = 2,      // ELL, K % 8 == 0, A*K/8 a power of two <= 32: 8 consecutive nonzeros per lane
+};
+
+__device__ __forceinline__ int4 ld_nc_int4(const int32_t* p)
 {
-    const int GS = a.GS;
-    if (ROWMODE) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <typename PT>
+__device__ __forceinline__ void ld8(const void* val, int64_t e, double (&v)[8])
+{
+    if constexpr (sizeof(PT) == 4) {
+        const float4 a = ld_stream(reinterpret_cast<const float4*>(static_cast<const float*>(val) + e));
+        const float4 b = ld_stream(reinterpret_cast<const float4*>(static_cast<const float*>(val) + e + 4));
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    } else {
+        const double* d = static_cast<const double*>(val) + e;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 x = ld_stream(reinterpret_cast<const double2*>(d + 2 * q));
+            v[2 * q] = x.x, v[2 * q + 1] = x.y;
+        }
+    }
+}
+
+// (lower value, then lower action) butterfly over lane offsets [o_lo, GS)
+__device__ __forceinline__ void argmin_butterfly(double& Q, int& arg, int o_lo, int GS)
+{
+    for (int o = GS >> 1; o >= o_lo && o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, Q, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        // lane order == action order, so (lower value, then lower index)
+        // reproduces "first strict minimum"; a NaN in the lowest action stays
+        // (as in the oracle, where a NaN Q_0 is never replaced)
+        if (ov < Q || (ov == Q && oa < arg) || (arg == 0x7fffffff && oa != 0x7fffffff)) {
+            Q = ov;
+            arg = oa;
+        }
+    }
+}
+
+// Backup of state s against X by a group of GS lanes (g = lane in group).
+// act_fixed >= 0: B_{pi,b} row only.  Result valid in lane g == 0 (all modes)
+// and in every lane for SM_ROW / SM_VEC min.
+template <typename PT, int MODE>
+__device__ __forceinline__ void backup_state(const SparseArgs& a, const double* X, int64_t s, int act_fixed, int g,
+                                             int GS, bool valid, double& best, int& barg)
+{
+    if (MODE == SM_ROW) {
         double Q = INFINITY;
         int arg = 0x7fffffff;
         const int act = !valid ? -1 : act_fixed >= 0 ? (g == 0 ? act_fixed : -1) : (g < a.A ? g : -1);
@@ -106,17 +156,42 @@ __device__ __forceinline__ void backup_state(const SparseArgs& a, const double* 
             Q = __dadd_rn(ldv<PT>(a.c, row), __dmul_rn(a.gamma, acc));
             arg = act;
         }
-        for (int o = GS >> 1; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, Q, o);
-            const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-            // lane order == action order, so (lower value, then lower index)
-            // reproduces "first strict minimum"; a NaN in lane 0 stays (as in
-            // the oracle, where a NaN Q_0 is never replaced)
-            if (ov < Q || (ov == Q && oa < arg) || (arg == 0x7fffffff && oa != 0x7fffffff)) {
-                Q = ov;
-                arg = oa;
-            }
+        argmin_butterfly(Q, arg, 1, GS);
+        best = Q;
+        barg = arg;
+        return;
+    }
+    if (MODE == SM_VEC) {
+        // lane g owns nonzeros [8g, 8g+8) of the state's block (min) or of the
+        // row pi(s) (eval): 2x128-bit col + 2x128-bit val loads, 8 gathers in
+        // flight, a sequential 8-term sum, then a butterfly over the K/8 lanes
+        // of the action and an argmin butterfly over the actions
+        const int L = a.K >> 3;  // lanes per action row
+        double Q = INFINITY;
+        int arg = 0x7fffffff;
+        if (valid) {
+            const int act = act_fixed >= 0 ? act_fixed : (8 * g) / a.K;
+            const int64_t e = act_fixed >= 0 ? (s * a.A + act_fixed) * a.K + 8 * g : s * a.A * a.K + 8 * g;
+            const int4 c0 = ld_nc_int4(a.col + e);
+            const int4 c1 = ld_nc_int4(a.col + e + 4);
+            double v[8];
+            ld8<PT>(a.val, e, v);
+            const double x0 = __ldcg(X + c0.x), x1 = __ldcg(X + c0.y), x2 = __ldcg(X + c0.z), x3 = __ldcg(X + c0.w);
+            const double x4 = __ldcg(X + c1.x), x5 = __ldcg(X + c1.y), x6 = __ldcg(X + c1.z), x7 = __ldcg(X + c1.w);
+            double acc = v[0] * x0;
+            acc = fma(v[1], x1, acc);
+            acc = fma(v[2], x2, acc);
+            acc = fma(v[3], x3, acc);
+            acc = fma(v[4], x4, acc);
+            acc = fma(v[5], x5, acc);
+            acc = fma(v[6], x6, acc);
+            acc = fma(v[7], x7, acc);
+            Q = acc;
+            arg = act;
         }
+        for (int o = 1; o < L; o <<= 1) Q += __shfl_xor_sync(0xffffffffu, Q, o);
+        if (valid) Q = ldv<PT>(a.c, s * a.A + arg) + a.gamma * Q;
+        if (act_fixed < 0) argmin_butterfly(Q, arg, L, GS);
         best = Q;
         barg = arg;
         return;
@@ -200,11 +275,11 @@ __device__ __forceinline__ SweepResult read_slot(const SparseArgs& a, int slot)
 }
 
 // One application of B_b (EVAL false) or B_{pi,b} (EVAL true), sweep k.
-template <typename PT, bool ROWMODE, bool EVAL>
+template <typename PT, int MODE, bool EVAL>
 __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const int32_t* pol)
 {
     const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
-    const int GS = a.GS;
+    const int GS = EVAL ? a.GSE : a.GS;
     const int g = threadIdx.x & (GS - 1);
     // warp-uniform trip counts: all 32 lanes stay in the loop for the shuffles
     const int64_t ngroups = (int64_t)gridDim.x * (kSThreads / GS);
@@ -233,7 +308,7 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
             const int64_t s = !valid ? 0 : bperm ? (int64_t)__ldg(bperm + lo + i) : lo + i;
             double v;
             int arg;
-            backup_state<PT, ROWMODE>(a, Xc, s, EVAL ? pol[s] : -1, g, valid, v, arg);
+            backup_state<PT, MODE>(a, Xc, s, EVAL && valid ? pol[s] : (EVAL ? 0 : -1), g, GS, valid, v, arg);
             if (valid && g == 0) {
                 const double old = __ldcg(Xc + s);
                 rmax = fmax(rmax, fabs(v - old));
@@ -285,7 +360,7 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
 
 // Policy improvement over all states against X_cur (no X write):
 // pw_next = greedy, changed vs pw_cur, ||TV - V||_inf.
-template <typename PT, bool ROWMODE>
+template <typename PT, int MODE>
 __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx, const int32_t* pcur, int32_t* pnext,
                                    bool count_changed)
 {
@@ -306,7 +381,7 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
         const bool valid = s < a.n;
         double v;
         int arg;
-        backup_state<PT, ROWMODE>(a, Xc, valid ? s : 0, -1, g, valid, v, arg);
+        backup_state<PT, MODE>(a, Xc, valid ? s : 0, -1, g, GS, valid, v, arg);
         if (valid && g == 0) {
             rmax = fmax(rmax, fabs(v - __ldcg(Xc + s)));
             bad |= !isfinite(v);
@@ -357,7 +432,7 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
     return r;
 }
 
-template <typename PT, bool ROWMODE>
+template <typename PT, int MODE>
 __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const SparseArgs a)
 {
     SCtx x{};
@@ -388,8 +463,8 @@ __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const Spars
     if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
         const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
         while (it < iters) {
-            SweepResult r = a.mode == MODE_APPLY_PI ? run_sweep<PT, ROWMODE, true>(a, x, k, a.pw0)
-                                                    : run_sweep<PT, ROWMODE, false>(a, x, k, nullptr);
+            SweepResult r = a.mode == MODE_APPLY_PI ? run_sweep<PT, MODE, true>(a, x, k, a.pw0)
+                                                    : run_sweep<PT, MODE, false>(a, x, k, nullptr);
             if (lead && it < a.trace_len) a.trace[it] = r.r;
             ++it;
             ++k;
@@ -399,7 +474,7 @@ __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const Spars
         }
         if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
     } else if (a.mode == MODE_IMPROVE) {
-        SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, a.pw0, a.pw1, true);
+        SweepResult r = run_improve<PT, MODE>(a, x, imp++, a.pw0, a.pw1, true);
         pcur = 1;
         last = r.r;
         changed = r.changed;
@@ -407,7 +482,7 @@ __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const Spars
     } else {  // MODE_MPI
         bool bad = false;
         if (!a.pi_given) {
-            SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, a.pw0, a.pw1, false);
+            SweepResult r = run_improve<PT, MODE>(a, x, imp++, a.pw0, a.pw1, false);
             pcur = 1;
             bad = r.bad;
         }
@@ -415,14 +490,14 @@ __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const Spars
             const int64_t row = outer * (a.msweeps + 1);
             const int32_t* pol = pcur ? a.pw1 : a.pw0;
             for (int e = 0; e < a.msweeps && !bad; ++e) {
-                SweepResult r = run_sweep<PT, ROWMODE, true>(a, x, k, pol);
+                SweepResult r = run_sweep<PT, MODE, true>(a, x, k, pol);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.r;
                 ++k;
                 ++it;
                 bad = r.bad;
             }
             if (bad) { ++outer; break; }
-            SweepResult r = run_improve<PT, ROWMODE>(a, x, imp++, pol, pcur ? a.pw0 : a.pw1, true);
+            SweepResult r = run_improve<PT, MODE>(a, x, imp++, pol, pcur ? a.pw0 : a.pw1, true);
             pcur ^= 1;
             if (lead && row + a.msweeps < a.trace_len) a.trace[row + a.msweeps] = r.r;
             if (lead && outer < a.chg_len) a.chg[outer] = r.changed;
@@ -456,10 +531,10 @@ __global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const Spars
     }
 }
 
-template <typename PT, bool ROWMODE>
+template <typename PT, int MODE>
 static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
 {
-    auto kern = sparse_solver_kernel<PT, ROWMODE>;
+    auto kern = sparse_solver_kernel<PT, MODE>;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSThreads, 0);
     if (e != cudaSuccess) return e;
@@ -493,14 +568,27 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
     const double avg = pr.n * pr.A > 0 ? (double)pr.nnz / (double)(pr.n * pr.A) : 1.0;
-    const bool rowmode = pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32;
-    int GS = 1;
-    if (rowmode) {
+    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
+    const int64_t AK = (int64_t)pr.A * pr.ell_K;
+    const bool aligned = ((uintptr_t)pr.col % 16 == 0) && ((uintptr_t)pr.val % 16 == 0);
+    int mode = SM_STRIDED;
+    int GS = 1, GSE = 1;
+    if (pr.ell_K > 0 && pr.ell_K % 8 == 0 && aligned && AK / 8 <= 32 && ((AK / 8) & (AK / 8 - 1)) == 0 &&
+        ((pr.ell_K / 8) & (pr.ell_K / 8 - 1)) == 0) {
+        mode = SM_VEC;
+        GS = (int)(AK / 8);
+        GSE = pr.ell_K / 8;
+    } else if (pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32) {
+        mode = SM_ROW;
         while (GS < pr.A) GS <<= 1;
+        GSE = 1;  // B_{pi,b}: one row per state -> a lane per state
     } else {
         while (GS < 32 && GS < avg) GS <<= 1;
+        GSE = GS;
     }
+    (void)psz;
     a.GS = GS;
+    a.GSE = GSE;
 
     cudaStream_t st = pr.stream;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.part.ensure((size_t)2 * n * 8 + (size_t)2 * n * 4 + 256) != cudaSuccess ||
@@ -532,9 +620,13 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     const int grid = pr.num_sms;
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
-            ce = rowmode ? launch_sparse<float, true>(a, grid, st) : launch_sparse<float, false>(a, grid, st);
+            ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, st)
+                 : mode == SM_ROW ? launch_sparse<float, SM_ROW>(a, grid, st)
+                                  : launch_sparse<float, SM_STRIDED>(a, grid, st);
         else
-            ce = rowmode ? launch_sparse<double, true>(a, grid, st) : launch_sparse<double, false>(a, grid, st);
+            ce = mode == SM_VEC   ? launch_sparse<double, SM_VEC>(a, grid, st)
+                 : mode == SM_ROW ? launch_sparse<double, SM_ROW>(a, grid, st)
+                                  : launch_sparse<double, SM_STRIDED>(a, grid, st);
     }
     if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
     long long out[OUT_N + 4] = {0};
