@@ -64,8 +64,8 @@ typedef struct {
     rmb_dtype p_dtype;  /* storage type of P (or CSR val) and c                      */
     rmb_dtype v_dtype;  /* storage type of V: RMB_F64 only in this build             */
     int64_t row_begin;  /* owned states [row_begin,row_end); 0 and n_states on 1 GPU  */
-    int64_t row_end;
-    void* nccl_comm;    /* reserved for the multi-GPU exchange; must be NULL         */
+    int64_t row_end;    /*   (sharded handles: see the multi-GPU section below)      */
+    void* nccl_comm;    /* ncclComm_t from rmb_nccl_comm_init for sharded solves, or NULL */
     void* stream;       /* cudaStream_t used for all work of this handle (NULL = legacy default) */
 } rmb_desc;
 
@@ -143,6 +143,45 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
  * (lowest index on ties), *changed = #{states whose action changed},
  * *bellman_resid = ||TV - V||_inf.  pi: [n] int32 in/out.  Outputs HOST or NULL. */
 rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellman_resid, int64_t* changed);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: rows of P sharded by contiguous state ownership,
+ * V replicated, one exchange of the batch's updated (state, value, argmin)
+ * entries per batch (an all-gather).  The partition of every sweep is global,
+ * so each batch is the same set of states on every rank, and every state's
+ * backup is computed with the single-GPU arithmetic: V, pi and the residual
+ * trace are bitwise identical for any number of ranks.
+ * A shard handle is created with desc.row_begin/row_end from rmb_shard_range
+ * and P / c pointing at the owned rows only ([row_end-row_begin][A][n] and
+ * [row_end-row_begin][A]); V and pi are full-length on every rank (pi entries
+ * outside the owned range are unspecified on return).  Dense MDPs only in
+ * this build.
+ * ------------------------------------------------------------------------ */
+
+/* Owned rows of rank g of G: [begin, end) = [g*ceil(n/G), (g+1)*ceil(n/G)) ∩ [0,n). */
+rmb_status rmb_shard_range(int64_t n, int32_t G, int32_t g, int64_t* begin, int64_t* end);
+
+/* NCCL bootstrap: rank 0 draws a 128-byte unique id (HOST buffer), the
+ * caller broadcasts it (e.g. over torch.distributed), every rank creates its
+ * communicator (returned as an opaque ncclComm_t, stored in desc.nccl_comm).
+ * NCCL is loaded at run time (the process's libnccl.so.2). */
+rmb_status rmb_nccl_unique_id(void* id128);
+rmb_status rmb_nccl_comm_init(int32_t nranks, int32_t rank, const void* id128, void** comm);
+rmb_status rmb_nccl_comm_destroy(void* comm);
+
+/* With desc.nccl_comm set, rmb_vi / rmb_mpi above run the sharded protocol;
+ * they are collective: every rank calls with identical b, m, seed, eps,
+ * limits and flags, and identical V0 (and pi0 with RMB_PI_GIVEN).
+ *
+ * Logical group on ONE device: G shard handles (rank order, rmb_shard_range
+ * rows, same stream) run the same protocol with device-copy exchange; V and
+ * pi (full, host or device) are shared in/out.  Used to test the sharded path
+ * on one GPU; results equal the single-handle solve bit for bit. */
+rmb_status rmb_vi_group(rmb_problem* handles, int32_t G, int64_t b, uint64_t seed, double eps, int64_t max_sweeps,
+                        uint32_t flags, void* V, int32_t* pi, double* trace, rmb_stats* stats);
+rmb_status rmb_mpi_group(rmb_problem* handles, int32_t G, int64_t b, int32_t m, uint64_t seed, double eps,
+                         int64_t max_outer, uint32_t flags, void* V, int32_t* pi, double* trace, int64_t* changed,
+                         rmb_stats* stats);
 
 /* Host-side partition generator: perm[p] = pi_sweep(p),
  * the state processed at position p of operator application `sweep`;

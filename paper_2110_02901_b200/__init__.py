@@ -78,6 +78,18 @@ _SIGS = {
     "rmb_generate_grid": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "rmb_last_launch_count": ([ctypes.c_void_p], ctypes.c_int64),
+    "rmb_shard_range": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                         ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "rmb_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
+    "rmb_nccl_comm_init": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)],
+                           ctypes.c_int),
+    "rmb_nccl_comm_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "rmb_vi_group": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                      ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.POINTER(Stats)], ctypes.c_int),
+    "rmb_mpi_group": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                       ctypes.c_uint64, ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "rmb_last_phase_times": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "rmb_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "rmb_status_string": ([ctypes.c_int], ctypes.c_char_p),
@@ -175,11 +187,16 @@ class Problem:
 
     # ------------------------------------------------------------ creation
     @classmethod
-    def dense(cls, P, c, gamma, stream=None, validate=False):
-        """P: [n][A][n], c: [n][A] (float32/float64, torch cuda/cpu or numpy)."""
-        n, A, n2 = P.shape
-        assert n == n2 and tuple(c.shape) == (n, A) and c.dtype == P.dtype
-        d = _Desc(n, A, float(gamma), _dtype_code(P), F64, 0, n, None, _stream_ptr(stream))
+    def dense(cls, P, c, gamma, stream=None, validate=False, n=None, row_range=None, nccl_comm=None):
+        """P: [n][A][n], c: [n][A] (float32/float64, torch cuda/cpu or numpy).
+        Shard handle (multi-GPU): P = the owned rows [r1-r0][A][n], c = [r1-r0][A],
+        n = the global state count, row_range = (r0, r1) from shard_range(),
+        nccl_comm = comm_init(...) (or None for a logical group on one GPU)."""
+        rows, A, ncol = P.shape
+        n = ncol if n is None else n
+        r0, r1 = row_range if row_range is not None else (0, n)
+        assert ncol == n and rows == r1 - r0 and tuple(c.shape) == (rows, A) and c.dtype == P.dtype
+        d = _Desc(n, A, float(gamma), _dtype_code(P), F64, r0, r1, nccl_comm, _stream_ptr(stream))
         h = ctypes.c_void_p()
         _check(lib().rmb_create_dense(ctypes.byref(d), _ptr(P), _ptr(c), VALIDATE if validate else 0,
                                       ctypes.byref(h)))
@@ -274,6 +291,72 @@ class Problem:
         out = np.zeros(4, dtype=np.int64)
         _check(lib().rmb_last_phase_times(self._h, _ptr(out)))
         return tuple(int(x) for x in out)
+
+
+# ------------------------------------------------------------ multi-GPU
+def shard_range(n, G, g):
+    """Owned rows [begin, end) of rank g of G (contiguous blocks of ceil(n/G))."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().rmb_shard_range(n, G, g, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().rmb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(nranks, rank, uid: bytes):
+    """ncclComm_t (as an int) for desc.nccl_comm; uid from rank 0's nccl_unique_id()."""
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(lib().rmb_nccl_comm_init(nranks, rank, buf, ctypes.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm):
+    _check(lib().rmb_nccl_comm_destroy(comm))
+
+
+def _handles(problems):
+    arr = (ctypes.c_void_p * len(problems))(*[p._h.value if isinstance(p._h, ctypes.c_void_p) else p._h
+                                              for p in problems])
+    return arr
+
+
+def vi_group(problems, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
+             device="cuda"):
+    """MB-VI over G logical shard handles on one GPU (device-copy exchange)."""
+    import torch
+    n = problems[0].n
+    V = torch.zeros(n, dtype=torch.float64, device=device) if V is None else V
+    pi = torch.zeros(n, dtype=torch.int32, device=device) if pi is None else pi
+    tr = np.zeros(max_sweeps)
+    st = Stats()
+    flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+    s = lib().rmb_vi_group(_handles(problems), len(problems), b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi),
+                           _ptr(tr), ctypes.byref(st))
+    _check(s, (OK, NOT_CONVERGED, NONFINITE))
+    return Solution(V, pi, tr[: st.sweeps], s, st)
+
+
+def mpi_group(problems, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
+              v0_zero=False, device="cuda"):
+    """MB-MPI over G logical shard handles on one GPU."""
+    import torch
+    n = problems[0].n
+    V = torch.zeros(n, dtype=torch.float64, device=device) if V is None else V
+    pi = torch.zeros(n, dtype=torch.int32, device=device) if pi is None else pi
+    tr = np.zeros(max_outer * (m + 1))
+    ch = np.zeros(max_outer, dtype=np.int64)
+    st = Stats()
+    flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+    s = lib().rmb_mpi_group(_handles(problems), len(problems), b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi),
+                            _ptr(tr), _ptr(ch), ctypes.byref(st))
+    _check(s, (OK, NOT_CONVERGED, NONFINITE))
+    o = st.outer_iters
+    return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
 
 
 # ---------------------------------------------------------- free functions

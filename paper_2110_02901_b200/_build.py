@@ -14,8 +14,23 @@ SO = os.path.join(HERE, "librmb.so")
 BUILD = os.path.join(HERE, "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include():
+    """nccl.h for the NCCL types (the library itself is dlopen'ed at run time)."""
+    cands = []
+    try:
+        import nvidia.nccl  # torch's NCCL wheel
+        cands += [os.path.join(p, "include") for p in nvidia.nccl.__path__]
+    except Exception:
+        pass
+    cands += ["/usr/include", "/usr/local/cuda/include"]
+    for c in cands:
+        if os.path.exists(os.path.join(c, "nccl.h")):
+            return c
+    raise RuntimeError("nccl.h not found")
+
+
 NVFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                  "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+                  "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
 
 
 def _nvcc():
@@ -56,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
     tmp = SO + ".tmp"
-    r = subprocess.run([nvcc] + ARCH + ["-shared", "-o", tmp] + objs, capture_output=True, text=True)
+    r = subprocess.run([nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, SO)

@@ -65,9 +65,8 @@ static rmb_status check_desc(const rmb_desc* d)
     if (!(d->gamma > 0.0 && d->gamma < 1.0)) return fail(RMB_ERR_INVALID_ARG, "gamma not in (0,1)");
     if (d->p_dtype != RMB_F32 && d->p_dtype != RMB_F64) return fail(RMB_ERR_INVALID_ARG, "bad p_dtype");
     if (d->v_dtype != RMB_F64) return fail(RMB_ERR_INVALID_ARG, "v_dtype must be RMB_F64 in this build");
-    if (!(d->row_begin == 0 && d->row_end == d->n_states))
-        return fail(RMB_ERR_UNSUPPORTED, "row sharding (row_begin/row_end != 0/n) is not in this build");
-    if (d->nccl_comm) return fail(RMB_ERR_UNSUPPORTED, "nccl_comm must be NULL in this build");
+    if (!(0 <= d->row_begin && d->row_begin <= d->row_end && d->row_end <= d->n_states))
+        return fail(RMB_ERR_INVALID_ARG, "need 0 <= row_begin <= row_end <= n_states");
     return RMB_OK;
 }
 
@@ -78,6 +77,9 @@ static rmb_status init_problem(Problem& pr, const rmb_desc* d)
     pr.gamma = d->gamma;
     pr.pdt = d->p_dtype;
     pr.stream = (cudaStream_t)d->stream;
+    pr.row_begin = d->row_begin;
+    pr.row_end = d->row_end;
+    pr.nccl_comm = d->nccl_comm;
     cudaError_t e = cudaGetDevice(&pr.device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     int v = 0;
@@ -124,9 +126,14 @@ static rmb_status validate_mdp(Problem& pr)
     return RMB_OK;
 }
 
+static bool is_shard(const Problem& pr) { return pr.nccl_comm || pr.row_begin != 0 || pr.row_end != pr.n; }
+
 static rmb_status solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t tl, long long* chg_dev,
                         int64_t cl, SolveResult* res)
 {
+    if (is_shard(pr))
+        return fail(RMB_ERR_INVALID_ARG, "this handle owns a row range: use rmb_vi / rmb_mpi with an NCCL "
+                                         "communicator, or rmb_vi_group / rmb_mpi_group");
     return pr.dense ? dense_solve(pr, rq, trace_dev, tl, chg_dev, cl, res)
                     : sparse_solve(pr, rq, trace_dev, tl, chg_dev, cl, res);
 }
@@ -203,6 +210,7 @@ using namespace rmb;
 
 // ===================================================================== ABI
 extern "C" {
+rmb_status rmb_shard_range(int64_t n, int32_t G, int32_t g, int64_t* begin, int64_t* end);
 
 const char* rmb_version(void) { return "rmb 0.1 (sm_100a)"; }
 
@@ -235,9 +243,10 @@ rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, 
     Problem* pr = new Problem();
     s = init_problem(*pr, desc);
     const size_t psz = desc->p_dtype == RMB_F32 ? 4 : 8;
-    const size_t pbytes = (size_t)pr->n * pr->A * pr->n * psz;
+    const size_t rows = (size_t)(desc->row_end - desc->row_begin);  // owned states (all of them on one GPU)
+    const size_t pbytes = std::max<size_t>(1, rows * pr->A * pr->n * psz);
     if (s == RMB_OK) s = device_view(*pr, P, pbytes, &pr->P, "copy P to device");
-    if (s == RMB_OK) s = device_view(*pr, c, (size_t)pr->n * pr->A * psz, &pr->c, "copy c to device");
+    if (s == RMB_OK) s = device_view(*pr, c, std::max<size_t>(1, rows * pr->A * psz), &pr->c, "copy c to device");
     pr->dense = true;
     if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
     if (s != RMB_OK) {
@@ -257,6 +266,8 @@ rmb_status rmb_create_csr(const rmb_desc* desc, const int64_t* row_ptr, const in
     rmb_status s = check_desc(desc);
     if (s != RMB_OK) return s;
     if (!row_ptr || !col || !val || !c) return fail(RMB_ERR_INVALID_ARG, "row_ptr, col, val or c is NULL");
+    if (desc->row_begin != 0 || desc->row_end != desc->n_states || desc->nccl_comm)
+        return fail(RMB_ERR_UNSUPPORTED, "sharded (multi-GPU) solves cover dense MDPs in this build");
     Problem* pr = new Problem();
     s = init_problem(*pr, desc);
     pr->dense = false;
@@ -342,6 +353,21 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     rq.V = sg.V;
     rq.pi = sg.pi;
     SolveResult r;
+    if (is_shard(pr)) {  // multi-GPU: this rank's rows, NCCL exchange per batch
+        if (!pr.nccl_comm) return fail(RMB_ERR_INVALID_ARG, "a row-range handle needs nccl_comm (or rmb_vi_group)");
+        pr.stage_V = sg.V;
+        pr.stage_pi = sg.pi;
+        std::vector<double> tr((size_t)max_sweeps);
+        Problem* one = &pr;
+        s = sharded_solve(&one, 1, true, rq, tr.data(), max_sweeps, nullptr, 0, &r);
+        if (s != RMB_OK) return s;
+        s = stage_out(pr, V, pi, sg);
+        if (s == RMB_OK && trace) memcpy(trace, tr.data(), (size_t)r.sweeps * 8);
+        if (s != RMB_OK) return s;
+        rmb_status ret = (rmb_status)r.status;
+        fill_stats(stats, r, ret);
+        return ret;
+    }
     s = solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
     if (s != RMB_OK) return s;
     s = stage_out(pr, V, pi, sg);
@@ -369,13 +395,13 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     Staged sg;
     rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
     if (s != RMB_OK) return s;
-    if (pi_given) {  // validate the given policy on the host side of the copy
+    if (pi_given) {  // validate the given policy (the owned entries) on the host side of the copy
         std::vector<int32_t> hp((size_t)pr.n);
         cudaError_t e = cudaMemcpyAsync(hp.data(), sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
         if (e != cudaSuccess) return cuda_fail(e, "read pi");
-        for (int32_t a : hp)
-            if (a < 0 || a >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
+        for (int64_t q = pr.row_begin; q < pr.row_end; ++q)
+            if (hp[q] < 0 || hp[q] >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
     }
     const int64_t tl = max_outer * (int64_t)(m + 1);
     if (pr.trace.ensure((size_t)tl * 8) != cudaSuccess || pr.chg.ensure((size_t)max_outer * 8) != cudaSuccess)
@@ -393,6 +419,23 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     rq.V = sg.V;
     rq.pi = sg.pi;
     SolveResult r;
+    if (is_shard(pr)) {
+        if (!pr.nccl_comm) return fail(RMB_ERR_INVALID_ARG, "a row-range handle needs nccl_comm (or rmb_mpi_group)");
+        pr.stage_V = sg.V;
+        pr.stage_pi = sg.pi;
+        std::vector<double> tr((size_t)tl);
+        std::vector<int64_t> ch((size_t)max_outer);
+        Problem* one = &pr;
+        s = sharded_solve(&one, 1, true, rq, tr.data(), tl, ch.data(), max_outer, &r);
+        if (s != RMB_OK) return s;
+        s = stage_out(pr, V, pi, sg);
+        if (s != RMB_OK) return s;
+        if (trace) memcpy(trace, tr.data(), (size_t)(r.outer * (m + 1)) * 8);
+        if (changed) memcpy(changed, ch.data(), (size_t)r.outer * 8);
+        rmb_status ret = (rmb_status)r.status;
+        fill_stats(stats, r, ret);
+        return ret;
+    }
     s = solve(pr, rq, static_cast<double*>(pr.trace.p), tl, static_cast<long long*>(pr.chg.p), max_outer, &r);
     if (s != RMB_OK) return s;
     s = stage_out(pr, V, pi, sg);
@@ -407,6 +450,100 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     if (ret == RMB_ERR_NONFINITE) g_err = "a backup produced a non-finite value";
     fill_stats(stats, r, ret);
     return ret;
+}
+
+// G logical ranks on ONE device (handles created with rmb_shard_range row
+// ranges): the sharded protocol with device-copy exchange.  Each rank keeps its
+// own replica of V; outputs are rank 0's V and pi assembled from the owners.
+static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint32_t flags, void* V, int32_t* pi,
+                              double* trace, int64_t tl, int64_t* changed, int64_t cl, rmb_stats* stats)
+{
+    if (!hs || G < 1) return fail(RMB_ERR_INVALID_ARG, "handles NULL or G < 1");
+    if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    std::vector<Problem*> rk((size_t)G);
+    for (int g = 0; g < G; ++g) {
+        if (!hs[g]) return fail(RMB_ERR_INVALID_ARG, "a handle is NULL");
+        rk[g] = reinterpret_cast<Problem*>(hs[g]);
+        const Problem& p = *rk[g];
+        const Problem& p0 = *rk[0];
+        int64_t b0, b1;
+        rmb_shard_range(p0.n, G, g, &b0, &b1);
+        if (p.n != p0.n || p.A != p0.A || p.gamma != p0.gamma || p.pdt != p0.pdt || !p.dense || p.nccl_comm ||
+            p.row_begin != b0 || p.row_end != b1 || p.stream != p0.stream)
+            return fail(RMB_ERR_INVALID_ARG, "group handles must share n, A, gamma, dtype, stream and own the "
+                                             "rmb_shard_range(n, G, g) rows in rank order");
+    }
+    Problem& p0 = *rk[0];
+    const int64_t n = p0.n;
+    if (rq.b < 1 || rq.b > n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
+    const size_t vb = (size_t)n * 8, pb = (size_t)n * 4;
+    const bool v_zero = flags & RMB_V0_ZERO;
+    cudaStream_t st = p0.stream;
+    for (int g = 0; g < G; ++g) {
+        Problem& p = *rk[g];
+        if (p.vstage.ensure(vb) != cudaSuccess || p.pistage.ensure(pb) != cudaSuccess)
+            return fail(RMB_ERR_OOM, "replica allocation failed");
+        p.stage_V = static_cast<double*>(p.vstage.p);
+        p.stage_pi = static_cast<int32_t*>(p.pistage.p);
+        cudaError_t e = v_zero ? cudaMemsetAsync(p.stage_V, 0, vb, st)
+                               : cudaMemcpyAsync(p.stage_V, V, vb, cudaMemcpyDefault, st);
+        if (e == cudaSuccess) e = rq.pi_given ? cudaMemcpyAsync(p.stage_pi, pi, pb, cudaMemcpyDefault, st)
+                                              : cudaMemsetAsync(p.stage_pi, 0, pb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "group staging");
+    }
+    SolveResult r;
+    rmb_status s = sharded_solve(rk.data(), G, false, rq, trace, tl, changed, cl, &r);
+    if (s != RMB_OK) return s;
+    cudaError_t e = cudaMemcpyAsync(V, p0.stage_V, vb, cudaMemcpyDefault, st);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+        const Problem& p = *rk[g];
+        if (p.row_end > p.row_begin)
+            e = cudaMemcpyAsync(pi + p.row_begin, p.stage_pi + p.row_begin, (size_t)(p.row_end - p.row_begin) * 4,
+                                cudaMemcpyDefault, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "group outputs");
+    rmb_status ret = (rmb_status)r.status;
+    if (ret == RMB_ERR_NOT_CONVERGED) g_err = "iteration limit reached before the stopping test passed";
+    fill_stats(stats, r, ret);
+    return ret;
+}
+
+rmb_status rmb_vi_group(rmb_problem* hs, int32_t G, int64_t b, uint64_t seed, double eps, int64_t max_sweeps,
+                        uint32_t flags, void* V, int32_t* pi, double* trace, rmb_stats* stats)
+{
+    g_err.clear();
+    if (!(eps > 0.0) || !std::isfinite(eps) || max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "eps or max_sweeps");
+    SolveRequest rq;
+    rq.mode = MODE_VI;
+    rq.b = b;
+    rq.seed = seed;
+    rq.k0 = 1;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = eps;
+    rq.max_iter = max_sweeps;
+    return group_solve(hs, G, rq, flags, V, pi, trace, trace ? max_sweeps : 0, nullptr, 0, stats);
+}
+
+rmb_status rmb_mpi_group(rmb_problem* hs, int32_t G, int64_t b, int32_t m, uint64_t seed, double eps,
+                         int64_t max_outer, uint32_t flags, void* V, int32_t* pi, double* trace, int64_t* changed,
+                         rmb_stats* stats)
+{
+    g_err.clear();
+    if (m < 1 || !(eps > 0.0) || !std::isfinite(eps) || max_outer < 1)
+        return fail(RMB_ERR_INVALID_ARG, "m, eps or max_outer");
+    SolveRequest rq;
+    rq.mode = MODE_MPI;
+    rq.b = b;
+    rq.msweeps = m;
+    rq.seed = seed;
+    rq.k0 = 1;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = eps;
+    rq.max_iter = max_outer;
+    rq.pi_given = flags & RMB_PI_GIVEN;
+    return group_solve(hs, G, rq, flags, V, pi, trace, trace ? max_outer * (int64_t)(m + 1) : 0, changed,
+                       changed ? max_outer : 0, stats);
 }
 
 rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uint32_t flags, const int32_t* pi_or_null,

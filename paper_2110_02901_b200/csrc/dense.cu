@@ -88,6 +88,13 @@ struct DenseArgs {
     int64_t chg_len;
     long long* out;
     unsigned int* wctr;  // [2] work-stealing counters (phase parity)
+    // multi-GPU shard steps
+    int64_t row0, row1;        // owned states (P and c are offset so that global state ids index them)
+    const uint32_t* olist;     // this rank's states of the batch (compacted)
+    const int* ocount;         // their number (device)
+    double* send_val;          // per owned batch state: new value
+    uint32_t* send_idx;        //                        state id
+    int32_t* send_arg;         //                        argmin (or pi(s))
     int64_t qs_cap;      // doubles of smem scratch for S-mode reductions
     int64_t qs_off;      // byte offset of that scratch in dynamic smem
     long long* prof;     // [0] compute ns, [1] barrier ns, [2] combine ns, [3] barriers (CTA 0)
@@ -707,10 +714,21 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
 
 // Apply a state's new value to this CTA's smem copy (KIND 0: B_b, 1: B_pi,b,
 // 2: improvement).  CTA 0 also writes the global outputs.
+// KIND 3 / 4 (shard B_b / B_pi,b): the new value goes to this rank's send list
+// (position i) instead of the local V; the exchange + commit apply it.
 template <int KIND>
-__device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int32_t* pis, int64_t s, double v, int arg,
-                                            PhaseAcc& acc)
+__device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int32_t* pis, int64_t i, int64_t s, double v,
+                                            int arg, PhaseAcc& acc)
 {
+    if (KIND >= 3) {
+        acc.bad |= !isfinite(v);
+        if (blockIdx.x == 0) {
+            a.send_val[i] = v;
+            a.send_idx[i] = (uint32_t)s;
+            a.send_arg[i] = arg;
+        }
+        return;
+    }
     const double old = Vs[s];
     acc.rmax = fmax(acc.rmax, fabs(v - old));
     acc.bad |= !isfinite(v);
@@ -758,7 +776,7 @@ template <typename PT, int VE, int KIND, bool CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
                           int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
 {
-    constexpr bool EVAL = KIND == 1;
+    constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
     // the other parity's work counter was last used before the previous
     // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
@@ -777,7 +795,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     }
     timed_sync(x);
     const bool F = pl.C == 1;
-    auto patch = [&](int64_t, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, s, v, arg, acc); };
+    auto patch = [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc); };
     if (pl.redundant) {
         if (F) {
             for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
@@ -785,7 +803,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
                 double v;
                 int arg;
                 reduce_state_F<EVAL>(a, part, i, v, arg, pl.ng);
-                patch_state<KIND>(a, Vs, pis, s, v, arg, acc);
+                patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc);
             }
         } else {
             reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, 0, 1, pis, Qs, patch);
@@ -794,7 +812,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
         // last-arriver mode: the list was completed during the compute phase
         for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
             const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-            patch_state<KIND>(a, Vs, pis, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
+            patch_state<KIND>(a, Vs, pis, i, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
         }
     }
     __syncthreads();
@@ -844,8 +862,8 @@ template <typename PT, int VE, bool CTA>
 __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, double* Qs)
 {
     PhaseAcc acc{0.0, 0, 0};
-    for (int64_t lo = 0; lo < a.n; lo += a.imp_sub) {
-        const int64_t cnt = min(a.imp_sub, a.n - lo);
+    for (int64_t lo = a.row0; lo < a.row1; lo += a.imp_sub) {
+        const int64_t cnt = min(a.imp_sub, a.row1 - lo);
         run_batch<PT, VE, 2, CTA>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
     }
     return block_reduce(acc);
@@ -859,7 +877,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     const int64_t n_pad = (a.n + 1) & ~int64_t(1);
     int32_t* pis = reinterpret_cast<int32_t*>(Vs + n_pad);
     double* Qs = reinterpret_cast<double*>(smem_raw + a.qs_off);
-    const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE;
+    const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE ||
+                         a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
+    const bool shard = a.mode >= MODE_SHARD_MIN;
 
     for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
         Vs[j] = a.V[j];
@@ -867,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     }
     Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
     if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
-    if (!a.identity && a.mode != MODE_IMPROVE) {
+    if (!a.identity && a.mode != MODE_IMPROVE && !shard) {
         Permutation pm;
         pm.init(a.n, a.seed, a.k0);
         uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
@@ -882,7 +902,23 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     long long changed = 0;
     double last = 0.0;
 
-    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
+    if (a.mode == MODE_SHARD_MIN || a.mode == MODE_SHARD_EVAL) {
+        // one batch of this rank's states, against the replica V, into the send list
+        PhaseAcc acc{0.0, 0, 0};
+        const int64_t cnt = *a.ocount;
+        if (a.mode == MODE_SHARD_MIN)
+            run_batch<PT, VE, 3, CTA>(a, x, Vs, pis, a.olist, 0, cnt, a.plan[0], acc, Qs, 0);
+        else
+            run_batch<PT, VE, 4, CTA>(a, x, Vs, pis, a.olist, 0, cnt, a.plan[1], acc, Qs, 0);
+        PhaseAcc r = block_reduce(acc);
+        status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
+        x.batches = 1;
+    } else if (a.mode == MODE_SHARD_IMPROVE) {
+        PhaseAcc r = run_improve<PT, VE, CTA>(a, x, Vs, pis, Qs);
+        last = r.rmax;
+        changed = r.changed;
+        status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
+    } else if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
         const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
         while (it < iters) {
             PhaseAcc r = a.mode == MODE_APPLY_PI ? run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs)
@@ -999,14 +1035,25 @@ static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaS
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
-rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
-                       long long* chg_dev, int64_t chg_len, SolveResult* res)
+struct DenseLaunch {
+    DenseArgs a;
+    size_t smem;
+    int VE;
+    int64_t lcap;
+};
+
+// Plans (chunking, combine mode) and workspace for one launch.  The plan
+// depends on (n, A, b, mode) only — never on how many states a shard owns —
+// so every state's reduction order is identical for any number of GPUs.
+static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                                long long* chg_dev, int64_t chg_len, DenseLaunch& L)
 {
     const int64_t n = pr.n;
     const int psz = pr.pdt == RMB_F32 ? 4 : 8;
     int VE = 16 / psz;
     if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
-    const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE;
+    const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE ||
+                         rq.mode == MODE_SHARD_EVAL || rq.mode == MODE_SHARD_IMPROVE;
     const int64_t n_pad = (n + 1) & ~int64_t(1);
     const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
     if (smem_v + 12288 > pr.smem_optin) {
@@ -1015,10 +1062,15 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
                   "); column panels for larger dense n are not in this build");
         return RMB_ERR_UNSUPPORTED;
     }
-
-    DenseArgs a{};
-    a.P = pr.P;
-    a.c = pr.c;
+    DenseArgs& a = L.a;
+    a = DenseArgs{};
+    // P and c hold the rows of the owned states [row0, row1); offset the base
+    // pointers so that global state ids index them directly
+    const int64_t row0 = pr.row_begin, row1 = pr.row_end;
+    a.P = static_cast<const char*>(pr.P) - (size_t)row0 * pr.A * n * psz;
+    a.c = static_cast<const char*>(pr.c) - (size_t)row0 * pr.A * psz;
+    a.row0 = row0;
+    a.row1 = row1;
     a.n = n;
     a.A = pr.A;
     a.gamma = pr.gamma;
@@ -1041,7 +1093,7 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     // smem scratch for split-row (S-mode) reductions: up to 32 KB after V / pi
     a.qs_off = (int64_t)smem_v;
     a.qs_cap = std::min<int64_t>(4096, ((int64_t)pr.smem_optin - (int64_t)smem_v - 12288) / 8);
-    const size_t smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
+    L.smem = smem_v + (size_t)std::max<int64_t>(a.qs_cap, 0) * 8;
     const bool split_ok = a.qs_cap >= pr.A;  // else every row stays whole (C = 1)
     a.plan[0] = plan_chunks(n, rq.b, NAG, pr.A, VE, sms, split_ok, ng_b, psz);
     a.plan[0].ng = ng_b;
@@ -1056,11 +1108,11 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
                                               plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A)});
     a.part_stride = (stride + 31) / 32 * 32;
-    const int64_t lcap = std::max<int64_t>(rq.b, a.imp_sub);
+    L.lcap = std::max<int64_t>(rq.b, a.imp_sub);
+    L.VE = VE;
 
-    cudaStream_t st = pr.stream;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess ||
-        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)lcap * 16 + 64) != cudaSuccess ||
+        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)L.lcap * 16 + 64) != cudaSuccess ||
         pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("dense solver: workspace allocation failed");
         return RMB_ERR_OOM;
@@ -1068,35 +1120,71 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     a.perm = static_cast<uint32_t*>(pr.perm.p);
     a.part = static_cast<double*>(pr.part.p);
     a.lval = a.part + 2 * a.part_stride;
-    a.larg = reinterpret_cast<int32_t*>(a.lval + lcap);
-    a.scnt = reinterpret_cast<unsigned int*>(a.larg + lcap);
+    a.larg = reinterpret_cast<int32_t*>(a.lval + L.lcap);
+    a.scnt = reinterpret_cast<unsigned int*>(a.larg + L.lcap);
     unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
-    a.bar = ctrl;                                      // [0], [32]
-    a.err = reinterpret_cast<int*>(ctrl + 64);         // [64]
-    a.out = reinterpret_cast<long long*>(ctrl + 128);  // [128..136)
-    a.prof = reinterpret_cast<long long*>(ctrl + 192); // [192..196)
-    a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256); // [256]
+    a.bar = ctrl;                                          // [0], [32]
+    a.err = reinterpret_cast<int*>(ctrl + 64);             // [64]
+    a.out = reinterpret_cast<long long*>(ctrl + 128);      // [128..136)
+    a.prof = reinterpret_cast<long long*>(ctrl + 192);     // [192..196)
+    a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256);  // [256]
     a.trace = trace_dev;
     a.trace_len = trace_len;
     a.chg = chg_dev;
     a.chg_len = chg_len;
+    return RMB_OK;
+}
 
+static cudaError_t dense_launch(Problem& pr, const DenseLaunch& L, cudaStream_t st)
+{
+    cudaError_t ce = cudaMemsetAsync(L.a.bar, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(L.a.scnt, 0, (size_t)L.lcap * 4, st);
+    if (ce != cudaSuccess) return ce;
+    const int sms = pr.num_sms;
+    if (pr.pdt == RMB_F32)
+        return L.VE == 4 ? launch_typed<float, 4>(L.a, L.smem, sms, st) : launch_typed<float, 1>(L.a, L.smem, sms, st);
+    return L.VE == 2 ? launch_typed<double, 2>(L.a, L.smem, sms, st) : launch_typed<double, 1>(L.a, L.smem, sms, st);
+}
+
+// One shard step (MODE_SHARD_*) launched asynchronously on `st`: the result
+// block (status, residual, changed) lands in the returned device pointer.
+rmb_status dense_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t* olist, const int* ocount,
+                            double* send_val, uint32_t* send_idx, int32_t* send_arg, cudaStream_t st,
+                            long long** out_dev)
+{
+    DenseLaunch L;
+    rmb_status s = dense_prepare(pr, rq, nullptr, 0, nullptr, 0, L);
+    if (s != RMB_OK) return s;
+    L.a.olist = olist;
+    L.a.ocount = ocount;
+    L.a.send_val = send_val;
+    L.a.send_idx = send_idx;
+    L.a.send_arg = send_arg;
+    cudaError_t ce = dense_launch(pr, L, st);
+    if (ce != cudaSuccess) {
+        set_error(std::string("dense shard step: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    if (out_dev) *out_dev = L.a.out;
+    return RMB_OK;
+}
+
+rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                       long long* chg_dev, int64_t chg_len, SolveResult* res)
+{
+    DenseLaunch L;
+    rmb_status s = dense_prepare(pr, rq, trace_dev, trace_len, chg_dev, chg_len, L);
+    if (s != RMB_OK) return s;
+    cudaStream_t st = pr.stream;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(a.scnt, 0, (size_t)lcap * 4, st);
-    if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
-    if (ce == cudaSuccess) {
-        if (pr.pdt == RMB_F32)
-            ce = VE == 4 ? launch_typed<float, 4>(a, smem, sms, st) : launch_typed<float, 1>(a, smem, sms, st);
-        else
-            ce = VE == 2 ? launch_typed<double, 2>(a, smem, sms, st) : launch_typed<double, 1>(a, smem, sms, st);
-    }
+    cudaError_t ce = cudaEventRecord(e0, st);
+    if (ce == cudaSuccess) ce = dense_launch(pr, L, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
     long long out[OUT_N + 8] = {0};
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, L.a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, L.a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
     float ms = 0.f;
     if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);

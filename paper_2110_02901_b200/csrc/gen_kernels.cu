@@ -154,8 +154,9 @@ __global__ void validate_csr_kernel(const int64_t* row_ptr, const int32_t* col, 
 
 cudaError_t launch_validate(const Problem& pr, int* bad, cudaStream_t st)
 {
-    const int64_t rows = pr.n * pr.A;
+    const int64_t rows = (pr.row_end - pr.row_begin) * pr.A;  // owned rows
     const double tol = pr.pdt == RMB_F64 ? 1e-9 : 1e-5;
+    if (rows == 0) return cudaMemsetAsync(bad, 0, sizeof(int), st);
     cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     if (pr.dense) {

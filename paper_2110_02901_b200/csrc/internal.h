@@ -16,6 +16,10 @@ enum Mode : int {
     MODE_APPLY = 2,    // one application of B_b
     MODE_APPLY_PI = 3, // one application of B_{pi,b}
     MODE_IMPROVE = 4,  // one policy improvement (greedy, ||TV-V||, changed)
+    // multi-GPU shard steps (one launch each, host-driven exchange between them)
+    MODE_SHARD_MIN = 5,     // B_b backups of this rank's states of one batch -> send list
+    MODE_SHARD_EVAL = 6,    // B_{pi,b} backups of this rank's states of one batch -> send list
+    MODE_SHARD_IMPROVE = 7, // improvement of this rank's states (pi owned entries, resid, changed)
 };
 
 // Device-side result block written by the solver kernels (long long[8]).
@@ -86,6 +90,11 @@ struct Problem {
     const int32_t* col = nullptr;
     const void* val = nullptr;
     int64_t nnz = 0;
+    // multi-GPU: owned states [row_begin, row_end) and the exchange backend
+    int64_t row_begin = 0, row_end = 0;
+    void* nccl_comm = nullptr;
+    double* stage_V = nullptr;    // sharded solves: this rank's replica of V (device)
+    int32_t* stage_pi = nullptr;  //                 this rank's pi (owned entries meaningful)
     int ell_K = 0;  // > 0: fixed-stride rows (ELL)
     cudaStream_t stream = nullptr;
     int device = 0;
@@ -101,6 +110,12 @@ struct Problem {
 // dense.cu
 rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                        long long* chg_dev, int64_t chg_len, SolveResult* res);
+rmb_status dense_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t* olist, const int* ocount,
+                            double* send_val, uint32_t* send_idx, int32_t* send_arg, cudaStream_t st,
+                            long long** out_dev);
+// shard.cu: multi-GPU (NCCL) and logical-group (one GPU) sharded solves
+rmb_status sharded_solve(Problem** ranks, int G, bool nccl, const SolveRequest& rq, double* trace_host,
+                         int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res);
 // sparse.cu
 rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                         long long* chg_dev, int64_t chg_len, SolveResult* res);

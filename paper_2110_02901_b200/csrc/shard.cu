@@ -1,0 +1,468 @@
+// shard.cu — multi-GPU mini-batch solves.
+//
+// Rows of P (and c) are sharded by contiguous state ownership; every rank
+// keeps a full replica of V.  The partition pi_k is global (every rank draws
+// the same permutation), so batch t is the same set of states everywhere.
+// Per batch:
+//   1. compact:   this rank's states of the batch (perm ∩ [row_begin,row_end));
+//   2. compute:   their backups against the replica V (the dense persistent
+//                 kernel in MODE_SHARD_*: one launch, one batch) -> send list
+//                 (value, state, argmin) of capacity cap = min(b, max rows);
+//   3. exchange:  all-gather of the fixed-size send lists (NCCL over NVLink,
+//                 or device copies between the logical ranks of one GPU);
+//   4. commit:    every rank scatters all ranks' updates into its replica
+//                 (identical on every rank), max |new - old| -> sweep residual.
+// Eq. 12 holds exactly: the batch's reads all happen in step 2, against the
+// replica as it was after the previous batch's commit.
+// Each state's arithmetic is the single-GPU kernel's (the chunk plan depends on
+// (n, A, b) only), so V, pi and the residual trace are bitwise identical for
+// any number of ranks (tested with logical ranks on one GPU).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "nccl_min.h"
+#include "partition.cuh"
+
+namespace rmb {
+
+// ---------------------------------------------------------------- NCCL API
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// dlopen'ed (not linked) so that the process uses the one NCCL it already has
+// loaded (torch's); falls back to the system library.
+static NcclApi& nccl()
+{
+    static NcclApi api = [] {
+        NcclApi x;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            x.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return x;
+        }
+#define RMB_SYM(name, field)                                                      \
+    x.field = reinterpret_cast<decltype(x.field)>(dlsym(h, name));               \
+    if (!x.field) {                                                               \
+        x.why = std::string("libnccl lacks ") + name;                             \
+        return x;                                                                 \
+    }
+        RMB_SYM("ncclGetUniqueId", GetUniqueId);
+        RMB_SYM("ncclCommInitRank", CommInitRank);
+        RMB_SYM("ncclCommDestroy", CommDestroy);
+        RMB_SYM("ncclCommCount", CommCount);
+        RMB_SYM("ncclCommUserRank", CommUserRank);
+        RMB_SYM("ncclAllGather", AllGather);
+        RMB_SYM("ncclGetErrorString", GetErrorString);
+#undef RMB_SYM
+        x.ok = true;
+        return x;
+    }();
+    return api;
+}
+
+static rmb_status nccl_fail(ncclResult_t r, const char* where)
+{
+    set_error(std::string(where) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+    return RMB_ERR_NCCL;
+}
+
+// ---------------------------------------------------------------- kernels
+// this rank's states of batch positions [lo, lo+cnt): order-free compaction
+// (the list order does not affect any state's result)
+__global__ void compact_owned_kernel(const uint32_t* perm, int64_t lo, int64_t cnt, int64_t row0, int64_t row1,
+                                     uint32_t* olist, int* ocount)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < cnt; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        int64_t s = -1;
+        if (i < cnt) s = perm ? (int64_t)perm[lo + i] : lo + i;
+        const bool own = i < cnt && s >= row0 && s < row1;
+        const unsigned m = __ballot_sync(0xffffffffu, own);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(ocount, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (own) olist[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)s;
+    }
+}
+
+// Exchange record layout (per rank, `chunk` bytes): int count | pad to 16 |
+// double val[cap] | uint32 idx[cap] | int32 arg[cap]
+struct Rec {
+    int64_t cap;
+    size_t chunk;
+    __host__ __device__ size_t off_val() const { return 16; }
+    __host__ __device__ size_t off_idx() const { return 16 + 8 * (size_t)cap; }
+    __host__ __device__ size_t off_arg() const { return 16 + 12 * (size_t)cap; }
+};
+
+__global__ void copy_count_kernel(const int* ocount, char* send) { *reinterpret_cast<int*>(send) = *ocount; }
+
+// apply all ranks' updates to this rank's replica; residual / nonfinite
+__global__ void commit_kernel(double* V, int32_t* pi, int64_t row0, int64_t row1, const char* recv, int G, Rec rec,
+                              unsigned long long* resid_bits, int* bad)
+{
+    const int64_t total = (int64_t)G * rec.cap;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(j / rec.cap);
+        const int64_t q = j - (int64_t)r * rec.cap;
+        const char* base = recv + (size_t)r * rec.chunk;
+        if (q >= *reinterpret_cast<const int*>(base)) continue;
+        const double v = reinterpret_cast<const double*>(base + rec.off_val())[q];
+        const int64_t s = reinterpret_cast<const uint32_t*>(base + rec.off_idx())[q];
+        const int arg = reinterpret_cast<const int32_t*>(base + rec.off_arg())[q];
+        const double d = fabs(v - V[s]);
+        atomicMax(resid_bits, (unsigned long long)__double_as_longlong(d));
+        if (!isfinite(v)) atomicOr(bad, 1);
+        V[s] = v;
+        if (pi && s >= row0 && s < row1) pi[s] = arg;
+    }
+}
+
+// ------------------------------------------------------------------ driver
+struct RankWs {
+    Problem* pr;
+    DevBuf buf;  // perm (n) | olist (cap) | ocount | send (chunk) | recv (G*chunk) | resid | bad | imp
+    uint32_t* perm;
+    uint32_t* olist;
+    int* ocount;
+    char* send;
+    char* recv;
+    unsigned long long* resid;
+    int* bad;
+    char* imp_send;  // improvement record: double resid | int64 changed | int64 status (24 B)
+    char* imp_recv;
+};
+
+static int blocks_for(int64_t work) { return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8)); }
+
+rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const SolveRequest& rq0, double* trace_host,
+                         int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res)
+{
+    Problem& p0 = *ranks[0];
+    const int64_t n = p0.n;
+    cudaStream_t st = p0.stream;
+    int G = G_local;
+    ncclComm_t comm = nullptr;
+    if (use_nccl) {
+        if (!nccl().ok) {
+            set_error("NCCL unavailable: " + nccl().why);
+            return RMB_ERR_NCCL;
+        }
+        comm = static_cast<ncclComm_t>(p0.nccl_comm);
+        ncclResult_t r = nccl().CommCount(comm, &G);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclCommCount");
+    }
+    if (!p0.dense) {
+        set_error("sharded solves cover dense MDPs in this build");
+        return RMB_ERR_UNSUPPORTED;
+    }
+    // capacity: the largest owned range (identical on every rank: ranges from
+    // rmb_shard_range, i.e. ceil(n / G))
+    const int64_t max_rows = (n + G - 1) / G;
+    int64_t local_max = 0;
+    for (int r = 0; r < G_local; ++r) local_max = std::max(local_max, ranks[r]->row_end - ranks[r]->row_begin);
+    if (local_max > max_rows) {
+        set_error("owned row ranges must come from rmb_shard_range (at most ceil(n/G) rows per rank)");
+        return RMB_ERR_INVALID_ARG;
+    }
+    Rec rec;
+    rec.cap = std::min<int64_t>(rq0.b, max_rows);
+    rec.chunk = ((16 + 16 * (size_t)rec.cap) + 255) / 256 * 256;
+
+    std::vector<RankWs> ws(G_local);
+    for (int r = 0; r < G_local; ++r) {
+        RankWs& w = ws[r];
+        w.pr = ranks[r];
+        const size_t need = (size_t)n * 4 + (size_t)rec.cap * 4 + 256 + rec.chunk + (size_t)G * rec.chunk + 256 +
+                            256 + 24 * (size_t)G + 256;
+        if (w.pr->aux.ensure(need + 1024) != cudaSuccess) {
+            set_error("sharded solve: workspace allocation failed");
+            return RMB_ERR_OOM;
+        }
+        char* b = static_cast<char*>(w.pr->aux.p);
+        auto take = [&](size_t bytes) {
+            char* q = b;
+            b += (bytes + 255) / 256 * 256;
+            return q;
+        };
+        w.perm = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+        w.olist = reinterpret_cast<uint32_t*>(take((size_t)rec.cap * 4));
+        w.ocount = reinterpret_cast<int*>(take(16));
+        w.send = take(rec.chunk);
+        w.recv = take((size_t)G * rec.chunk);
+        w.resid = reinterpret_cast<unsigned long long*>(take(16));
+        w.bad = reinterpret_cast<int*>(take(16));
+        w.imp_send = take(24);
+        w.imp_recv = take(24 * (size_t)G);
+    }
+
+    auto check = [&](cudaError_t e, const char* where) -> rmb_status {
+        if (e == cudaSuccess) return RMB_OK;
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return RMB_ERR_CUDA;
+    };
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    int64_t launches = 0;
+
+    // one operator application (B_b if !eval, else B_{pi,b}) with sweep index k
+    auto sweep = [&](int64_t k, bool eval, double* r_out, bool* bad_out) -> rmb_status {
+        for (int r = 0; r < G_local; ++r) {
+            RankWs& w = ws[r];
+            cudaError_t e = launch_partition(n, rq0.seed, k, rq0.identity, w.perm, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(w.resid, 0, 32, st);
+            if (rmb_status s = check(e, "shard partition"); s != RMB_OK) return s;
+            ++launches;
+        }
+        for (int64_t lo = 0; lo < n; lo += rq0.b) {
+            const int64_t cnt = std::min<int64_t>(rq0.b, n - lo);
+            for (int r = 0; r < G_local; ++r) {
+                RankWs& w = ws[r];
+                Problem& pr = *w.pr;
+                cudaError_t e = cudaMemsetAsync(w.ocount, 0, sizeof(int), st);
+                if (e != cudaSuccess) return check(e, "shard compact");
+                compact_owned_kernel<<<blocks_for(cnt), 256, 0, st>>>(w.perm, lo, cnt, pr.row_begin, pr.row_end, w.olist,
+                                                                       w.ocount);
+                if (rmb_status s = check(cudaGetLastError(), "shard compact"); s != RMB_OK) return s;
+                SolveRequest rq = rq0;
+                rq.mode = eval ? MODE_SHARD_EVAL : MODE_SHARD_MIN;
+                rq.V = ranks[r]->stage_V;
+                rq.pi = ranks[r]->stage_pi;
+                rmb_status s = dense_shard_step(pr, rq, w.olist, w.ocount,
+                                                reinterpret_cast<double*>(w.send + rec.off_val()),
+                                                reinterpret_cast<uint32_t*>(w.send + rec.off_idx()),
+                                                reinterpret_cast<int32_t*>(w.send + rec.off_arg()), st, nullptr);
+                if (s != RMB_OK) return s;
+                copy_count_kernel<<<1, 1, 0, st>>>(w.ocount, w.send);
+                launches += 3;
+            }
+            if (use_nccl) {
+                ncclResult_t nr = nccl().AllGather(ws[0].send, ws[0].recv, rec.chunk, ncclUint8, comm, st);
+                if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather");
+            } else {
+                for (int r = 0; r < G_local; ++r)
+                    for (int q = 0; q < G_local; ++q) {
+                        cudaError_t e = cudaMemcpyAsync(ws[r].recv + (size_t)q * rec.chunk, ws[q].send, rec.chunk,
+                                                        cudaMemcpyDeviceToDevice, st);
+                        if (e != cudaSuccess) return check(e, "logical exchange");
+                    }
+            }
+            for (int r = 0; r < G_local; ++r) {
+                RankWs& w = ws[r];
+                Problem& pr = *w.pr;
+                commit_kernel<<<blocks_for((int64_t)G * rec.cap), 256, 0, st>>>(
+                    pr.stage_V, eval ? nullptr : pr.stage_pi, pr.row_begin, pr.row_end, w.recv, G, rec, w.resid, w.bad);
+                if (rmb_status s = check(cudaGetLastError(), "shard commit"); s != RMB_OK) return s;
+                ++launches;
+            }
+            ++res->batches;
+        }
+        unsigned long long rb = 0;
+        int bb = 0;
+        cudaError_t e = cudaMemcpyAsync(&rb, ws[0].resid, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&bb, ws[0].bad, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return check(e, "shard residual");
+        memcpy(r_out, &rb, 8);
+        *bad_out = bb != 0;
+        return RMB_OK;
+    };
+
+    // improvement over every rank's own states; (max residual, sum changed, any bad)
+    auto improve = [&](double* r_out, long long* changed_out, bool* bad_out) -> rmb_status {
+        std::vector<long long*> outs(G_local);
+        for (int r = 0; r < G_local; ++r) {
+            SolveRequest rq = rq0;
+            rq.mode = MODE_SHARD_IMPROVE;
+            rq.V = ranks[r]->stage_V;
+            rq.pi = ranks[r]->stage_pi;
+            rmb_status s = dense_shard_step(*ranks[r], rq, nullptr, nullptr, nullptr, nullptr, nullptr, st, &outs[r]);
+            if (s != RMB_OK) return s;
+            ++launches;
+            // record: residual bits, changed, status
+            cudaError_t e = cudaMemcpyAsync(ws[r].imp_send, outs[r] + OUT_RESID_BITS, 8, cudaMemcpyDeviceToDevice, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(ws[r].imp_send + 8, outs[r] + OUT_CHANGED, 8, cudaMemcpyDeviceToDevice, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(ws[r].imp_send + 16, outs[r] + OUT_STATUS, 8, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return check(e, "shard improve record");
+        }
+        std::vector<long long> all(3 * (size_t)G);
+        if (use_nccl) {
+            ncclResult_t nr = nccl().AllGather(ws[0].imp_send, ws[0].imp_recv, 24, ncclUint8, comm, st);
+            if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather(improve)");
+            cudaError_t e = cudaMemcpyAsync(all.data(), ws[0].imp_recv, 24 * (size_t)G, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return check(e, "improve gather");
+        } else {
+            for (int r = 0; r < G_local; ++r) {
+                cudaError_t e = cudaMemcpyAsync(all.data() + 3 * r, ws[r].imp_send, 24, cudaMemcpyDeviceToHost, st);
+                if (e != cudaSuccess) return check(e, "improve gather");
+            }
+        }
+        if (rmb_status s = check(cudaStreamSynchronize(st), "improve sync"); s != RMB_OK) return s;
+        double rmax = 0.0;
+        long long ch = 0;
+        bool bad = false;
+        for (int r = 0; r < G; ++r) {
+            double d;
+            memcpy(&d, &all[3 * r], 8);
+            if (!std::isfinite(d) || all[3 * r + 2] == RMB_ERR_NONFINITE) bad = true;
+            rmax = std::max(rmax, d);
+            ch += all[3 * r + 1];
+        }
+        *r_out = rmax;
+        *changed_out = ch;
+        *bad_out = bad;
+        return RMB_OK;
+    };
+
+    rmb_status status = RMB_ERR_NOT_CONVERGED;
+    int64_t k = rq0.k0, it = 0, outer = 0;
+    double last = 0.0;
+    long long changed = 0;
+    if (rq0.mode == MODE_VI) {
+        while (it < rq0.max_iter) {
+            double r;
+            bool bad;
+            if (rmb_status s = sweep(k, false, &r, &bad); s != RMB_OK) return s;
+            if (trace_host && it < trace_len) trace_host[it] = r;
+            ++it;
+            ++k;
+            last = r;
+            if (bad) { status = RMB_ERR_NONFINITE; break; }
+            if (r <= rq0.eps) { status = RMB_OK; break; }
+        }
+    } else if (rq0.mode == MODE_MPI) {
+        bool bad = false;
+        if (!rq0.pi_given) {
+            double r;
+            long long ch;
+            if (rmb_status s = improve(&r, &ch, &bad); s != RMB_OK) return s;
+        }
+        while (!bad && outer < rq0.max_iter) {
+            const int64_t row = outer * (rq0.msweeps + 1);
+            for (int e = 0; e < rq0.msweeps && !bad; ++e) {
+                double r;
+                if (rmb_status s = sweep(k, true, &r, &bad); s != RMB_OK) return s;
+                if (trace_host && row + e < trace_len) trace_host[row + e] = r;
+                ++k;
+                ++it;
+            }
+            if (bad) { ++outer; break; }
+            double r;
+            long long ch;
+            if (rmb_status s = improve(&r, &ch, &bad); s != RMB_OK) return s;
+            if (trace_host && row + rq0.msweeps < trace_len) trace_host[row + rq0.msweeps] = r;
+            if (chg_host && outer < chg_len) chg_host[outer] = ch;
+            ++outer;
+            last = r;
+            changed = ch;
+            if (bad) break;
+            if (ch == 0 && r <= rq0.eps) { status = RMB_OK; break; }
+        }
+        if (bad) status = RMB_ERR_NONFINITE;
+    } else {
+        set_error("sharded solve: unsupported mode");
+        return RMB_ERR_UNSUPPORTED;
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    res->sweeps = it;
+    res->outer = outer;
+    res->status = status;
+    res->final_resid = last;
+    res->changed = changed;
+    res->ms = ms;
+    res->launches = (int)launches;
+    for (int r = 0; r < G_local; ++r) ranks[r]->last_launches = launches;
+    return RMB_OK;
+}
+
+}  // namespace rmb
+
+// ------------------------------------------------------------ C entry points
+using namespace rmb;
+
+extern "C" rmb_status rmb_nccl_unique_id(void* id128)
+{
+    if (!id128) {
+        set_error("id buffer is NULL");
+        return RMB_ERR_INVALID_ARG;
+    }
+    if (!nccl().ok) {
+        set_error("NCCL unavailable: " + nccl().why);
+        return RMB_ERR_NCCL;
+    }
+    ncclUniqueId id;
+    ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(id128, &id, sizeof(id));
+    return RMB_OK;
+}
+
+extern "C" rmb_status rmb_nccl_comm_init(int32_t nranks, int32_t rank, const void* id128, void** comm)
+{
+    if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("rmb_nccl_comm_init: invalid argument");
+        return RMB_ERR_INVALID_ARG;
+    }
+    if (!nccl().ok) {
+        set_error("NCCL unavailable: " + nccl().why);
+        return RMB_ERR_NCCL;
+    }
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    ncclResult_t r = nccl().CommInitRank(&c, nranks, id, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+    *comm = c;
+    return RMB_OK;
+}
+
+extern "C" rmb_status rmb_nccl_comm_destroy(void* comm)
+{
+    if (!comm) {
+        set_error("comm is NULL");
+        return RMB_ERR_INVALID_ARG;
+    }
+    if (!nccl().ok) return RMB_ERR_NCCL;
+    ncclResult_t r = nccl().CommDestroy(static_cast<ncclComm_t>(comm));
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+    return RMB_OK;
+}
+
+extern "C" rmb_status rmb_shard_range(int64_t n, int32_t G, int32_t g, int64_t* begin, int64_t* end)
+{
+    if (n < 1 || G < 1 || g < 0 || g >= G || !begin || !end) {
+        set_error("rmb_shard_range: invalid argument");
+        return RMB_ERR_INVALID_ARG;
+    }
+    // contiguous blocks of ceil(n/G) rows; trailing ranks may own fewer (or none)
+    const int64_t q = (n + G - 1) / G;
+    *begin = std::min<int64_t>(n, (int64_t)g * q);
+    *end = std::min<int64_t>(n, (int64_t)(g + 1) * q);
+    return RMB_OK;
+}

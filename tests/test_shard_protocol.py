@@ -1,0 +1,107 @@
+"""CPU, world_size-2 `gloo` test of the multi-GPU exchange protocol.
+
+Each process owns the rows rmb_shard_range() gives it (product host code),
+draws every sweep's partition with rmb_partition() (product host code), backs
+up its states of each batch against its replica V (oracle arithmetic, one
+state at a time), packs (state, value, argmin) into the fixed-capacity record
+the library exchanges (cap = min(b, ceil(n/G))), all-gathers the records over
+torch.distributed (gloo here, NCCL on GPUs) and commits every rank's updates.
+The result must equal the single-process oracle MB-VI bit for bit: the
+protocol realises Eq. 12 exactly and is independent of the number of ranks.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gen
+import oracle
+import paper_2110_02901_b200 as rmb
+
+N, A, GAMMA, SEED, EPS = 37, 3, 0.9, 5, 1e-9
+
+
+def sharded_vi(rank, world, b, sweeps):
+    r0, r1 = rmb.shard_range(N, world, rank)
+    P, c = gen.dense(N, A, 11, dtype=np.float64)
+    Pl, cl = P[r0:r1], c[r0:r1]
+    cap = min(b, -(-N // world))
+    V = np.zeros(N)
+    pi = np.zeros(N, np.int32)
+    trace = []
+    for k in range(1, sweeps + 1):
+        perm = rmb.partition(N, SEED, k)
+        r = 0.0
+        for lo in range(0, N, b):
+            batch = perm[lo:lo + b]
+            mine = [int(s) for s in batch if r0 <= s < r1]
+            assert len(mine) <= cap
+            rec = torch.zeros(1 + 3 * cap, dtype=torch.float64)
+            rec[0] = len(mine)
+            for q, s in enumerate(mine):
+                v, a = oracle.backup_dense_row(Pl[s - r0], cl[s - r0], GAMMA, V)
+                rec[1 + q], rec[1 + cap + q], rec[1 + 2 * cap + q] = v, s, a
+            recs = [torch.zeros_like(rec) for _ in range(world)]
+            dist.all_gather(recs, rec)
+            for g in range(world):
+                cnt = int(recs[g][0])
+                for q in range(cnt):
+                    v = float(recs[g][1 + q])
+                    s = int(recs[g][1 + cap + q])
+                    r = max(r, abs(v - V[s]))
+                    V[s] = v
+                    if r0 <= s < r1:
+                        pi[s] = int(recs[g][1 + 2 * cap + q])
+        trace.append(r)
+    return V, pi, np.array(trace), (r0, r1)
+
+
+def _worker(rank, world, port, b, sweeps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        V, pi, tr, (r0, r1) = sharded_vi(rank, world, b, sweeps)
+        out[rank] = (V, pi[r0:r1], tr, r0, r1)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("b", [1, 4, 10, N])
+def test_two_rank_gloo_protocol_equals_oracle(b):
+    world, sweeps = 2, 6
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, _free_port(), b, sweeps, out), nprocs=world, join=True)
+        res = dict(out)
+    P, c = gen.dense(N, A, 11, dtype=np.float64)
+    ref = oracle.vi(oracle.MDP(N, A, GAMMA, c, P=P), b, seed=SEED, eps=1e-300, max_sweeps=sweeps)
+    pi = np.zeros(N, np.int32)
+    for rank in range(world):
+        V, pil, tr, r0, r1 = res[rank]
+        assert np.array_equal(V, ref.V)          # every replica is the oracle's V, bit for bit
+        assert np.array_equal(tr, ref.trace)     # and so is the residual trace
+        pi[r0:r1] = pil
+    assert np.array_equal(pi, ref.pi)
+
+
+def test_shard_ranges_partition_the_states():
+    for n in (1, 2, 5, 37, 10_000, 50_000):
+        for G in (1, 2, 3, 4, 7, 8):
+            spans = [rmb.shard_range(n, G, g) for g in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
+                assert e0 == b1 and b0 <= e0
+            assert max(e - b for b, e in spans) == -(-n // G)
