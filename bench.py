@@ -229,9 +229,20 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
-    # each rank solves its own instance (replicas)
-    P, c = rmb.generate_dense(N_STATES, N_ACTIONS, INST_SEED + rank)
-    prob = rmb.Problem.dense(P, c, GAMMA)
+    comm = None
+    if world == 1:
+        P, c = rmb.generate_dense(N_STATES, N_ACTIONS, INST_SEED)
+        prob = rmb.Problem.dense(P, c, GAMMA)
+        rows = (0, N_STATES)
+    else:
+        # the sharded path: this rank's rows of the ONE config-2
+        # instance, V replicated, per-batch NCCL all-gather of the updates
+        rows = rmb.shard_range(N_STATES, world, rank)
+        P, c = rmb.generate_dense(N_STATES, N_ACTIONS, INST_SEED, rows=rows)
+        uid = [rmb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = rmb.nccl_comm_init(world, rank, uid[0])
+        prob = rmb.Problem.dense(P, c, GAMMA, n=N_STATES, row_range=rows, nccl_comm=comm)
     V = torch.zeros(N_STATES, dtype=torch.float64, device=dev)
     pi = torch.zeros(N_STATES, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
@@ -266,15 +277,15 @@ def main():
     t = ev0.elapsed_time(ev1) / 1e3
     tt = torch.tensor([t, sweeps], dtype=torch.float64, device=dev)
     if dist:
+        # one instance sharded over the ranks: every rank runs the same sweeps
+        # and together they back up every state once per sweep; time = max
         tmax = tt.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tot = tt.clone()
-        dist.all_reduce(tot[1:], op=dist.ReduceOp.SUM)
-        t, sweeps_all = float(tmax[0]), float(tot[1])
-    else:
-        sweeps_all = sweeps
-    value = sweeps_all * N_STATES * N_ACTIONS / t
+        t = float(tmax[0])
+    value = sweeps * N_STATES * N_ACTIONS / t
 
+    # roofline of THIS rank's kernels: its rows of P per sweep
+    frac_rows = (rows[1] - rows[0]) / N_STATES
     peak, peak_src = peaks()
     traffic = None
     try:  # DRAM bytes per sweep of the solver kernel from the committed ncu --set full capture
@@ -284,14 +295,17 @@ def main():
     except Exception:
         pass
     bps = algo_bytes_per_sweep(N_STATES, N_ACTIONS, 4, args.b)
-    achieved = sweeps * bps / kernel_s / 1e9  # per launch = whole solve kernel
+    if world > 1:
+        bps = int(bps * frac_rows)
+    achieved = sweeps * bps / kernel_s / 1e9  # per launch = whole solve kernel (N=1); per rank share (N>1)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "b": args.b, "sweeps_per_solve": sweeps / args.steps,
                    "l2": "inputs larger than L2 (P 6.4 GB) + 256 MB flush between solves",
-                   "parallelism": f"replicas{world}" if world > 1 else "dp1"},
+                   "parallelism": f"shard{world} (rows by state, V replicated, NCCL all-gather per batch)"
+                   if world > 1 else "dp1"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_note": "dram read+write bytes per launch = per-sweep DRAM bytes of the committed "
@@ -303,7 +317,7 @@ def main():
         "clocks": clk.summary(),
     }
 
-    if rank == 0 and not args.no_bsweep:
+    if rank == 0 and world == 1 and not args.no_bsweep:
         table = []
         for b in (1, 64, 1000, 10_000):
             sol = solve(b, seed=7)
@@ -316,7 +330,7 @@ def main():
                           "GB_per_s": st.sweeps * bb / st.seconds / 1e9})
         result["time_to_eps_vs_b"] = table
 
-    if rank == 0 and not args.no_e2e:
+    if rank == 0 and world == 1 and not args.no_e2e:
         # e2e through the C ABI with HOST buffers: H2D of P, c inside the timed region
         Ph = torch.empty(P.shape, dtype=P.dtype, pin_memory=True)
         ch = torch.empty(c.shape, dtype=c.dtype, pin_memory=True)
@@ -348,10 +362,10 @@ def main():
                          "d2h_bytes_per_step": int(N_STATES * 8 + N_STATES * 4 + 8 * sw / ksteps),
                          "steps": ksteps, "path": "rmb_create_dense(host P,c) + rmb_vi(host V,pi) + rmb_destroy"}
 
-    if rank == 0 and not args.no_other:
+    if rank == 0 and world == 1 and not args.no_other:
         result["other_configs"] = other_configs(rmb, torch, dev)
 
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         rate, cores, sample = oracle_sample()
         result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
 
@@ -359,6 +373,8 @@ def main():
         print(json.dumps(result), flush=True)
     if dist:
         dist.barrier()
+        del prob
+        rmb.nccl_comm_destroy(comm)
         dist.destroy_process_group()
     return 0
 

@@ -229,7 +229,8 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         for (int r = 0; r < G_local; ++r) {
             RankWs& w = ws[r];
             cudaError_t e = launch_partition(n, rq0.seed, k, rq0.identity, w.perm, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(w.resid, 0, 32, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(w.resid, 0, 8, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(w.bad, 0, sizeof(int), st);
             if (rmb_status s = check(e, "shard partition"); s != RMB_OK) return s;
             ++launches;
         }
