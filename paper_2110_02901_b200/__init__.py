@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librmb.so")
+LIB_PATH = os.environ.get("RMB_LIB_PATH") or os.path.join(_HERE, "librmb.so")  # override: experiments only
 
 # status codes (include/rmb.h)
 OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(9)
@@ -103,7 +103,7 @@ def lib():
     global _lib
     if _lib is None:
         from . import _build
-        if _build.needs_build():
+        if LIB_PATH == _build.SO and _build.needs_build():
             _build.build()
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"librmb.so not found at {LIB_PATH}; run __graft_entry__.build()")

@@ -52,16 +52,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """out/defines: alternative builds for A/B experiments (never the product .so)."""
+    so = out or SO
+    if not force and out is None and not needs_build():
         return SO
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD if out is None else BUILD + "_" + os.path.basename(out).replace(".so", "")
+    os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        r = subprocess.run([nvcc] + NVFLAGS + ["-c", src, "-o", obj], capture_output=True, text=True)
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        r = subprocess.run([nvcc] + NVFLAGS + dflags + ["-c", src, "-o", obj], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         with open(obj + ".ptxas.txt", "w") as f:
@@ -70,15 +74,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     r = subprocess.run([nvcc] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, SO)
+    os.replace(tmp, so)
     if verbose:
         for o in objs:
             print(open(o + ".ptxas.txt").read())
-    return SO
+    return so
 
 
 if __name__ == "__main__":

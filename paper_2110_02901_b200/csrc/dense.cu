@@ -45,6 +45,7 @@ namespace rmb {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kAG = 4;                     // actions per compute item (min modes)
+constexpr int kPathWarp = 0, kPathCta = 1, kPathRows = 2;  // compute path of a kernel instantiation
 constexpr int64_t kRedundantMax = 8192;    // doubles of batch partials reduced by every CTA
 
 struct Plan {
@@ -52,6 +53,7 @@ struct Plan {
     int C;          // chunks per row
     int redundant;  // 1: every CTA reduces every state (single barrier)
     int cta;        // 1: CTA-cooperative tile pipeline, 0: warp-owned items
+    int rows;       // 1: CTA-per-state rows mode (whole rows, C = 1, ng = A)
     int ng;         // action rows per warp item in min modes (4, or 1 for short-tail batches)
 };
 
@@ -88,6 +90,10 @@ struct DenseArgs {
     int64_t chg_len;
     long long* out;
     unsigned int* wctr;  // [2] work-stealing counters (phase parity)
+    int path;            // compute path (kPathWarp / kPathCta / kPathRows)
+    unsigned int* pctr;  // [2] tail-prefetch counters (phase parity)
+    int64_t pf_bytes;    // tail-prefetch budget per batch (bytes of P)
+    int64_t vs_half;     // smem V: offset of the hi plane (VE == 4), 0 = linear
     // multi-GPU shard steps
     int64_t row0, row1;        // owned states (P and c are offset so that global state ids index them)
     const uint32_t* olist;     // this rank's states of the batch (compacted)
@@ -127,12 +133,22 @@ struct Vec<double, 1> {
     __device__ static __forceinline__ void get(const T& x, double (&d)[1]) { d[0] = x; }
 };
 
+// Shared-memory layout of V.  With float4 P vectors (VE == 4) a lane needs
+// V[j..j+3] (32 B); stored linearly, 8 lanes of a quarter warp would hit the
+// same banks twice.  So V is split into two planes: lo holds (V[4q], V[4q+1])
+// at [2q, 2q+1], hi holds (V[4q+2], V[4q+3]) at half + [2q, 2q+1]; each
+// 128-bit read is then at a 16-byte lane stride (conflict-free).  Other VE: linear.
+__device__ __forceinline__ int64_t vs_index(int64_t j, int64_t half)
+{
+    return half ? ((j & 2) ? half : 0) + ((j >> 2) << 1) + (j & 1) : j;
+}
+
 template <int VE>
-__device__ __forceinline__ void load_v(const double* Vs, int64_t j, double (&v)[VE])
+__device__ __forceinline__ void load_v(const double* Vs, int64_t j, double (&v)[VE], int64_t half = 0)
 {
     if constexpr (VE == 4) {
-        const double2 a = *reinterpret_cast<const double2*>(Vs + j);
-        const double2 b = *reinterpret_cast<const double2*>(Vs + j + 2);
+        const double2 a = *reinterpret_cast<const double2*>(Vs + (j >> 1));
+        const double2 b = *reinterpret_cast<const double2*>(Vs + half + (j >> 1));
         v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
     } else if constexpr (VE == 2) {
         const double2 a = *reinterpret_cast<const double2*>(Vs + j);
@@ -146,9 +162,18 @@ __device__ __forceinline__ void load_v(const double* Vs, int64_t j, double (&v)[
 // in increasing j order per lane (fixed order -> reproducible).
 template <typename PT, int VE, int NG, int U>
 __device__ __forceinline__ void dot_rows(const PT* __restrict__ row0, int64_t n, int na, int64_t j0,
-                                         int64_t j1, const double* Vs, int lane, double (&acc)[NG])
+                                         int64_t j1, const double* Vs, int lane, double (&acc)[NG], int64_t half)
 {
     using VT = typename Vec<PT, VE>::T;
+    // single-row streams keep VE independent partial sums (one per vector
+    // component) so the fp64 FMA chain per iteration is U long, not U*VE;
+    // multi-row streams already interleave NG chains
+    constexpr int NA = 1;  // (VE partial sums for single rows measured slower: register pressure)
+    double part[NG][NA];
+#pragma unroll
+    for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int e = 0; e < NA; ++e) part[g][e] = 0.0;
     const int64_t nvec = (j1 - j0) / VE;  // j0, j1 multiples of VE
     const VT* rows[NG];
 #pragma unroll
@@ -167,18 +192,25 @@ __device__ __forceinline__ void dot_rows(const PT* __restrict__ row0, int64_t n,
             const int64_t vv = v + (int64_t)kWarp * u;
             if (vv < nvec) {
                 double vs[VE];
-                load_v<VE>(Vs, j0 + vv * VE, vs);
+                load_v<VE>(Vs, j0 + vv * VE, vs, half);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     if (g < na) {
                         double p[VE];
                         Vec<PT, VE>::get(x[u][g], p);
 #pragma unroll
-                        for (int e = 0; e < VE; ++e) acc[g] = fma(p[e], vs[e], acc[g]);
+                        for (int e = 0; e < VE; ++e) part[g][e % NA] = fma(p[e], vs[e], part[g][e % NA]);
                     }
                 }
             }
         }
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        double t = part[g][0];
+        if constexpr (NA == 4) t = (part[g][0] + part[g][1]) + (part[g][2] + part[g][3]);
+        if constexpr (NA == 2) t = part[g][0] + part[g][1];
+        acc[g] += t;
     }
 }
 
@@ -253,9 +285,21 @@ __device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const doub
 //   C == 1, min : part[2(i*NAG+ag)+{0,1}] = (min Q over the group, argmin)   (2*NAG)
 //   C >  1, EVAL: part[i*C + ch]               (C)
 //   C >  1, min : part[(i*A + a)*C + ch]       (A*C)
+// Tail prefetch: a warp that finds no more items in this batch asks a second
+// counter for items of the NEXT batch (same decomposition, grabbed in the same
+// order there) and issues one cp.async.bulk.prefetch.L2 per row chunk, so the
+// HBM bandwidth the end-of-batch tail leaves idle fetches the next batch's
+// first items into L2 (a bounded budget so they are still there when used).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <typename PT, int VE, bool EVAL, int NGT>
 __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
-                              int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
+                              int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr,
+                              const uint32_t* perm_next = nullptr, int64_t lo_next = 0, int64_t cnt_next = 0,
+                              unsigned int* pctr = nullptr)
 {
     const int lane = threadIdx.x & 31;
     const int C = pl.C;
@@ -288,7 +332,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
         double acc[NG];
 #pragma unroll
         for (int g = 0; g < NG; ++g) acc[g] = 0.0;
-        dot_rows<PT, VE, NG, U>(P + ((int64_t)s * a.A + a0) * a.n, a.n, na, j0, j1, Vs, lane, acc);
+        dot_rows<PT, VE, NG, U>(P + ((int64_t)s * a.A + a0) * a.n, a.n, na, j0, j1, Vs, lane, acc, a.vs_half);
 #pragma unroll
         for (int g = 0; g < NG; ++g) acc[g] = warp_sum(acc[g]);
         if (C == 1) {
@@ -344,6 +388,28 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
             }
         }
         it = it_next;
+    }
+    if (cnt_next > 0 && pctr && VE > 1 && a.pf_bytes > 0) {
+        const int64_t items_next = cnt_next * per_state;
+        const int64_t item_bytes = (int64_t)NG * Lc * (int64_t)sizeof(PT);
+        const int64_t budget = min(items_next, max((int64_t)1, a.pf_bytes / item_bytes));
+        while (true) {
+            unsigned int r = 0;
+            if (lane == 0) r = atomicAdd(pctr, 1u);
+            r = __shfl_sync(0xffffffffu, r, 0);
+            if ((int64_t)r >= budget) break;
+            const int64_t i = (int64_t)r / per_state;
+            const int rr = (int)((int64_t)r - i * per_state);
+            const int ag = rr / C;
+            const int ch = rr - ag * C;
+            const int64_t s = min(a.n - 1, perm_next ? (int64_t)__ldcg(perm_next + lo_next + i) : lo_next + i);
+            const int a0 = EVAL ? pis[s] : ag * NG;
+            const int na = EVAL ? 1 : min(NG, a.A - a0);
+            const int64_t j0 = (int64_t)ch * Lc;
+            const int64_t j1 = min(a.n, j0 + Lc);
+            if (lane < na)
+                prefetch_l2(P + ((int64_t)s * a.A + a0 + lane) * a.n + j0, (uint32_t)((j1 - j0) * sizeof(PT)));
+        }
     }
 }
 
@@ -523,7 +589,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         for (int u = 0; u < U2; ++u) {
             if (cleft > kCT * u) {
                 double vs[VE];
-                load_v<VE>(Vs, cvo + kCT * VE * u, vs);
+                load_v<VE>(Vs, cvo + kCT * VE * u, vs, a.vs_half);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     if (g < cna) {
@@ -622,6 +688,138 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
         }
     }
     __syncthreads();  // pairs with the producer's; every epilogue is complete
+}
+
+// ------------------------------------------------ CTA-per-state rows mode
+// For batches that offer >= 4 states per SM: an ITEM is g = max(1, 16/A)
+// whole states; the CTA's 16 warps take its action rows (warp w: rows w,
+// w+16, ...) and stream each WHOLE row with 8 x 128-bit loads in flight per
+// lane (one warp reduction per row, as in the warp-item path).  A state's
+// (min Q, argmin) is taken in shared memory by the last warp to finish the
+// item, in action order (lowest index on ties).  An item is ~15 us of one SM's
+// HBM share, so the end-of-batch tail is ~4x shorter than with warp-owned
+// 4-row items, and no per-state partials or global atomics are needed.
+// Items come from the global work-stealing counter through a 4-deep smem ring
+// refilled by the last warp of each item.
+constexpr int kRR = 4;          // ring depth
+constexpr int kRowsMax = 64;    // actions per state supported by rows mode
+
+struct RowsRing {
+    long long it[kRR];
+    int ready[kRR];
+    int arrive[kRR];
+    double q[kRR][kRowsMax];
+};
+
+template <typename PT, int VE, bool EVAL>
+__device__ void compute_phase_rows(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
+                                   int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
+{
+    __shared__ RowsRing rr;
+    __shared__ long long r_base;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int Ae = EVAL ? 1 : a.A;
+    const int gst = max(1, kWarps / Ae);  // states per item
+    const int64_t items = (cnt + gst - 1) / gst;
+    const PT* P = static_cast<const PT*>(a.P);
+    __syncthreads();  // the previous phase is done with rr
+    if (threadIdx.x < kRR) {
+        rr.arrive[threadIdx.x] = 0;
+        rr.ready[threadIdx.x] = -1;
+    }
+    if (threadIdx.x == 0) r_base = (long long)atomicAdd(ctr, (unsigned int)kRR);
+    __syncthreads();
+    if (threadIdx.x < kRR) {
+        rr.it[threadIdx.x] = r_base + threadIdx.x;
+        rr.ready[threadIdx.x] = threadIdx.x;
+    }
+    __syncthreads();
+    volatile RowsRing& vr = rr;
+    // a grab issued by this warp's last epilogue, published after its next
+    // row so that the atomic's latency hides behind the streaming
+    bool pending = false;
+    int pend_sl = 0, pend_q = 0;
+    unsigned int pend_it = 0;
+    auto publish = [&]() {
+        if (pending && lane == 0) {
+            vr.it[pend_sl] = (long long)pend_it;  // smem stores of one thread land in order:
+            vr.ready[pend_sl] = pend_q;           // the slot is complete once ready is seen
+        }
+        pending = false;
+    };
+    for (int q = 0;; ++q) {
+        const int sl = q & (kRR - 1);
+        while (vr.ready[sl] != q) {
+        }
+        const long long it = vr.it[sl];
+        if (it >= items) {
+            publish();
+            break;
+        }
+        const int64_t i0 = it * gst;
+        const int ns = (int)min((int64_t)gst, cnt - i0);
+        for (int r = warp; r < ns * Ae; r += kWarps) {
+            const int ist = r / Ae;
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i0 + ist) : lo + i0 + ist;
+            const int act = EVAL ? pis[s] : r - ist * Ae;
+            double acc[1] = {0.0};
+            dot_rows<PT, VE, 1, 8>(P + ((int64_t)s * a.A + act) * a.n, a.n, 1, 0, a.n, Vs, lane, acc, a.vs_half);
+            const double d = warp_sum(acc[0]);
+            if (lane == 0) rr.q[sl][r] = load_cost<PT>(a, s * a.A + act) + a.gamma * d;
+            publish();
+        }
+        publish();
+        int last = 0;
+        if (lane == 0) last = atomicAdd(&rr.arrive[sl], 1) == kWarps - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+#ifndef RMB_ROWS_VARIANT
+#define RMB_ROWS_VARIANT 1
+#endif
+        if (last && lane == 0) {
+            for (int ist = 0; ist < ns; ++ist) {
+                const int64_t i = i0 + ist;
+                double best = vr.q[sl][ist * Ae];
+                int barg = 0;
+                if (EVAL) {
+                    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                    barg = pis[s];
+                } else {
+                    for (int act = 1; act < Ae; ++act) {
+                        const double Q = vr.q[sl][ist * Ae + act];
+                        if (Q < best) best = Q, barg = act;
+                    }
+                }
+                if (pl.redundant) {
+                    if (EVAL) {
+                        part[i] = best;
+                    } else {
+                        part[2 * i] = best;
+                        part[2 * i + 1] = (double)barg;
+                    }
+                } else {
+                    a.lval[i] = best;
+                    a.larg[i] = barg;
+                }
+            }
+            vr.arrive[sl] = 0;
+#if RMB_ROWS_VARIANT == 2
+            pend_it = atomicAdd(ctr, 1u);  // consumed at publish()
+            pend_sl = sl;
+            pend_q = q + kRR;
+            pending = true;
+#else
+            vr.it[sl] = (long long)atomicAdd(ctr, 1u);
+#if RMB_ROWS_VARIANT == 0
+            __threadfence_block();
+#endif
+            vr.ready[sl] = q + kRR;
+#endif
+        }
+        pending = __shfl_sync(0xffffffffu, pending ? 1 : 0, 0) != 0;
+        __syncwarp();
+    }
+    __syncthreads();
 }
 
 struct PhaseAcc {
@@ -729,7 +927,8 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
         }
         return;
     }
-    const double old = Vs[s];
+    const int64_t vi = vs_index(s, a.vs_half);
+    const double old = Vs[vi];
     acc.rmax = fmax(acc.rmax, fabs(v - old));
     acc.bad |= !isfinite(v);
     const bool writer = blockIdx.x == 0;
@@ -738,7 +937,7 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
         pis[s] = arg;
         if (writer) a.pi[s] = arg;
     } else {
-        Vs[s] = v;
+        Vs[vi] = v;
         if (writer) {
             a.V[s] = v;
             if (KIND == 0 && a.pi) a.pi[s] = arg;
@@ -772,19 +971,28 @@ __device__ __forceinline__ void timed_sync(Ctx& x)
 }
 
 // One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
-template <typename PT, int VE, int KIND, bool CTA>
+template <typename PT, int VE, int KIND, int CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
-                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
+                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k,
+                          const uint32_t* perm_next = nullptr, int64_t lo_next = 0, int64_t cnt_next = 0)
 {
     constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
     // the other parity's work counter was last used before the previous
     // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
-    if constexpr (CTA)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
+        atomicExch(a.pctr + ((x.phase + 1) & 1), 0u);
+    }
+    // one compute path per kernel instantiation (register allocation is per
+    // kernel: mixing paths made every path spill)
+    if constexpr (CTA == kPathRows)
+        compute_phase_rows<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+    else if constexpr (CTA == kPathCta)
         compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     else
-        compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
+        compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1), perm_next,
+                                         lo_next, cnt_next, a.pctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
@@ -843,7 +1051,7 @@ __device__ PhaseAcc block_reduce(PhaseAcc v)
 }
 
 // One application of B_b (EVAL = false) or B_{pi,b} (EVAL = true), sweep k.
-template <typename PT, int VE, bool EVAL, bool CTA>
+template <typename PT, int VE, bool EVAL, int CTA>
 __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, int64_t k, double* Qs)
 {
     const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
@@ -851,14 +1059,25 @@ __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* p
     PhaseAcc acc{0.0, 0, 0};
     for (int64_t lo = 0; lo < a.n; lo += a.b) {
         const int64_t cnt = min(a.b, a.n - lo);
+        // next batch for the tail prefetch: later in this sweep, or the first
+        // batch of the next sweep (its order was generated in batch 0)
+        const uint32_t* pn = perm;
+        int64_t ln = lo + a.b, cn = 0;
+        if (ln < a.n) {
+            cn = min(a.b, a.n - ln);
+        } else if (a.b < a.n && a.mode == MODE_VI) {
+            pn = a.identity ? nullptr : a.perm + ((k + 1) % 3) * a.n;
+            ln = 0;
+            cn = a.b;
+        }
         run_batch<PT, VE, EVAL ? 1 : 0, CTA>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
-                                         (lo == 0 && !a.identity) ? k + 1 : 0);
+                                         (lo == 0 && !a.identity) ? k + 1 : 0, pn, ln, cn);
         ++x.batches;
     }
     return block_reduce(acc);
 }
 
-template <typename PT, int VE, bool CTA>
+template <typename PT, int VE, int CTA>
 __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, double* Qs)
 {
     PhaseAcc acc{0.0, 0, 0};
@@ -869,12 +1088,12 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
     return block_reduce(acc);
 }
 
-template <typename PT, int VE, bool CTA>
+template <typename PT, int VE, int CTA>
 __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* Vs = reinterpret_cast<double*>(smem_raw);
-    const int64_t n_pad = (a.n + 1) & ~int64_t(1);
+    const int64_t n_pad = (a.n + 3) & ~int64_t(3);
     int32_t* pis = reinterpret_cast<int32_t*>(Vs + n_pad);
     double* Qs = reinterpret_cast<double*>(smem_raw + a.qs_off);
     const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE ||
@@ -882,7 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     const bool shard = a.mode >= MODE_SHARD_MIN;
 
     for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
-        Vs[j] = a.V[j];
+        Vs[vs_index(j, a.vs_half)] = a.V[j];
         if (need_pi) pis[j] = a.pi[j];
     }
     Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
@@ -1007,7 +1226,7 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     }
     int64_t L = (n + c - 1) / c;
     L = (L + unit - 1) / unit * unit;
-    Plan p;
+    Plan p{};
     p.Lc = (int)L;
     p.C = (int)((n + L - 1) / L);
     const int64_t per_state = p.C == 1 ? (A_eff == 1 ? 1 : 2 * groups_per_state) : (int64_t)A_eff * p.C;
@@ -1024,7 +1243,9 @@ static int64_t plan_doubles(const Plan& p, int64_t cnt, int64_t groups_per_state
 template <typename PT, int VE>
 static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaStream_t st)
 {
-    auto kern = a.plan[0].cta ? dense_solver_kernel<PT, VE, true> : dense_solver_kernel<PT, VE, false>;
+    auto kern = a.path == kPathRows ? dense_solver_kernel<PT, VE, kPathRows>
+                : a.path == kPathCta ? dense_solver_kernel<PT, VE, kPathCta>
+                                     : dense_solver_kernel<PT, VE, kPathWarp>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -1054,7 +1275,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
     const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE ||
                          rq.mode == MODE_SHARD_EVAL || rq.mode == MODE_SHARD_IMPROVE;
-    const int64_t n_pad = (n + 1) & ~int64_t(1);
+    const int64_t n_pad = (n + 3) & ~int64_t(3);
     const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
     if (smem_v + 12288 > pr.smem_optin) {
         set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
@@ -1071,6 +1292,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.c = static_cast<const char*>(pr.c) - (size_t)row0 * pr.A * psz;
     a.row0 = row0;
     a.row1 = row1;
+    a.vs_half = VE == 4 ? n_pad / 2 : 0;
     a.n = n;
     a.A = pr.A;
     a.gamma = pr.gamma;
@@ -1099,14 +1321,46 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.plan[0].ng = ng_b;
     a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok, 1, psz);
     a.plan[1].ng = 1;
+    // CTA-per-state rows mode for batches with >= 4 items (state groups) per SM
+    auto rows_plan = [&](Plan& p, int64_t cnt, int Ae) {
+        // measured: equal to the warp path at b = 1000 (tail 4x shorter, streaming
+        // ~9 % slower), slower at b = n -> opt-in
+        const char* e = getenv("RMB_DENSE_ROWS");
+        if (!(e && e[0] == '1')) return;
+        const int gst = std::max(1, kWarps / Ae);
+        if (pr.A > kRowsMax || p.cta || (cnt + gst - 1) / gst < 4LL * sms) return;
+        p.rows = 1;
+        p.C = 1;
+        p.Lc = (int)n;
+        p.ng = Ae;  // one (min, argmin) pair per state
+        p.redundant = cnt * (Ae == 1 ? 1 : 2) <= kRedundantMax ? 1 : 0;
+    };
+    Plan rp[3] = {a.plan[0], a.plan[1], a.plan[2]};
+    rows_plan(rp[0], rq.b, pr.A);
+    rows_plan(rp[1], rq.b, 1);
     // improvement (no V write): as few sub-batches as a bounded scratch allows
     const int64_t NAG4 = (pr.A + kAG - 1) / kAG;
     a.imp_sub = n * NAG4 * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / (2 * NAG4));
     a.plan[2] = plan_chunks(n, a.imp_sub, NAG4, pr.A, VE, sms, split_ok, kAG, psz);
     a.plan[2].ng = kAG;
+    rp[2] = a.plan[2];
+    rows_plan(rp[2], a.imp_sub, pr.A);
+    // the plans a launch uses must all be on one compute path (one kernel
+    // instantiation each): rows if every used plan qualifies, else warp / CTA
+    bool rows = false;
+    switch (rq.mode) {
+    case MODE_VI: case MODE_APPLY: case MODE_SHARD_MIN: rows = rp[0].rows; break;
+    case MODE_APPLY_PI: case MODE_SHARD_EVAL: rows = rp[1].rows; break;
+    case MODE_IMPROVE: case MODE_SHARD_IMPROVE: rows = rp[2].rows; break;
+    default: rows = rp[1].rows && rp[2].rows; break;  // MPI
+    }
+    if (rows)
+        for (int q = 0; q < 3; ++q) a.plan[q] = rp[q];
+    a.path = rows ? kPathRows : a.plan[0].cta ? kPathCta : kPathWarp;
     const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
-                                              plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A)});
+                                              plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A), 2 * rq.b,
+                                              2 * a.imp_sub});
     a.part_stride = (stride + 31) / 32 * 32;
     L.lcap = std::max<int64_t>(rq.b, a.imp_sub);
     L.VE = VE;
@@ -1128,6 +1382,11 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.out = reinterpret_cast<long long*>(ctrl + 128);      // [128..136)
     a.prof = reinterpret_cast<long long*>(ctrl + 192);     // [192..196)
     a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256);  // [256]
+    a.pctr = reinterpret_cast<unsigned int*>(ctrl + 260);  // [260]
+    {
+        const char* e = getenv("RMB_PREFETCH_MB");
+        a.pf_bytes = (int64_t)(e ? atof(e) : 0.0) * (1 << 20);  // measured: no gain at b = 1000 -> opt-in
+    }
     a.trace = trace_dev;
     a.trace_len = trace_len;
     a.chg = chg_dev;
