@@ -259,7 +259,14 @@ __device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const doub
     for (int act = lane; act < a.A; act += kWarp) {
         const double* pp = part + (i * a.A + act) * C;
         double sum = 0.0;
-        for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + ch);
+        for (int c0 = 0; c0 < C; c0 += 8) {  // issue up to 8 loads, then add in chunk order
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = c0 + q < C ? __ldcg(pp + c0 + q) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (c0 + q < C) sum += t[q];
+        }
         const double Q = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
         if (barg == 0x7fffffff || Q < best) best = Q, barg = act;
     }
@@ -312,19 +319,40 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
     constexpr int U = NG == 1 ? 8 : 2;
     // dynamic work stealing over the whole grid (balances SMs whose HBM share
     // differs); the next item index is fetched while the current one streams
+    // batches with at most one item per warp: a static deal (CTA-major, so
+    // the items spread over all SMs) — 2368 warps grabbing from ONE counter at
+    // the same instant serialise on that L2 address for several microseconds
+    const int64_t W = (int64_t)gridDim.x * kWarps;
+    const bool stat = items <= W;
+    int64_t static_it = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     auto grab = [&]() -> int64_t {
+        if (stat) {
+            const int64_t r = static_it;
+            static_it = items;  // one item per warp
+            return r;
+        }
         unsigned int r = 0;
         if (lane == 0) r = atomicAdd(ctr, 1u);
         return (int64_t)__shfl_sync(0xffffffffu, r, 0);
     };
+    // the next item is requested while this one streams (1 deep: a deeper
+    // reservation turns the end of the batch into a static deal), and its
+    // state id (a dependent L2 load) is looked up right after this item's
+    // rows have streamed, overlapping the epilogue
+    auto state_of = [&](int64_t t) -> int64_t {
+        if (t >= items) return 0;
+        const int64_t i = t / per_state;
+        return perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+    };
     int64_t it = grab();
+    int64_t s_cur = state_of(it);
     while (it < items) {
         const int64_t it_next = grab();
         const int64_t i = it / per_state;
         const int rr = (int)(it - i * per_state);
         const int ag = rr / C;
         const int ch = rr - ag * C;
-        const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+        const int64_t s = s_cur;
         const int a0 = EVAL ? pis[s] : ag * NG;
         const int na = EVAL ? 1 : min(NG, a.A - a0);
         const int64_t j0 = (int64_t)ch * Lc;
@@ -333,6 +361,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
 #pragma unroll
         for (int g = 0; g < NG; ++g) acc[g] = 0.0;
         dot_rows<PT, VE, NG, U>(P + ((int64_t)s * a.A + a0) * a.n, a.n, na, j0, j1, Vs, lane, acc, a.vs_half);
+        const int64_t s_next = state_of(it_next);
 #pragma unroll
         for (int g = 0; g < NG; ++g) acc[g] = warp_sum(acc[g]);
         if (C == 1) {
@@ -388,6 +417,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
             }
         }
         it = it_next;
+        s_cur = s_next;
     }
     if (cnt_next > 0 && pctr && VE > 1 && a.pf_bytes > 0) {
         const int64_t items_next = cnt_next * per_state;
@@ -1215,7 +1245,8 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     }();
     if (allow_split && rows < 16LL * num_sms) {
         (void)lc_target;
-        c = (32LL * num_sms + rows - 1) / rows;
+        // at most one item per warp (the dynamic deal then has no second round)
+        c = std::max<int64_t>(1, (16LL * num_sms) / rows);
         if (use_cta) {  // CTA tiles: at least one full slot (512 threads x 4 vectors) per tile
             const int64_t min_lc = (int64_t)kCT * VE * (kSlotLoads / ng);
             c = std::min<int64_t>(c, std::max<int64_t>(1, n / min_lc));
