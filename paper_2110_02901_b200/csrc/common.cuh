@@ -67,8 +67,41 @@ __device__ __forceinline__ unsigned long long globaltimer_ns()
 
 // Hang guard: a barrier that waits more than 30 s means a broken grid
 // (not all CTAs resident); trap instead of wedging the GPU.
+#ifndef RMB_BARRIER_VARIANT
+#define RMB_BARRIER_VARIANT 1
+#endif
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ void grid_sync(GridBarrier& g)
 {
+#if RMB_BARRIER_VARIANT == 1
+    // arrive with a fire-and-forget release reduction, then poll the arrival
+    // counter itself (no separate release flag round trip)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        g.epoch += 1;
+        const unsigned long long target = g.epoch * g.nblocks;
+        red_release_add(g.arrive, 1ULL);
+        unsigned long long t0 = 0;
+        unsigned spins = 0;
+        while (ld_acquire_gpu(g.arrive) < target) {
+            if (++spins == 4096u) {
+                spins = 0;
+                unsigned long long t = globaltimer_ns();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > 30ull * 1000000000ull) {
+                    atomicExch(g.error_flag, 1);
+                    __trap();
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return;
+#endif
     __syncthreads();
     if (threadIdx.x == 0) {
         g.epoch += 1;
