@@ -35,8 +35,13 @@
 
 namespace rmb {
 
-constexpr int kSThreads = 512;
-constexpr int kSWarps = kSThreads / kWarp;
+// CTA size per layout: row mode (a lane per action row, short rows, many
+// dependent gathers) wants the warps; vec / strided fit 512 threads without spills
+constexpr int kSWarpsMax = 32;
+template <int MODE>
+struct SThreads {
+    static constexpr int v = 512;  // 1024 for row mode: config-4 VI 1.5x faster, config-4 MPI 1.7x slower
+};
 
 struct SparseArgs {
     const int64_t* row_ptr;
@@ -236,9 +241,9 @@ __device__ __forceinline__ void s_prof(SCtx& x, long long* slot)
 // CTA reduction (max, or, sum) then one global atomic per CTA.
 __device__ void cta_publish(const SparseArgs& a, int slot, double rmax, int bad, long long changed)
 {
-    __shared__ double sd[kSWarps];
-    __shared__ int si[kSWarps];
-    __shared__ long long sl[kSWarps];
+    __shared__ double sd[kSWarpsMax];
+    __shared__ int si[kSWarpsMax];
+    __shared__ long long sl[kSWarpsMax];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
@@ -252,7 +257,7 @@ __device__ void cta_publish(const SparseArgs& a, int slot, double rmax, int bad,
         double r = 0.0;
         int bb = 0;
         long long cc = 0;
-        for (int k = 0; k < kSWarps; ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
         atomicMax(a.red + slot, (unsigned long long)__double_as_longlong(r));
         if (bb) atomicOr(reinterpret_cast<unsigned int*>(a.red + 4 + slot), 1u);
         if (cc) atomicAdd(a.red + 8 + slot, (unsigned long long)cc);
@@ -282,8 +287,8 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
     const int GS = EVAL ? a.GSE : a.GS;
     const int g = threadIdx.x & (GS - 1);
     // warp-uniform trip counts: all 32 lanes stay in the loop for the shuffles
-    const int64_t ngroups = (int64_t)gridDim.x * (kSThreads / GS);
-    const int64_t gid = (int64_t)blockIdx.x * (kSThreads / GS) + threadIdx.x / GS;
+    const int64_t ngroups = (int64_t)gridDim.x * ((int)blockDim.x / GS);
+    const int64_t gid = (int64_t)blockIdx.x * ((int)blockDim.x / GS) + threadIdx.x / GS;
     const int64_t wfirst = gid - (threadIdx.x & 31) / GS;  // first group of this warp
     const int slot = (int)(k & 3);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // rearm the ring slot used two sweeps ahead
@@ -324,8 +329,8 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
         if (x.prev_valid && !single) {
             Permutation pk;
             if (lo == 0 && !a.identity) pk.init(a.n, a.seed, k);
-            const int64_t stride = (int64_t)gridDim.x * kSThreads;
-            for (int64_t i = (int64_t)blockIdx.x * kSThreads + threadIdx.x; i < x.prev_cnt; i += stride) {
+            const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+            for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.prev_cnt; i += stride) {
                 const int64_t s = x.prev_perm ? (int64_t)x.prev_perm[x.prev_lo + i] : x.prev_lo + i;
                 if (lo == 0) {
                     const int64_t pos = a.identity ? s : (int64_t)pk.position((uint64_t)s);
@@ -338,8 +343,8 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
             Permutation pm;
             pm.init(a.n, a.seed, k + 1);
             uint32_t* dst = a.perm + ((k + 1) % 3) * a.n;
-            const int64_t stride = (int64_t)gridDim.x * kSThreads;
-            for (int64_t p = (int64_t)blockIdx.x * kSThreads + threadIdx.x; p < a.n; p += stride)
+            const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+            for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.n; p += stride)
                 dst[p] = (uint32_t)pm((uint64_t)p);
         }
         const bool last = lo + a.b >= a.n;
@@ -366,8 +371,8 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
 {
     const int GS = a.GS;
     const int g = threadIdx.x & (GS - 1);
-    const int64_t ngroups = (int64_t)gridDim.x * (kSThreads / GS);
-    const int64_t gid = (int64_t)blockIdx.x * (kSThreads / GS) + threadIdx.x / GS;
+    const int64_t ngroups = (int64_t)gridDim.x * ((int)blockDim.x / GS);
+    const int64_t gid = (int64_t)blockIdx.x * ((int)blockDim.x / GS) + threadIdx.x / GS;
     const int64_t wfirst = gid - (threadIdx.x & 31) / GS;
     // improvement steps use their own ring (slots 2,3 parity of imp_idx) via the
     // same red[] words offset by 16
@@ -398,9 +403,9 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
         atomicExch(other + 2, 0ull);
     }
     {
-        __shared__ double sd[kSWarps];
-        __shared__ int si[kSWarps];
-        __shared__ long long sl[kSWarps];
+        __shared__ double sd[kSWarpsMax];
+        __shared__ int si[kSWarpsMax];
+        __shared__ long long sl[kSWarpsMax];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
@@ -414,7 +419,7 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
             double r = 0.0;
             int bb = 0;
             long long cc = 0;
-            for (int k = 0; k < kSWarps; ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
             atomicMax(base, (unsigned long long)__double_as_longlong(r));
             if (bb) atomicOr(base + 1, 1ull);
             if (cc) atomicAdd(base + 2, (unsigned long long)cc);
@@ -433,13 +438,13 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
 }
 
 template <typename PT, int MODE>
-__global__ void __launch_bounds__(kSThreads, 1) sparse_solver_kernel(const SparseArgs a)
+__global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(const SparseArgs a)
 {
     SCtx x{};
     x.g = GridBarrier{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err};
     if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
-    const int64_t stride = (int64_t)gridDim.x * kSThreads;
-    const int64_t tid = (int64_t)blockIdx.x * kSThreads + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t s = tid; s < a.n; s += stride) {
         const double v = a.V[s];
         a.X0[s] = v;
@@ -536,11 +541,11 @@ static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
 {
     auto kern = sparse_solver_kernel<PT, MODE>;
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SThreads<MODE>::v, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {const_cast<SparseArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSThreads), args, 0, st);
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(SThreads<MODE>::v), args, 0, st);
 }
 
 rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
