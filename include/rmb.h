@@ -139,6 +139,15 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
                      const int32_t* pi_or_null, const void* V_in, void* V_out, int32_t* argmin_out,
                      double* resid_out);
 
+/* Policy evaluation: V <- B_{pi,b} V applied until ||V_k - V_{k-1}||_inf <= eps
+ * (MPI's evaluation operator, Eq. 13, run to convergence; its fixed
+ * point is J_pi, Eq. 4, Lemma 4; on return ||V - J_pi||_inf <=
+ * gamma * r_K / (1 - gamma)).  pi: [n] int32 in.  V: [n] float64 in (V0, or 0
+ * with RMB_V0_ZERO) / out.  trace: HOST [max_sweeps] or NULL.
+ * Returns OK, NOT_CONVERGED (V valid), NONFINITE or an error. */
+rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_t seed, double eps, int64_t max_sweeps,
+                            uint32_t flags, void* V, double* trace, rmb_stats* stats);
+
 /* Policy improvement of Algorithm 1 alone: pi <- greedy(V)
  * (lowest index on ties), *changed = #{states whose action changed},
  * *bellman_resid = ||TV - V||_inf.  pi: [n] int32 in/out.  Outputs HOST or NULL. */

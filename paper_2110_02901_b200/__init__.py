@@ -63,6 +63,9 @@ _SIGS = {
     "rmb_apply": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32,
                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                    ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "rmb_policy_value": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                          ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)],
+                         ctypes.c_int),
     "rmb_improve": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                      ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "rmb_partition": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p],
@@ -275,6 +278,19 @@ class Problem:
                             _ptr(V_out), _ptr(argmin), ctypes.byref(r))
         _check(s, (OK, NONFINITE))
         return V_out, argmin, r.value
+
+    def policy_value(self, pi, b=None, seed=0, eps=1e-10, max_sweeps=1_000_000, V=None, v0_zero=True,
+                     identity=False, device="cuda"):
+        """J_pi by B_{pi,b} iteration to ||V_k - V_{k-1}|| <= eps (Eq. 4 / Lemma 4)."""
+        import torch
+        V = torch.zeros(self.n, dtype=torch.float64, device=device) if V is None else V
+        tr = np.zeros(min(max_sweeps, 1 << 20))
+        st = Stats()
+        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+        s = lib().rmb_policy_value(self._h, _ptr(pi), self.n if b is None else b, seed, eps, max_sweeps, flags,
+                                   _ptr(V), _ptr(tr) if max_sweeps <= len(tr) else None, ctypes.byref(st))
+        _check(s, (OK, NOT_CONVERGED, NONFINITE))
+        return Solution(V, pi, tr[: min(st.sweeps, len(tr))], s, st)
 
     def improve(self, V, pi):
         """Policy improvement (Alg. 1): pi in place; returns (pi, ||TV-V||, changed)."""

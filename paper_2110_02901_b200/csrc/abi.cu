@@ -635,6 +635,52 @@ rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellma
     return (rmb_status)r.status;
 }
 
+rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_t seed, double eps, int64_t max_sweeps,
+                            uint32_t flags, void* V, double* trace, rmb_stats* stats)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (b < 1 || b > pr.n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
+    if (!(eps > 0.0) || !std::isfinite(eps)) return fail(RMB_ERR_INVALID_ARG, "eps must be finite and > 0");
+    if (max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "max_sweeps < 1");
+    if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    Staged sg;
+    rmb_status s = stage_in(pr, V, const_cast<int32_t*>(pi), flags & RMB_V0_ZERO, true, sg);
+    if (s != RMB_OK) return s;
+    {
+        std::vector<int32_t> hp((size_t)pr.n);
+        cudaError_t e = cudaMemcpyAsync(hp.data(), sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+        if (e != cudaSuccess) return cuda_fail(e, "read pi");
+        for (int32_t a : hp)
+            if (a < 0 || a >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
+    }
+    if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
+    SolveRequest rq;
+    rq.mode = MODE_POLICY_VALUE;
+    rq.b = b;
+    rq.seed = seed;
+    rq.k0 = 1;
+    rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.eps = eps;
+    rq.max_iter = max_sweeps;
+    rq.V = sg.V;
+    rq.pi = sg.pi;
+    SolveResult r;
+    s = solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
+    if (s != RMB_OK) return s;
+    Staged vo = sg;
+    vo.pi_host = false;  // pi is an input here
+    s = stage_out(pr, V, nullptr, vo);
+    if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.sweeps);
+    if (s != RMB_OK) return s;
+    rmb_status ret = (rmb_status)r.status;
+    if (ret == RMB_ERR_NOT_CONVERGED) g_err = "max_sweeps reached before r_k <= eps";
+    fill_stats(stats, r, ret);
+    return ret;
+}
+
 rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm)
 {
     g_err.clear();

@@ -1126,9 +1126,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
     const int64_t n_pad = (a.n + 3) & ~int64_t(3);
     int32_t* pis = reinterpret_cast<int32_t*>(Vs + n_pad);
     double* Qs = reinterpret_cast<double*>(smem_raw + a.qs_off);
-    const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE ||
+    const bool need_pi = a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE || a.mode == MODE_POLICY_VALUE ||
                          a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
-    const bool shard = a.mode >= MODE_SHARD_MIN;
+    const bool shard = a.mode == MODE_SHARD_MIN || a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
 
     for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
         Vs[vs_index(j, a.vs_half)] = a.V[j];
@@ -1167,10 +1167,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
         last = r.rmax;
         changed = r.changed;
         status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
-    } else if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
-        const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
+    } else if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI ||
+               a.mode == MODE_POLICY_VALUE) {
+        const bool eval = a.mode == MODE_APPLY_PI || a.mode == MODE_POLICY_VALUE;
+        const int64_t iters = (a.mode == MODE_VI || a.mode == MODE_POLICY_VALUE) ? a.max_iter : 1;
         while (it < iters) {
-            PhaseAcc r = a.mode == MODE_APPLY_PI ? run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs)
+            PhaseAcc r = eval ? run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs)
                                                  : run_sweep<PT, VE, false, CTA>(a, x, Vs, pis, k, Qs);
             if (lead && it < a.trace_len) a.trace[it] = r.rmax;
             ++it;
@@ -1179,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
             if (r.bad) { status = RMB_ERR_NONFINITE; break; }
             if (a.eps >= 0.0 && r.rmax <= a.eps) { status = RMB_OK; break; }
         }
-        if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+        if ((a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
     } else if (a.mode == MODE_IMPROVE) {
         PhaseAcc r = run_improve<PT, VE, CTA>(a, x, Vs, pis, Qs);
         last = r.rmax;
@@ -1304,7 +1306,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     const int psz = pr.pdt == RMB_F32 ? 4 : 8;
     int VE = 16 / psz;
     if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
-    const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE ||
+    const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE || rq.mode == MODE_POLICY_VALUE ||
                          rq.mode == MODE_SHARD_EVAL || rq.mode == MODE_SHARD_IMPROVE;
     const int64_t n_pad = (n + 3) & ~int64_t(3);
     const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
@@ -1381,7 +1383,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     bool rows = false;
     switch (rq.mode) {
     case MODE_VI: case MODE_APPLY: case MODE_SHARD_MIN: rows = rp[0].rows; break;
-    case MODE_APPLY_PI: case MODE_SHARD_EVAL: rows = rp[1].rows; break;
+    case MODE_APPLY_PI: case MODE_SHARD_EVAL: case MODE_POLICY_VALUE: rows = rp[1].rows; break;
     case MODE_IMPROVE: case MODE_SHARD_IMPROVE: rows = rp[2].rows; break;
     default: rows = rp[1].rows && rp[2].rows; break;  // MPI
     }

@@ -20,6 +20,7 @@ enum Mode : int {
     MODE_SHARD_MIN = 5,     // B_b backups of this rank's states of one batch -> send list
     MODE_SHARD_EVAL = 6,    // B_{pi,b} backups of this rank's states of one batch -> send list
     MODE_SHARD_IMPROVE = 7, // improvement of this rank's states (pi owned entries, resid, changed)
+    MODE_POLICY_VALUE = 8,  // B_{pi,b} applied until ||V_k - V_{k-1}|| <= eps (policy evaluation)
 };
 
 // Device-side result block written by the solver kernels (long long[8]).

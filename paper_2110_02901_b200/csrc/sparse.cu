@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
         const double v = a.V[s];
         a.X0[s] = v;
         a.X1[s] = v;
-        if (a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE) a.pw0[s] = a.pi[s];
+        if (a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE || a.mode == MODE_POLICY_VALUE)
+            a.pw0[s] = a.pi[s];
     }
     if (!a.identity && a.mode != MODE_IMPROVE) {
         Permutation pm;
@@ -465,10 +466,12 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
     long long changed = 0;
     double last = 0.0;
     int pcur = 0;  // which pw buffer holds the current policy
-    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) {
-        const int64_t iters = a.mode == MODE_VI ? a.max_iter : 1;
+    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI ||
+               a.mode == MODE_POLICY_VALUE) {
+        const bool eval = a.mode == MODE_APPLY_PI || a.mode == MODE_POLICY_VALUE;
+        const int64_t iters = (a.mode == MODE_VI || a.mode == MODE_POLICY_VALUE) ? a.max_iter : 1;
         while (it < iters) {
-            SweepResult r = a.mode == MODE_APPLY_PI ? run_sweep<PT, MODE, true>(a, x, k, a.pw0)
+            SweepResult r = eval ? run_sweep<PT, MODE, true>(a, x, k, a.pw0)
                                                     : run_sweep<PT, MODE, false>(a, x, k, nullptr);
             if (lead && it < a.trace_len) a.trace[it] = r.r;
             ++it;
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
             if (r.bad) { status = RMB_ERR_NONFINITE; break; }
             if (a.eps >= 0.0 && r.r <= a.eps) { status = RMB_OK; break; }
         }
-        if (a.mode != MODE_VI && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+        if ((a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
     } else if (a.mode == MODE_IMPROVE) {
         SweepResult r = run_improve<PT, MODE>(a, x, imp++, a.pw0, a.pw1, true);
         pcur = 1;

@@ -275,3 +275,22 @@ def test_config2_full_size_sampled(b):
         assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
         assert arg[s] == a
     assert r == pytest.approx(np.abs(V1 - V0).max(), abs=0)
+
+
+@pytest.mark.parametrize("b", [1, 50, 400])
+def test_policy_value_matches_linear_solve(b):
+    """rmb_policy_value: B_{pi,b} iterated to eps reaches J_pi (Eq. 4, Lemma 4),
+    the oracle's dense linear solve, within the certificate gamma r/(1-gamma)."""
+    n, A, gamma = 400, 6, 0.95
+    m, prob, P, c = make(n, A, seed=12, dtype=np.float64, gamma=gamma)
+    pi = np.random.default_rng(3).integers(0, A, n).astype(np.int32)
+    sol = prob.policy_value(tdev(pi), b=b, seed=1, eps=1e-11)
+    assert sol.status == rmb.OK
+    J = oracle.policy_value(m, pi)
+    r = sol.stats.final_residual
+    assert np.abs(sol.V.cpu().numpy() - J).max() <= gamma * r / (1 - gamma) + 1e-9
+    # and the sweep-by-sweep trajectory is the oracle's B_{pi,b} iteration
+    V = np.zeros(n)
+    for k in range(1, 6):
+        V, _, ro = oracle.sweep(m, V, b, oracle.partition(n, 1, k), pi)
+        assert abs(sol.trace[k - 1] - ro) <= 1e-11 * max(1.0, np.abs(V).max())

@@ -186,3 +186,16 @@ def test_config4_full_size_sampled_eval():
         hrp, hcol, hval, hc = gen.grid(N, rows=(s, s + 1))
         q, _ = oracle.backup_csr_row(n, hrp, hcol, hval, hc[0], gamma, Vint, pi_a=int(pi[s]))
         assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
+
+
+def test_policy_value_on_grid():
+    m, prob = grid_instance(16, dtype=np.float64)
+    pi = np.random.default_rng(0).integers(0, 4, m.n).astype(np.int32)
+    sol = prob.policy_value(tdev(pi), b=37, seed=2, eps=1e-11)
+    assert sol.status == rmb.OK
+    J = oracle.policy_value(m, pi)
+    assert np.abs(sol.V.cpu().numpy() - J).max() <= 0.95 * sol.stats.final_residual / 0.05 + 1e-9
+    V = np.zeros(m.n)
+    for k in range(1, 6):
+        V, _, ro = oracle.sweep(m, V, 37, oracle.partition(m.n, 2, k), pi)
+        assert abs(sol.trace[k - 1] - ro) <= 1e-11 * max(1.0, np.abs(V).max())
