@@ -74,6 +74,9 @@ typedef struct {
 #define RMB_V0_ZERO 0x2u        /* ignore V's content on entry and start from V0 = 0        */
 #define RMB_PI_GIVEN 0x4u       /* rmb_mpi: pi holds the initial policy (else pi_0 = greedy(V0))     */
 #define RMB_VALIDATE 0x8u       /* rmb_create_*: check the MDP on device (RMB_ERR_INVALID_MDP)       */
+#define RMB_DENSE_NO_TMA 0x10u  /* rmb_create_dense: stream P rows with per-warp register loads instead
+                                   of the default TMA (cp.async.bulk) shared-memory ring; results agree
+                                   to fp64 rounding (A/B measurement and cross-path tests)            */
 
 /* Create a handle over a DENSE MDP.
  *   P: [n][A][n] row-major, P[(s*A + a)*n + j] = p(j | s, a), dtype desc->p_dtype.

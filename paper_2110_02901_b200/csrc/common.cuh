@@ -75,12 +75,26 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// CTA-level barrier of the first NT threads (named barrier 1).  With NT ==
+// blockDim.x it is __syncthreads(); kernels with a producer warp outside the
+// first NT threads (dense TMA path) keep that warp out of every CTA barrier.
+template <int NT>
+__device__ __forceinline__ void bar_sync_n()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+template <int NT = 0>
 __device__ __forceinline__ void grid_sync(GridBarrier& g)
 {
+    auto csync = [] {
+        if constexpr (NT == 0) __syncthreads();
+        else bar_sync_n<NT>();
+    };
 #if RMB_BARRIER_VARIANT == 1
     // arrive with a fire-and-forget release reduction, then poll the arrival
     // counter itself (no separate release flag round trip)
-    __syncthreads();
+    csync();
     if (threadIdx.x == 0) {
         g.epoch += 1;
         const unsigned long long target = g.epoch * g.nblocks;
@@ -99,10 +113,10 @@ __device__ __forceinline__ void grid_sync(GridBarrier& g)
             }
         }
     }
-    __syncthreads();
+    csync();
     return;
 #endif
-    __syncthreads();
+    csync();
     if (threadIdx.x == 0) {
         g.epoch += 1;
         const unsigned long long target = g.epoch * g.nblocks;
@@ -126,7 +140,7 @@ __device__ __forceinline__ void grid_sync(GridBarrier& g)
             }
         }
     }
-    __syncthreads();
+    csync();
 }
 
 // ------------------------------------------------------------- reductions

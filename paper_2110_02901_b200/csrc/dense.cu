@@ -45,8 +45,13 @@ namespace rmb {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kAG = 4;                     // actions per compute item (min modes)
-constexpr int kPathWarp = 0, kPathCta = 1, kPathRows = 2;  // compute path of a kernel instantiation
+constexpr int kPathWarp = 0, kPathCta = 1, kPathRows = 2, kPathTma = 3;  // compute path of a kernel instantiation
 constexpr int64_t kRedundantMax = 8192;    // doubles of batch partials reduced by every CTA
+
+// CTA barrier of the 512 compute threads (named barrier 1).  Identical to
+// __syncthreads() for the 512-thread paths; the TMA path adds a producer warp
+// (threads 512..543) that never joins it.
+__device__ __forceinline__ void csync() { bar_sync_n<kThreads>(); }
 
 struct Plan {
     int Lc;         // chunk length (elements)
@@ -55,6 +60,8 @@ struct Plan {
     int cta;        // 1: CTA-cooperative tile pipeline, 0: warp-owned items
     int rows;       // 1: CTA-per-state rows mode (whole rows, C = 1, ng = A)
     int ng;         // action rows per warp item in min modes (4, or 1 for short-tail batches)
+    int raw;        // 1 (TMA path): items store raw row dot products part[(i*Ae + a)*C + ch]; costs,
+                    //   chunk sums and min/argmin are all done by the combine (S-mode, even at C == 1)
 };
 
 struct DenseArgs {
@@ -104,6 +111,13 @@ struct DenseArgs {
     int64_t qs_cap;      // doubles of smem scratch for S-mode reductions
     int64_t qs_off;      // byte offset of that scratch in dynamic smem
     long long* prof;     // [0] compute ns, [1] barrier ns, [2] combine ns, [3] barriers (CTA 0)
+    int64_t tma_off;     // TMA path: byte offset of the stage ring in dynamic smem
+    int tma_nst;         //           ring stages
+    int tma_gmin;        //           minimum items per dynamic grab (experiments: RMB_TMA_G)
+    int tma_piece;       //           columns per stage and row slot
+    int tma_static;      //           batches with <= tma_static * grid items are dealt statically
+    int tma_slot;        //           bytes per ring slot (piece bytes rounded up to 128)
+    int tma_hint;        //           L2 evict-first hint on the bulk copies (RMB_TMA_HINT=0 disables)
 };
 
 // ---------------------------------------------------------------- loads
@@ -292,6 +306,72 @@ __device__ __forceinline__ void finish_state_warp(const DenseArgs& a, const doub
 //   C == 1, min : part[2(i*NAG+ag)+{0,1}] = (min Q over the group, argmin)   (2*NAG)
 //   C >  1, EVAL: part[i*C + ch]               (C)
 //   C >  1, min : part[(i*A + a)*C + ch]       (A*C)
+// Item epilogue (warp-wide, acc[] identical in all lanes): write the item's
+// result into the partial buffer and, in last-arriver mode, finish the state
+// once all its items are in (shared by the warp and TMA compute paths).
+template <typename PT, bool EVAL, int NG>
+__device__ __forceinline__ void item_epilogue(const DenseArgs& a, const Plan& pl, double* part, int64_t i, int64_t s,
+                                              int a0, int na, int ch, const double (&acc)[NG])
+{
+    const int lane = threadIdx.x & 31;
+    const int C = pl.C;
+    const int NAG = EVAL ? 1 : (a.A + NG - 1) / NG;
+    const int64_t per_state = (int64_t)NAG * C;
+    const int ag = a0 / NG;
+    if (C == 1) {
+        if (lane == 0) {
+            if (EVAL) {
+                part[i] = load_cost<PT>(a, s * a.A + a0) + a.gamma * acc[0];
+            } else {
+                double best = 0.0;
+                int barg = a0;
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    if (g < na) {
+                        const double Q = load_cost<PT>(a, s * a.A + a0 + g) + a.gamma * acc[g];
+                        if (g == 0 || Q < best) best = Q, barg = a0 + g;
+                    }
+                }
+                part[2 * (i * NAG + ag)] = best;
+                part[2 * (i * NAG + ag) + 1] = (double)barg;
+            }
+        }
+    } else if (EVAL) {
+        if (lane == 0) part[i * C + ch] = acc[0];
+    } else {
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+            if (lane == g && g < na) part[(i * a.A + a0 + g) * C + ch] = acc[g];
+    }
+    if (!pl.redundant) {
+        // last arriver of state i finishes its backup into the list
+        if (per_state == 1) {
+            if (lane == 0) {
+                if (EVAL) {
+                    a.lval[i] = part[i];
+                    a.larg[i] = a0;
+                } else {
+                    a.lval[i] = part[2 * i];
+                    a.larg[i] = (int)part[2 * i + 1];
+                }
+            }
+        } else {
+            __syncwarp();
+            unsigned int prev = 0;
+            if (lane == 0) {
+                __threadfence();
+                prev = atomicAdd(a.scnt + i, 1u);
+            }
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == (unsigned int)(per_state - 1)) {
+                __threadfence();
+                finish_state_warp<PT, EVAL>(a, part, C, i, s, a0, NG);
+                if (lane == 0) a.scnt[i] = 0u;  // rearmed for the next batch (ordered by its barrier)
+            }
+        }
+    }
+}
+
 // Tail prefetch: a warp that finds no more items in this batch asks a second
 // counter for items of the NEXT batch (same decomposition, grabbed in the same
 // order there) and issues one cp.async.bulk.prefetch.L2 per row chunk, so the
@@ -364,58 +444,7 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
         const int64_t s_next = state_of(it_next);
 #pragma unroll
         for (int g = 0; g < NG; ++g) acc[g] = warp_sum(acc[g]);
-        if (C == 1) {
-            if (lane == 0) {
-                if (EVAL) {
-                    part[i] = load_cost<PT>(a, s * a.A + a0) + a.gamma * acc[0];
-                } else {
-                    double best = 0.0;
-                    int barg = a0;
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        if (g < na) {
-                            const double Q = load_cost<PT>(a, s * a.A + a0 + g) + a.gamma * acc[g];
-                            if (g == 0 || Q < best) best = Q, barg = a0 + g;
-                        }
-                    }
-                    part[2 * (i * NAG + ag)] = best;
-                    part[2 * (i * NAG + ag) + 1] = (double)barg;
-                }
-            }
-        } else if (EVAL) {
-            if (lane == 0) part[i * C + ch] = acc[0];
-        } else {
-#pragma unroll
-            for (int g = 0; g < NG; ++g)
-                if (lane == g && g < na) part[(i * a.A + a0 + g) * C + ch] = acc[g];
-        }
-        if (!pl.redundant) {
-            // last arriver of state i finishes its backup into the list
-            if (per_state == 1) {
-                if (lane == 0) {
-                    if (EVAL) {
-                        a.lval[i] = part[i];
-                        a.larg[i] = a0;
-                    } else {
-                        a.lval[i] = part[2 * i];
-                        a.larg[i] = (int)part[2 * i + 1];
-                    }
-                }
-            } else {
-                __syncwarp();
-                unsigned int prev = 0;
-                if (lane == 0) {
-                    __threadfence();
-                    prev = atomicAdd(a.scnt + i, 1u);
-                }
-                prev = __shfl_sync(0xffffffffu, prev, 0);
-                if (prev == (unsigned int)(per_state - 1)) {
-                    __threadfence();
-                    finish_state_warp<PT, EVAL>(a, part, C, i, s, a0, NG);
-                    if (lane == 0) a.scnt[i] = 0u;  // rearmed for the next batch (ordered by its barrier)
-                }
-            }
-        }
+        item_epilogue<PT, EVAL, NG>(a, pl, part, i, s, a0, na, ch, acc);
         it = it_next;
         s_cur = s_next;
     }
@@ -506,13 +535,13 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
     const PT* P = static_cast<const PT*>(a.P);
     const int64_t rowvec = a.n / VE;  // row stride in vectors
 
-    __syncthreads();  // the previous phase is done with tr
+    csync();  // the previous phase is done with tr
     if (tid < kRing) {
         tr.arrive[tid] = 0;
         tr.ready[tid] = -1;  // stale tile numbers of the previous phase must not match
         tr.allowed[tid] = tid;
     }
-    __syncthreads();
+    csync();
 
     if (warp == kCW) {
         // ------------------------------------------------ producer warp
@@ -551,7 +580,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
                 if (it >= items) break;
             }
         }
-        __syncthreads();
+        csync();
         return;
     }
 
@@ -717,7 +746,7 @@ __device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const in
             if (--cslots == 0) finalize();
         }
     }
-    __syncthreads();  // pairs with the producer's; every epilogue is complete
+    csync();  // pairs with the producer's; every epilogue is complete
 }
 
 // ------------------------------------------------ CTA-per-state rows mode
@@ -753,18 +782,18 @@ __device__ void compute_phase_rows(const DenseArgs& a, const double* Vs, const i
     const int gst = max(1, kWarps / Ae);  // states per item
     const int64_t items = (cnt + gst - 1) / gst;
     const PT* P = static_cast<const PT*>(a.P);
-    __syncthreads();  // the previous phase is done with rr
+    csync();  // the previous phase is done with rr
     if (threadIdx.x < kRR) {
         rr.arrive[threadIdx.x] = 0;
         rr.ready[threadIdx.x] = -1;
     }
     if (threadIdx.x == 0) r_base = (long long)atomicAdd(ctr, (unsigned int)kRR);
-    __syncthreads();
+    csync();
     if (threadIdx.x < kRR) {
         rr.it[threadIdx.x] = r_base + threadIdx.x;
         rr.ready[threadIdx.x] = threadIdx.x;
     }
-    __syncthreads();
+    csync();
     volatile RowsRing& vr = rr;
     // a grab issued by this warp's last epilogue, published after its next
     // row so that the atomic's latency hides behind the streaming
@@ -849,7 +878,447 @@ __device__ void compute_phase_rows(const DenseArgs& a, const double* Vs, const i
         pending = __shfl_sync(0xffffffffu, pending ? 1 : 0, 0) != 0;
         __syncwarp();
     }
-    __syncthreads();
+    csync();
+}
+
+// ------------------------------------------------- TMA ring path (default)
+// The compute phase as a bulk-copy pipeline.  Per SM, a PRODUCER warp (threads
+// 512..543, one elected lane) takes items (state, action group, column chunk)
+// from the batch's global work counter and streams each item's P rows into a
+// shared-memory ring of 16 KB stages with cp.async.bulk (TMA engine, L2
+// evict-first policy: P is read once per sweep), completion signalled on the
+// stage's `full` mbarrier.  The 16 compute warps read a stage from shared
+// memory (thread t: 16-byte vectors t and t + 512 of the stage), accumulate
+// fp64 dot products against the shared-memory V across the item's stages and
+// release the stage on its `empty` mbarrier.  At an item's last stage each
+// warp reduces its sums into a per-stage slot; the last arriving warp adds the
+// 32 slots in a fixed (half, warp) order — reproducible — and runs the item
+// epilogue (the same as the warp path's).
+//
+// Why: the bytes in flight per SM are set by the ring (~100 KB), not by
+// registers, and P does not depend on V — so the producer RUNS AHEAD into the
+// next batch while the compute warps are still in this batch's tail, grid
+// barrier and combine ("the batch is written back before the next batch
+// starts" constrains the V reads, not the P loads).  The ring is full when
+// the compute warps start the next batch.  Run-ahead is bounded to one batch,
+// and fenced where a batch's rows depend on the previous batch's outcome (an
+// evaluation sweep right after a policy improvement reads rows pi(s)).
+// Work counters: a producer leaves a batch with exactly one failing grab; the
+// one that draws items + grid - 1 (the last) re-arms the counter, before its
+// end-of-batch marker, hence before that batch's grid barrier (2 counters).
+#ifndef RMB_TMA_STAGE
+#define RMB_TMA_STAGE 32768
+#endif
+constexpr int kTmaStage = RMB_TMA_STAGE;   // bytes per ring stage
+constexpr int kTmaMaxStages = 24;
+constexpr int kTmaVecs = kTmaStage / 16;   // 16-byte vectors per stage
+constexpr int kTmaThreads = kThreads + kWarp;
+
+struct TmaMeta {         // one per stage, written by the producer before its arrive
+    long long i;         // batch position (END marker: batch sequence number)
+    int e;               // first column of this stage's window
+    int nvec;            // 16-byte vectors per row in this stage
+    int a0;              // rows in the item (na)
+    int na;              // action group index ag
+    int ch;              // chunk of the group range
+    int flags;           // 1: last stage of the item, 2: end of batch
+};
+constexpr int kTmaPerStageX = (int)sizeof(TmaMeta) + 16 + kWarps * kAG * 8 + 4;  // + the slot itself
+
+struct TmaSmem {
+    unsigned char* ring;
+    TmaMeta* meta;
+    unsigned long long* full;
+    unsigned long long* empty;
+    double* red;         // [stage][warp][2]
+    int* redcnt;         // [stage]
+    long long* ctl;      // [0] consumers' batch sequence number (-1 before the first), [1] stop flag
+    int nst;
+};
+
+__device__ __forceinline__ TmaSmem tma_smem(unsigned char* base, const DenseArgs& a)
+{
+    TmaSmem m;
+    m.nst = a.tma_nst;
+    m.ring = base + a.tma_off;
+    m.meta = reinterpret_cast<TmaMeta*>(m.ring + (size_t)m.nst * a.tma_slot);
+    m.full = reinterpret_cast<unsigned long long*>(m.meta + m.nst);
+    m.empty = m.full + m.nst;
+    m.red = reinterpret_cast<double*>(m.empty + m.nst);
+    m.redcnt = reinterpret_cast<int*>(m.red + (size_t)m.nst * kWarps * kAG);
+    m.ctl = reinterpret_cast<long long*>(m.redcnt + ((m.nst + 1) & ~1));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned tx)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Hang guard for ring waits (a broken pipeline traps instead of wedging the GPU).
+struct SpinGuard {
+    unsigned spins = 0;
+    unsigned long long t0 = 0;
+    __device__ __forceinline__ void tick()
+    {
+        if (++spins == 8192u) {
+            spins = 0;
+            const unsigned long long t = globaltimer_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 20ull * 1000000000ull) __trap();
+        }
+    }
+};
+
+#ifndef RMB_TMA_EXP
+#define RMB_TMA_EXP 0
+#endif
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                         uint64_t pol)
+{
+#if RMB_TMA_EXP == 1
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+    return;
+#endif
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ long long ld_acquire_cta(const long long* p)
+{
+    long long v;
+    asm volatile("ld.acquire.cta.shared.b64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(long long* p, long long v)
+{
+    asm volatile("st.release.cta.shared.b64 [%0], %1;" ::"r"(smem_addr(p)), "l"(v) : "memory");
+}
+
+// The batch sequence of a launch, as the compute threads will run it (one
+// entry per run_batch call), assuming no early stop.  Kinds as run_batch KIND.
+struct TmaBatch {
+    int kind;
+    const uint32_t* perm;
+    int64_t lo, cnt;
+};
+
+__device__ __forceinline__ bool tma_segment(const DenseArgs& a, int64_t sg, int& kind, int64_t& k)
+{
+    k = a.k0;
+    switch (a.mode) {
+    case MODE_VI: kind = 0; k = a.k0 + sg; return sg < a.max_iter;
+    case MODE_POLICY_VALUE: kind = 1; k = a.k0 + sg; return sg < a.max_iter;
+    case MODE_APPLY: kind = 0; return sg < 1;
+    case MODE_APPLY_PI: kind = 1; return sg < 1;
+    case MODE_IMPROVE: case MODE_SHARD_IMPROVE: kind = 2; return sg < 1;
+    case MODE_SHARD_MIN: kind = 3; return sg < 1;
+    case MODE_SHARD_EVAL: kind = 4; return sg < 1;
+    default: {  // MODE_MPI
+        int64_t q = sg;
+        if (!a.pi_given) {
+            if (q == 0) { kind = 2; return true; }
+            q -= 1;
+        }
+        const int64_t per = (int64_t)a.msweeps + 1;
+        const int64_t outer = q / per, r = q - outer * per;
+        if (outer >= a.max_iter) return false;
+        if (r < a.msweeps) {
+            kind = 1;
+            k = a.k0 + outer * a.msweeps + r;
+        } else {
+            kind = 2;
+        }
+        return true;
+    }
+    }
+}
+
+struct TmaSched {
+    int64_t sg = 0, lo = -1, k = 0;
+    int kind = -1;
+    __device__ bool next(const DenseArgs& a, TmaBatch& bt)
+    {
+        while (true) {
+            if (lo >= 0) {
+                const int64_t end = kind == 2 ? a.row1 : (kind >= 3 ? 1 : a.n);
+                if (lo < end) break;
+                ++sg;
+            }
+            if (!tma_segment(a, sg, kind, k)) return false;
+            lo = kind == 2 ? a.row0 : 0;
+        }
+        bt.kind = kind;
+        if (kind >= 3) {
+            bt.perm = a.olist;
+            bt.lo = 0;
+            bt.cnt = *(volatile const int*)a.ocount;
+            lo = 1;
+        } else if (kind == 2) {
+            bt.perm = nullptr;
+            bt.lo = lo;
+            bt.cnt = min(a.imp_sub, a.row1 - lo);
+            lo += a.imp_sub;
+        } else {
+            bt.perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
+            bt.lo = lo;
+            bt.cnt = min(a.b, a.n - lo);
+            lo += a.b;
+        }
+        return true;
+    }
+};
+
+// Producer: one lane.  q = batch sequence number (== the compute threads' x.phase).
+// An ITEM is (state s, action group ag = rows a0 .. a0+na-1, column chunk ch)
+// — or (s, row pi(s), ch) in B_{pi,b} batches.  It streams as stages of the
+// same column window [col, col + w) of its na rows: na bulk copies per stage
+// into na row slots of the ring slot, so a compute thread reads each V vector
+// once for all the rows of the group.
+template <typename PT>
+__device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSmem& m)
+{
+    uint64_t pol;
+    if (a.tma_hint)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    const PT* P = static_cast<const PT*>(a.P);
+    constexpr int VB = 16 / (int)sizeof(PT);  // elements per 16-byte vector
+    const int n = (int)a.n;
+    int st = 0;
+    unsigned ph = 0;
+    long long issued = 0;
+    bool stop = false;
+    auto stopped = [&]() -> bool { return ld_acquire_cta(m.ctl + 1) != 0; };
+    auto acquire = [&]() -> bool {
+        SpinGuard sg;
+        while (!mbar_try(m.empty + st, ph ^ 1u)) {
+            if (stopped()) return false;
+            sg.tick();
+        }
+        return true;
+    };
+    auto advance = [&]() {
+        ++issued;
+        if (++st == m.nst) st = 0, ph ^= 1u;
+    };
+    TmaSched sc;
+    TmaBatch bt;
+    int prev_kind = -1;
+    const unsigned G = gridDim.x;
+    for (long long q = 0; !stop && sc.next(a, bt); ++q) {
+        // run-ahead bound: one batch past the compute threads; fenced batches
+        // (the first, and B_{pi,b} batches right after an improvement) wait
+        // until the compute threads are in them
+        const bool fence = q == 0 || ((bt.kind == 1 || bt.kind == 4) && prev_kind == 2) ||
+                           (bt.perm != nullptr && bt.kind <= 1 && bt.lo == 0 && a.b >= a.n);
+        {
+            SpinGuard sg;
+            while (true) {
+                const long long cq = ld_acquire_cta(m.ctl);
+                if (q <= cq + (fence ? 0 : 1)) break;
+                if (stopped()) { stop = true; break; }
+                sg.tick();
+                __nanosleep(64);
+            }
+        }
+        if (stop) break;
+        prev_kind = bt.kind;
+        const bool eval = bt.kind == 1 || bt.kind == 4;
+        const Plan& pl = a.plan[eval ? 1 : (bt.kind == 2 ? 2 : 0)];
+        const int NG = eval ? 1 : pl.ng;
+        const int rslot = kTmaStage / NG;                     // bytes per row slot
+        const int w = rslot / (int)sizeof(PT);                // columns per stage
+        const unsigned NAG = eval ? 1u : (unsigned)((a.A + NG - 1) / NG);
+        const unsigned C = (unsigned)pl.C;
+        const unsigned per_state = NAG * C;
+        const unsigned items = (unsigned)bt.cnt * per_state;
+        // small batches: a static deal (CTA x: items x, x + grid, ...), no
+        // counter; else grabs of g items (>= ~4 stages) from the batch counter
+        const bool stat = items <= (unsigned)a.tma_static * G;
+        const unsigned spi = max(1u, (unsigned)(n / C / w));  // ~stages per item
+        unsigned g = 1;
+        if (!stat) g = max((unsigned)a.tma_gmin, min((4u + spi - 1) / spi, max(1u, items / (4u * G))));
+        unsigned int* ctr = a.wctr + (q & 1);
+        // failing grabs return multiples of g from fail0 on; each producer does
+        // exactly one, and the last of them re-arms the counter
+        const unsigned fail0 = (items + g - 1) / g * g;
+        unsigned r = stat ? blockIdx.x : atomicAdd(ctr, g);
+        unsigned r_end = stat ? r + 1 : r + g;
+        const unsigned nvecs = (unsigned)(n / VB);
+        while (true) {
+            if (r >= items) {
+                if (!stat && r == fail0 + (G - 1) * g) atomicExch(ctr, 0u);
+                break;
+            }
+            // next grab, in flight while this one streams
+            const bool local = !stat && r + 1 < r_end && r + 1 < items;
+            const unsigned rn = stat ? r + G : (local ? r + 1 : atomicAdd(ctr, g));
+            const unsigned i = r / per_state;
+            const unsigned rr = r - i * per_state;
+            const unsigned ag = rr / C;
+            const unsigned ch = rr - ag * C;
+            const int64_t s = bt.perm ? (int64_t)__ldcg(bt.perm + bt.lo + i) : bt.lo + i;
+            const int a0 = eval ? pis[s] : (int)ag * NG;
+            const int na = eval ? 1 : min(NG, a.A - a0);
+            // columns [c0, c1) (vector aligned) of the group's rows
+            const int c1 = (int)((uint64_t)nvecs * (ch + 1) / C) * VB;
+            const PT* rowp = P + ((int64_t)s * a.A + a0) * n;
+            for (int col = (int)((uint64_t)nvecs * ch / C) * VB; col < c1 && !stop; col += w) {
+                const int len = min(w, c1 - col);
+                if (!acquire()) { stop = true; break; }
+                TmaMeta& md = m.meta[st];
+                md.i = i;
+                md.e = col;
+                md.nvec = len / VB;
+                md.a0 = na;
+                md.na = (int)ag;
+                md.ch = (int)ch;
+                md.flags = col + len >= c1 ? 1 : 0;
+                const unsigned bytes = (unsigned)(len * (int)sizeof(PT));
+                mbar_arrive_tx(m.full + st, bytes * (unsigned)na);
+                unsigned char* dst = m.ring + (size_t)st * kTmaStage;
+                const PT* src = rowp + col;
+                for (int gg = 0; gg < na; ++gg) {
+                    bulk_g2s(dst, src, bytes, m.full + st, pol);
+                    dst += rslot;
+                    src += n;
+                }
+                advance();
+            }
+            if (stop) break;
+            if (!stat && !local) r_end = rn + g;
+            r = rn;
+        }
+        if (stop) break;
+        if (!acquire()) break;
+        m.meta[st].i = q;
+        m.meta[st].flags = 2;
+        mbar_arrive(m.full + st);
+        advance();
+    }
+    // drain: every issued bulk copy must land before the CTA may exit
+    const long long last = issued < m.nst ? issued : m.nst;
+    int s2 = st;
+    unsigned p2 = ph;
+    for (long long d = 0; d < last; ++d) {
+        if (s2 == 0) s2 = m.nst, p2 ^= 1u;
+        --s2;
+        SpinGuard sg;
+        while (!mbar_try(m.full + s2, p2)) sg.tick();
+    }
+}
+
+// Compute threads: consume this batch's stages up to its end marker.  A stage
+// holds the column window [col, col + 4*nvec) of the item's na rows (row g at
+// slot offset g * kTmaStage/NG); thread t takes column vectors t, t + 512, ...
+// and, per vector, reads V once and dots it with every row.  Raw partials:
+//   part[((i*NAG + ag)*C + ch)*NG + g] = sum over the item of P(row a0+g) . V
+template <typename PT, bool EVAL>
+__device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Plan& pl, double* part,
+                                  const TmaSmem& m, int& st, unsigned& ph)
+{
+    constexpr int E = 16 / (int)sizeof(PT);
+    constexpr int NG = EVAL ? 1 : kAG;
+    constexpr int RV = kTmaStage / NG / 16;  // vectors per row slot
+    using VT = typename Vec<PT, E>::T;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int NAG = EVAL ? 1 : (a.A + NG - 1) / NG;
+    const int C = pl.C;
+    const int64_t half = a.vs_half;
+    double acc[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) acc[g] = 0.0;
+    while (true) {
+        {
+            SpinGuard sg;
+            while (!mbar_try(m.full + st, ph)) sg.tick();
+        }
+        const TmaMeta md = m.meta[st];
+        if (md.flags & 2) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(m.empty + st);
+            if (++st == m.nst) st = 0, ph ^= 1u;
+            break;
+        }
+        const VT* stg = reinterpret_cast<const VT*>(m.ring + (size_t)st * kTmaStage);
+        if (RMB_TMA_EXP != 2) {
+#pragma unroll
+            for (int f0 = 0; f0 < RV; f0 += kThreads) {
+                const int f = f0 + t;
+                if (f < md.nvec) {
+                    double vs[E];
+                    load_v<E>(Vs, md.e + f * E, vs, half);
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        if (g < md.a0) {
+                            const VT x = stg[g * RV + f];
+                            double p[E];
+                            Vec<PT, E>::get(x, p);
+#pragma unroll
+                            for (int k = 0; k < E; ++k) acc[g] = fma(p[k], vs[k], acc[g]);
+                        }
+                    }
+                }
+            }
+        }
+        if (md.flags & 1) {
+            double* red = m.red + (size_t)st * kWarps * kAG;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const double w = warp_sum(acc[g]);
+                acc[g] = 0.0;
+                if (lane == 0) red[warp * kAG + g] = w;
+            }
+            // arrival count with acq_rel semantics at CTA scope
+            int prev = 0;
+            if (lane == 0) {
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(prev)
+                             : "r"(smem_addr(m.redcnt + st))
+                             : "memory");
+            }
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev == kWarps - 1) {
+                // lane g < NG sums row g over the warps in order; plain stores,
+                // no global round trip on the streaming warps (costs, chunk
+                // sums and the min are the combine's); rows >= na store 0
+                if (lane < NG) {
+                    double dsum = 0.0;
+                    for (int w = 0; w < kWarps; ++w) dsum += red[w * kAG + lane];
+                    part[(((int64_t)md.i * NAG + md.na) * C + md.ch) * NG + lane] = dsum;
+                }
+                if (lane == 0) m.redcnt[st] = 0;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(m.empty + st);
+        if (++st == m.nst) st = 0, ph ^= 1u;
+    }
 }
 
 struct PhaseAcc {
@@ -887,8 +1356,16 @@ __device__ __forceinline__ void reduce_state_F(const DenseArgs& a, const double*
 template <typename PT, bool EVAL, typename Sink>
 __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double* part, int C, const uint32_t* perm,
                                                 int64_t lo, int64_t cnt, int64_t first, int64_t step,
-                                                const int32_t* pis, double* Qs, Sink&& sink)
+                                                const int32_t* pis, double* Qs, Sink&& sink, bool raw = false)
 {
+    // partial layout: (i, a, ch) -> (i*A + a)*C + ch, stride 1 over ch; raw
+    // (TMA path, min modes): ((i*NAG + a/kAG)*C + ch)*kAG + a%kAG, stride kAG
+    const int NAGr = (a.A + kAG - 1) / kAG;
+    auto pbase = [&](int64_t i, int act) -> int64_t {
+        if (EVAL) return i * C;
+        return raw ? ((i * NAGr + act / kAG) * C) * kAG + act % kAG : (i * a.A + act) * C;
+    };
+    const int pstr = (raw && !EVAL) ? kAG : 1;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int Ae = EVAL ? 1 : a.A;
@@ -904,9 +1381,9 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
                 const int64_t i = first + (k0 + kk) * step;
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
                 const int act = EVAL ? pis[s] : ai;
-                const double* pp = part + (EVAL ? i : i * a.A + act) * C;
+                const double* pp = part + pbase(i, act);
                 double sum = 0.0;
-                for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + ch);
+                for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + (int64_t)ch * pstr);
                 Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
             }
         } else {       // few long sums: a warp per (state, action)
@@ -916,14 +1393,14 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
                 const int64_t i = first + (k0 + kk) * step;
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
                 const int act = EVAL ? pis[s] : ai;
-                const double* pp = part + (EVAL ? i : i * a.A + act) * C;
+                const double* pp = part + pbase(i, act);
                 double sum = 0.0;
-                for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + ch);
+                for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + (int64_t)ch * pstr);
                 sum = warp_sum(sum);
                 if (lane == 0) Qs[q] = load_cost<PT>(a, s * a.A + act) + a.gamma * sum;
             }
         }
-        __syncthreads();
+        csync();
         for (int64_t kk = threadIdx.x; kk < m; kk += kThreads) {
             const int64_t i = first + (k0 + kk) * step;
             const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
@@ -936,7 +1413,7 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
                 }
             sink(i, s, best, barg);
         }
-        __syncthreads();
+        csync();
     }
 }
 
@@ -981,6 +1458,9 @@ struct Ctx {
     int64_t batches;
     unsigned long long t_mark;
     long long t_comp, t_bar, t_comb, n_bar;
+    TmaSmem tm;       // TMA path: ring and the compute threads' position in it
+    int tst;
+    unsigned tph;
 };
 
 __device__ __forceinline__ void prof_mark(Ctx& x, long long* slot)
@@ -995,7 +1475,7 @@ __device__ __forceinline__ void prof_mark(Ctx& x, long long* slot)
 __device__ __forceinline__ void timed_sync(Ctx& x)
 {
     prof_mark(x, &x.t_comp);
-    grid_sync(x.g);
+    grid_sync<kThreads>(x.g);
     prof_mark(x, &x.t_bar);
     x.n_bar++;
 }
@@ -1008,15 +1488,21 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
 {
     constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
-    // the other parity's work counter was last used before the previous
-    // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if constexpr (CTA == kPathTma) {
+        // the producer may now run one batch ahead of this one (counters are
+        // re-armed by the producers themselves)
+        if (threadIdx.x == 0) st_release_cta(x.tm.ctl, x.phase);
+    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // the other parity's work counter was last used before the previous
+        // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
         atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
         atomicExch(a.pctr + ((x.phase + 1) & 1), 0u);
     }
     // one compute path per kernel instantiation (register allocation is per
     // kernel: mixing paths made every path spill)
-    if constexpr (CTA == kPathRows)
+    if constexpr (CTA == kPathTma)
+        compute_phase_tma<PT, EVAL>(a, Vs, pl, part, x.tm, x.tst, x.tph);
+    else if constexpr (CTA == kPathRows)
         compute_phase_rows<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     else if constexpr (CTA == kPathCta)
         compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
@@ -1032,9 +1518,24 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
             dst[p] = (uint32_t)pm((uint64_t)p);
     }
     timed_sync(x);
-    const bool F = pl.C == 1;
+    const bool F = pl.C == 1 && !pl.raw;
     auto patch = [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc); };
-    if (pl.redundant) {
+    if (pl.raw && !pl.redundant) {
+        // distributed combine: CTA x finishes the states x, x + grid, ... into
+        // the list, a second grid barrier, then every CTA patches from it
+        reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, blockIdx.x, gridDim.x, pis, Qs,
+                                  [&](int64_t i, int64_t s, double v, int arg) {
+                                      (void)s;
+                                      a.lval[i] = v;
+                                      a.larg[i] = arg;
+                                  },
+                                  true);
+        timed_sync(x);
+        for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+            patch_state<KIND>(a, Vs, pis, i, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
+        }
+    } else if (pl.redundant) {
         if (F) {
             for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
@@ -1044,7 +1545,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
                 patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc);
             }
         } else {
-            reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, 0, 1, pis, Qs, patch);
+            reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, 0, 1, pis, Qs, patch, pl.raw != 0);
         }
     } else {
         // last-arriver mode: the list was completed during the compute phase
@@ -1053,7 +1554,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
             patch_state<KIND>(a, Vs, pis, i, s, __ldcg(a.lval + i), __ldcg(a.larg + i), acc);
         }
     }
-    __syncthreads();
+    csync();
     prof_mark(x, &x.t_comb);
     ++x.phase;
 }
@@ -1071,12 +1572,12 @@ __device__ PhaseAcc block_reduce(PhaseAcc v)
         v.changed += __shfl_xor_sync(0xffffffffu, v.changed, o);
     }
     const int w = threadIdx.x >> 5;
-    __syncthreads();
+    csync();
     if ((threadIdx.x & 31) == 0) sd[w] = v.rmax, si[w] = v.bad, sl[w] = v.changed;
-    __syncthreads();
+    csync();
     PhaseAcc r{0.0, 0, 0};
     for (int k = 0; k < kWarps; ++k) r.rmax = fmax(r.rmax, sd[k]), r.bad |= si[k], r.changed += sl[k];
-    __syncthreads();
+    csync();
     return r;
 }
 
@@ -1119,9 +1620,9 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
 }
 
 template <typename PT, int VE, int CTA>
-__global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseArgs a)
+__global__ void __launch_bounds__(CTA == kPathTma ? kTmaThreads : kThreads, 1) dense_solver_kernel(const DenseArgs a)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     double* Vs = reinterpret_cast<double*>(smem_raw);
     const int64_t n_pad = (a.n + 3) & ~int64_t(3);
     int32_t* pis = reinterpret_cast<int32_t*>(Vs + n_pad);
@@ -1130,11 +1631,31 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
                          a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
     const bool shard = a.mode == MODE_SHARD_MIN || a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
 
+    Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
+    if constexpr (CTA == kPathTma) {
+        x.tm = tma_smem(smem_raw, a);
+        x.tst = 0;
+        x.tph = 0;
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < x.tm.nst; ++q) {
+                mbar_init(x.tm.full + q, 1);
+                mbar_init(x.tm.empty + q, kWarps);
+                x.tm.redcnt[q] = 0;
+            }
+            x.tm.ctl[0] = -1;
+            x.tm.ctl[1] = 0;
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();  // the only CTA-wide barrier: the producer warp leaves here
+        if (threadIdx.x >= kThreads) {
+            if (threadIdx.x == kThreads) tma_producer<PT>(a, pis, x.tm);
+            return;
+        }
+    }
     for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
         Vs[vs_index(j, a.vs_half)] = a.V[j];
         if (need_pi) pis[j] = a.pi[j];
     }
-    Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
     if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
     if (!a.identity && a.mode != MODE_IMPROVE && !shard) {
         Permutation pm;
@@ -1226,6 +1747,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
         a.prof[2] = x.t_comb;
         a.prof[3] = x.n_bar;
     }
+    if constexpr (CTA == kPathTma) {
+        csync();  // every compute thread is done with the ring
+        if (threadIdx.x == 0) st_release_cta(x.tm.ctl + 1, 1);  // the producer drains and exits
+    }
 }
 
 // ------------------------------------------------------------------ host
@@ -1245,7 +1770,17 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
         const char* e = getenv("RMB_DENSE_CTA");
         return e && e[0] == '1';
     }();
-    if (allow_split && rows < 16LL * num_sms) {
+    // RMB_DENSE_IPW=k (experiment): split rows until a batch offers >= k items per warp
+    static const int64_t ipw = [] {
+        const char* e = getenv("RMB_DENSE_IPW");
+        return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
+    }();
+    if (allow_split && ipw > 1 && rows < ipw * 16LL * num_sms) {
+        (void)lc_target;
+        c = std::max<int64_t>(1, (ipw * 16LL * num_sms + rows - 1) / rows);
+        c = std::min<int64_t>(c, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, cnt * A_eff)));
+        c = std::min(std::max<int64_t>(c, 1), maxC);
+    } else if (allow_split && rows < 16LL * num_sms) {
         (void)lc_target;
         // at most one item per warp (the dynamic deal then has no second round)
         c = std::max<int64_t>(1, (16LL * num_sms) / rows);
@@ -1270,6 +1805,7 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
 
 static int64_t plan_doubles(const Plan& p, int64_t cnt, int64_t groups_per_state, int A_eff)
 {
+    if (p.raw) return A_eff == 1 ? cnt * p.C : cnt * groups_per_state * kAG * p.C;
     return p.C == 1 ? cnt * (A_eff == 1 ? 1 : 2 * groups_per_state) : cnt * A_eff * p.C;
 }
 
@@ -1279,14 +1815,21 @@ static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaS
     auto kern = a.path == kPathRows ? dense_solver_kernel<PT, VE, kPathRows>
                 : a.path == kPathCta ? dense_solver_kernel<PT, VE, kPathCta>
                                      : dense_solver_kernel<PT, VE, kPathWarp>;
+    int threads = kThreads;
+    if constexpr (VE * sizeof(PT) == 16) {
+        if (a.path == kPathTma) {
+            kern = dense_solver_kernel<PT, VE, kPathTma>;
+            threads = kTmaThreads;
+        }
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {const_cast<DenseArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, st);
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st);
 }
 
 struct DenseLaunch {
@@ -1334,7 +1877,9 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.b = rq.b;
     a.seed = rq.seed;
     a.k0 = rq.k0;
-    a.identity = rq.identity ? 1 : 0;
+    // b >= n: one batch per sweep, whose result does not depend on the order
+    // of its states -> no permutation needed
+    a.identity = (rq.identity || rq.b >= n) ? 1 : 0;
     a.mode = rq.mode;
     a.pi_given = rq.pi_given ? 1 : 0;
     a.eps = rq.eps;
@@ -1390,6 +1935,68 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     if (rows)
         for (int q = 0; q < 3; ++q) a.plan[q] = rp[q];
     a.path = rows ? kPathRows : a.plan[0].cta ? kPathCta : kPathWarp;
+    // TMA ring path (default): 16-byte rows (VE full) and >= 2 ring stages next
+    // to V / pi / the reduction scratch.  Chosen from (n, A, dtype, need_pi),
+    // never from the shard, so every state's arithmetic is the same for any G.
+    {
+        static const bool tma_on = [] {
+            const char* e = getenv("RMB_DENSE_TMA");
+            return !(e && e[0] == '0');
+        }();
+        const int64_t qs_tma = std::min<int64_t>(a.qs_cap, std::max<int64_t>(1024, pr.A));  // >= A for the S-mode combine
+        const size_t ring_off = (smem_v + (size_t)std::max<int64_t>(qs_tma, 0) * 8 + 127) / 128 * 128;
+        const int64_t room = (int64_t)pr.smem_optin - (int64_t)ring_off - 16 - 4096;  // static smem
+        // ring slots of kTmaStage bytes: NG row slots of one column window
+        const int64_t piece = kTmaStage / psz, slot = kTmaStage;
+        int nst = (int)std::min<int64_t>(kTmaMaxStages, std::max<int64_t>(0, room / (slot + kTmaPerStageX)));
+        if (const char* e = getenv("RMB_TMA_NST")) nst = std::min(nst, atoi(e));
+        a.tma_gmin = 1;
+        if (const char* e = getenv("RMB_TMA_G")) a.tma_gmin = std::max(1, atoi(e));
+        a.tma_hint = 1;
+        if (const char* e = getenv("RMB_TMA_HINT")) a.tma_hint = atoi(e);
+        if (tma_on && !pr.no_tma && a.path == kPathWarp && VE * psz == 16 && nst >= 2 && qs_tma >= pr.A) {
+            a.path = kPathTma;
+            a.qs_cap = qs_tma;
+            a.tma_off = (int64_t)ring_off;
+            a.tma_nst = nst;
+            a.tma_piece = (int)piece;
+            a.tma_slot = (int)slot;
+            L.smem = ring_off + (size_t)nst * (slot + kTmaPerStageX) + 16;
+            // raw partials (A doubles per state and chunk), S-mode combines
+            a.imp_sub = n * pr.A <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / pr.A);
+            a.plan[2] = plan_chunks(n, a.imp_sub, NAG4, pr.A, VE, sms, split_ok, kAG, psz);
+            a.plan[2].ng = kAG;
+            static const int64_t red_max = [] {
+                const char* e = getenv("RMB_TMA_REDUNDANT_MAX");
+                return e ? (int64_t)atoll(e) : int64_t(2048);
+            }();
+            // items = contiguous chunks of a state's action-group range (or of
+            // its row pi(s)): C chunks per group, >= 8 items per SM per batch
+            static const int64_t ipsm = [] {  // target items per SM per batch
+                const char* e = getenv("RMB_TMA_IPSM");
+                return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
+            }();
+            a.tma_static = 16;
+            if (const char* e = getenv("RMB_TMA_STATIC")) a.tma_static = atoi(e);
+            const int64_t cnts[3] = {rq.b, rq.b, a.imp_sub};
+            const int64_t grp[3] = {NAG, 1, NAG4};
+            const int na_min = (pr.A % kAG) ? pr.A % kAG : kAG;
+            for (int q = 0; q < 3; ++q) {
+                Plan& p = a.plan[q];
+                const int64_t groups = cnts[q] * grp[q];
+                const int64_t vg_min = (q == 1 ? 1 : std::min(na_min, pr.A)) * n / VE;
+                const int64_t per = q == 1 ? 1 : kAG;  // doubles per item
+                int64_t C = groups >= ipsm * sms ? 1 : (ipsm * sms + groups - 1) / groups;
+                C = std::min<int64_t>(C, std::max<int64_t>(1, vg_min));
+                C = std::min<int64_t>(C, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, groups * per)));
+                p.C = (int)C;
+                p.Lc = 0;
+                p.raw = 1;
+                p.ng = q == 1 ? 1 : kAG;
+                p.redundant = groups * per * C <= red_max ? 1 : 0;
+            }
+        }
+    }
     const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
                                               plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A), 2 * rq.b,

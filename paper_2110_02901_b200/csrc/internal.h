@@ -97,6 +97,7 @@ struct Problem {
     double* stage_V = nullptr;    // sharded solves: this rank's replica of V (device)
     int32_t* stage_pi = nullptr;  //                 this rank's pi (owned entries meaningful)
     int ell_K = 0;  // > 0: fixed-stride rows (ELL)
+    bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 0;

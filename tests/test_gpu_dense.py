@@ -294,3 +294,36 @@ def test_policy_value_matches_linear_solve(b):
     for k in range(1, 6):
         V, _, ro = oracle.sweep(m, V, b, oracle.partition(n, 1, k), pi)
         assert abs(sol.trace[k - 1] - ro) <= 1e-11 * max(1.0, np.abs(V).max())
+
+
+# ------------------------------------------- TMA ring path vs warp path
+@pytest.mark.parametrize("n,A,b,dtype", [(600, 16, 64, np.float32), (1000, 6, 1, np.float32),
+                                         (2048, 16, 2048, np.float32), (512, 5, 37, np.float64),
+                                         (4096, 40, 500, np.float32)])
+def test_tma_path_matches_warp_path_and_oracle(n, A, b, dtype):
+    """The default dense path (cp.async.bulk ring, producer warp running one
+    batch ahead) and the register-streaming warp path (RMB_DENSE_NO_TMA) solve
+    the same MB-VI: same sweep count, V within rounding, and the oracle."""
+    m, prob, P, c = make(n, A, seed=31 + n, dtype=dtype, gamma=0.95)
+    warp = rmb.Problem.dense(tdev(P), tdev(c), 0.95, tma=False)
+    s1 = prob.vi(b, seed=4, eps=1e-8, max_sweeps=400)
+    s2 = warp.vi(b, seed=4, eps=1e-8, max_sweeps=400)
+    ref = oracle.vi(m, b, seed=4, eps=1e-8, max_sweeps=400)
+    assert s1.stats.sweeps == s2.stats.sweeps == ref.sweeps
+    assert_close(s1.V.cpu().numpy(), s2.V.cpu().numpy(), 1e-12)
+    assert_close(s1.V.cpu().numpy(), ref.V, 1e-9)
+    mask = qgap(m, ref.V) > 1e-6
+    assert np.array_equal(s1.pi.cpu().numpy()[mask], ref.pi[mask])
+
+
+@pytest.mark.parametrize("b,msweeps", [(1, 2), (100, 5), (1024, 3)])
+def test_tma_path_mpi_matches_oracle(b, msweeps):
+    """MB-MPI on the TMA path: evaluation sweeps right after an improvement are
+    fenced (their rows depend on the new pi); outer iterations, V, pi match."""
+    n, A = 1024, 8
+    m, prob, P, c = make(n, A, seed=77, dtype=np.float32, gamma=0.95)
+    sol = prob.mpi(b, msweeps, seed=2, eps=1e-7, max_outer=200)
+    ref = oracle.mpi(m, b, msweeps, seed=2, eps=1e-7, max_outer=200)
+    assert sol.stats.outer_iters == ref.outer
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
