@@ -116,6 +116,7 @@ struct DenseArgs {
     int tma_gmin;        //           minimum items per dynamic grab (experiments: RMB_TMA_G)
     int tma_piece;       //           columns per stage and row slot
     int tma_static;      //           batches with <= tma_static * grid items are dealt statically
+    int tma_pf;          //           L2 prefetch of an item's later stages at its start (RMB_TMA_PF=0 disables)
     int tma_slot;        //           bytes per ring slot (piece bytes rounded up to 128)
     int tma_hint;        //           L2 evict-first hint on the bulk copies (RMB_TMA_HINT=0 disables)
 };
@@ -913,6 +914,10 @@ constexpr int kTmaStage = RMB_TMA_STAGE;   // bytes per ring stage
 constexpr int kTmaMaxStages = 24;
 constexpr int kTmaVecs = kTmaStage / 16;   // 16-byte vectors per stage
 constexpr int kTmaThreads = kThreads + kWarp;
+#ifndef RMB_TMA_CW
+#define RMB_TMA_CW 16
+#endif
+constexpr int kTmaCW = RMB_TMA_CW;          // compute warps that consume the ring (the others idle to the barrier)
 
 struct TmaMeta {         // one per stage, written by the producer before its arrive
     long long i;         // batch position (END marker: batch sequence number)
@@ -1188,7 +1193,14 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
             // columns [c0, c1) (vector aligned) of the group's rows
             const int c1 = (int)((uint64_t)nvecs * (ch + 1) / C) * VB;
             const PT* rowp = P + ((int64_t)s * a.A + a0) * n;
-            for (int col = (int)((uint64_t)nvecs * ch / C) * VB; col < c1 && !stop; col += w) {
+            const int c0 = (int)((uint64_t)nvecs * ch / C) * VB;
+            if (a.tma_pf && c1 - c0 > w) {
+                // the item's stages after the first go through L2 first: HBM
+                // latency leaves the ring round trip, more bytes in flight
+                for (int gg = 0; gg < na; ++gg)
+                    prefetch_l2(rowp + (int64_t)gg * n + c0 + w, (uint32_t)((c1 - c0 - w) * (int)sizeof(PT)));
+            }
+            for (int col = c0; col < c1 && !stop; col += w) {
                 const int len = min(w, c1 - col);
                 if (!acquire()) { stop = true; break; }
                 TmaMeta& md = m.meta[st];
@@ -1247,6 +1259,7 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
     constexpr int RV = kTmaStage / NG / 16;  // vectors per row slot
     using VT = typename Vec<PT, E>::T;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (warp >= kTmaCW) return;  // fewer, fuller consumer warps: less issue overhead per byte
     const int NAG = EVAL ? 1 : (a.A + NG - 1) / NG;
     const int C = pl.C;
     const int64_t half = a.vs_half;
@@ -1268,7 +1281,7 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
         const VT* stg = reinterpret_cast<const VT*>(m.ring + (size_t)st * kTmaStage);
         if (RMB_TMA_EXP != 2) {
 #pragma unroll
-            for (int f0 = 0; f0 < RV; f0 += kThreads) {
+            for (int f0 = 0; f0 < RV; f0 += kTmaCW * kWarp) {
                 const int f = f0 + t;
                 if (f < md.nvec) {
                     double vs[E];
@@ -1287,7 +1300,7 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
             }
         }
         if (md.flags & 1) {
-            double* red = m.red + (size_t)st * kWarps * kAG;
+            double* red = m.red + (size_t)st * kTmaCW * kAG;
 #pragma unroll
             for (int g = 0; g < NG; ++g) {
                 const double w = warp_sum(acc[g]);
@@ -1303,13 +1316,13 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
                              : "memory");
             }
             prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev == kWarps - 1) {
+            if (prev == kTmaCW - 1) {
                 // lane g < NG sums row g over the warps in order; plain stores,
                 // no global round trip on the streaming warps (costs, chunk
                 // sums and the min are the combine's); rows >= na store 0
                 if (lane < NG) {
                     double dsum = 0.0;
-                    for (int w = 0; w < kWarps; ++w) dsum += red[w * kAG + lane];
+                    for (int w = 0; w < kTmaCW; ++w) dsum += red[w * kAG + lane];
                     part[(((int64_t)md.i * NAG + md.na) * C + md.ch) * NG + lane] = dsum;
                 }
                 if (lane == 0) m.redcnt[st] = 0;
@@ -1639,7 +1652,7 @@ __global__ void __launch_bounds__(CTA == kPathTma ? kTmaThreads : kThreads, 1) d
         if (threadIdx.x == 0) {
             for (int q = 0; q < x.tm.nst; ++q) {
                 mbar_init(x.tm.full + q, 1);
-                mbar_init(x.tm.empty + q, kWarps);
+                mbar_init(x.tm.empty + q, kTmaCW);
                 x.tm.redcnt[q] = 0;
             }
             x.tm.ctl[0] = -1;
@@ -1943,9 +1956,9 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
             const char* e = getenv("RMB_DENSE_TMA");
             return !(e && e[0] == '0');
         }();
-        const int64_t qs_tma = std::min<int64_t>(a.qs_cap, std::max<int64_t>(1024, pr.A));  // >= A for the S-mode combine
+        const int64_t qs_tma = std::min<int64_t>(a.qs_cap, std::max<int64_t>(512, pr.A));  // >= A for the S-mode combine
         const size_t ring_off = (smem_v + (size_t)std::max<int64_t>(qs_tma, 0) * 8 + 127) / 128 * 128;
-        const int64_t room = (int64_t)pr.smem_optin - (int64_t)ring_off - 16 - 4096;  // static smem
+        const int64_t room = (int64_t)pr.smem_optin - (int64_t)ring_off - 16 - 2048;  // static smem
         // ring slots of kTmaStage bytes: NG row slots of one column window
         const int64_t piece = kTmaStage / psz, slot = kTmaStage;
         int nst = (int)std::min<int64_t>(kTmaMaxStages, std::max<int64_t>(0, room / (slot + kTmaPerStageX)));
@@ -1977,6 +1990,8 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
                 return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
             }();
             a.tma_static = 16;
+            a.tma_pf = 0;  // measured: slower (the prefetches compete with the ring's own loads)
+            if (const char* e = getenv("RMB_TMA_PF")) a.tma_pf = atoi(e);
             if (const char* e = getenv("RMB_TMA_STATIC")) a.tma_static = atoi(e);
             const int64_t cnts[3] = {rq.b, rq.b, a.imp_sub};
             const int64_t grp[3] = {NAG, 1, NAG4};
