@@ -311,7 +311,7 @@ def main():
                      "traffic_note": "dram read+write bytes per launch = per-sweep DRAM bytes of the committed "
                                      "ncu --set full capture (profiles/ncu_traffic.json) x sweeps per solve",
                      "achieved_bytes_per_launch": sweeps * bps / args.steps,
-                     "peak_source": peak_src, "kernel": "dense_solver_kernel<float,4,3> (TMA ring path)",
+                     "peak_source": peak_src, "kernel": "dense_tma_kernel<float,4> (TMA ring path)",
                      "algorithmic_bytes_per_sweep": bps,
                      "peak_note": "MEASURED_PEAKS hbm_gbs is a device-to-device COPY (read+write turnaround); "
                                   "this kernel is a read stream (P) and can exceed it; frac_nominal is vs the "

@@ -1493,6 +1493,93 @@ __device__ __forceinline__ void timed_sync(Ctx& x)
     x.n_bar++;
 }
 
+
+// Fast redundant combine (TMA path, small batches): L = pow2 >= Ae lanes per
+// state, thread t serves action t % L of the states t / L + k * (512 / L).  The
+// state ids and costs (independent of V) are loaded BEFORE the grid barrier;
+// after it, the chunk partials are summed and the argmin (lower value, then
+// lower action) is a shuffle butterfly inside the L lanes: no smem scratch,
+// no CTA barrier, one L2 round trip after the grid barrier.
+constexpr int kFastK = 2;  // rounds per thread (states per batch <= kFastK * 512 / L)
+struct FastPre {
+    int s[kFastK];  // state id (< 2^31), -1 = idle lane
+    int act[kFastK];
+    double cost[kFastK];
+};
+__device__ __forceinline__ int fast_lanes(int Ae) { return Ae <= 1 ? 1 : 1 << (32 - __clz(Ae - 1)); }
+
+template <typename PT, bool EVAL>
+__device__ __forceinline__ void fast_pre(const DenseArgs& a, const uint32_t* perm, int64_t lo, int64_t cnt,
+                                         const int32_t* pis, int L, FastPre& fp)
+{
+    const int Ae = EVAL ? 1 : a.A;
+    const int t = threadIdx.x;
+    const int per_round = kThreads / L;
+#pragma unroll
+    for (int k = 0; k < kFastK; ++k) {
+        const int64_t kk = (int64_t)k * per_round + t / L;
+        const int act = t % L;
+        fp.s[k] = -1;
+        fp.act[k] = act;
+        fp.cost[k] = 0.0;
+        if (kk < cnt && act < Ae) {
+            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + kk) : lo + kk;
+            fp.s[k] = (int)s;
+            const int ac = EVAL ? pis[s] : act;
+            fp.act[k] = ac;
+            fp.cost[k] = load_cost<PT>(a, s * a.A + ac);
+        }
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void fast_argmin(double& v, int& arg)
+{
+    if constexpr (L > 1) group_argmin<L>(v, arg);
+}
+
+template <typename PT, int KIND>
+__device__ __forceinline__ void fast_finish(const DenseArgs& a, double* Vs, int32_t* pis, const double* part,
+                                            int C, int64_t cnt, int L, const FastPre& fp, PhaseAcc& acc)
+{
+    constexpr bool EVAL = KIND == 1 || KIND == 4;
+    const int t = threadIdx.x;
+    const int per_round = kThreads / L;
+    const int NAGr = (a.A + kAG - 1) / kAG;
+#pragma unroll
+    for (int k = 0; k < kFastK; ++k) {
+        const int64_t kk = (int64_t)k * per_round + t / L;
+        if (k * per_round >= cnt) break;  // uniform
+        double v = INFINITY;
+        int arg = 0x7fffffff;
+        if (fp.s[k] >= 0) {
+            const int act = fp.act[k];
+            const double* pp = part + (EVAL ? kk * C : ((kk * NAGr + act / kAG) * C) * kAG + act % kAG);
+            const int pstr = EVAL ? 1 : kAG;
+            double sum = 0.0;
+            for (int c0 = 0; c0 < C; c0 += 4) {  // 4 loads in flight, added in chunk order
+                double tv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tv[q] = c0 + q < C ? __ldcg(pp + (int64_t)(c0 + q) * pstr) : 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (c0 + q < C) sum += tv[q];
+            }
+            v = fp.cost[k] + a.gamma * sum;
+            arg = act;
+        }
+        switch (L) {
+        case 2: fast_argmin<2>(v, arg); break;
+        case 4: fast_argmin<4>(v, arg); break;
+        case 8: fast_argmin<8>(v, arg); break;
+        case 16: fast_argmin<16>(v, arg); break;
+        case 32: fast_argmin<32>(v, arg); break;
+        default: break;
+        }
+        if (t % L == 0 && fp.s[k] >= 0) patch_state<KIND>(a, Vs, pis, kk, (int64_t)fp.s[k], v, arg, acc);
+    }
+}
+
 // One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
 template <typename PT, int VE, int KIND, int CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
@@ -1530,10 +1617,22 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
         for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < a.n; p += stride)
             dst[p] = (uint32_t)pm((uint64_t)p);
     }
+    constexpr int AeK = EVAL ? 1 : 0;
+    const int Ae = AeK ? 1 : a.A;
+    const int L = fast_lanes(Ae);
+    // decided from the plan's batch size, not cnt (a shard step's cnt is its
+    // share): the same states take the same summation order for any G
+    const int64_t plan_cnt = KIND == 2 ? a.imp_sub : a.b;
+    const bool fast = CTA == kPathTma && pl.raw && pl.redundant && pl.C <= 4 && L <= 32 &&
+                      plan_cnt * L <= (int64_t)kFastK * kThreads;
+    FastPre fp;
+    if (fast) fast_pre<PT, EVAL>(a, perm, lo, cnt, pis, L, fp);
     timed_sync(x);
     const bool F = pl.C == 1 && !pl.raw;
     auto patch = [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc); };
-    if (pl.raw && !pl.redundant) {
+    if (fast) {
+        fast_finish<PT, KIND>(a, Vs, pis, part, pl.C, cnt, L, fp, acc);
+    } else if (pl.raw && !pl.redundant) {
         // distributed combine: CTA x finishes the states x, x + grid, ... into
         // the list, a second grid barrier, then every CTA patches from it
         reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, blockIdx.x, gridDim.x, pis, Qs,
@@ -1633,7 +1732,7 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
 }
 
 template <typename PT, int VE, int CTA>
-__global__ void __launch_bounds__(CTA == kPathTma ? kTmaThreads : kThreads, 1) dense_solver_kernel(const DenseArgs a)
+__device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* Vs = reinterpret_cast<double*>(smem_raw);
@@ -1766,6 +1865,21 @@ __global__ void __launch_bounds__(CTA == kPathTma ? kTmaThreads : kThreads, 1) d
     }
 }
 
+// register-streaming paths: 512 threads, 128 registers
+template <typename PT, int VE, int CTA>
+__global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseArgs a)
+{
+    dense_solver_body<PT, VE, CTA>(a);
+}
+
+// TMA ring path: 512 compute threads + the producer warp (17 warps: one SM
+// sub-partition holds 5 of them, so 96 registers per thread)
+template <typename PT, int VE>
+__global__ void __launch_bounds__(kTmaThreads, 1) dense_tma_kernel(const DenseArgs a)
+{
+    dense_solver_body<PT, VE, kPathTma>(a);
+}
+
 // ------------------------------------------------------------------ host
 // rows = (states per batch) x (items per state before chunking).  Items are
 // NG rows x Lc columns of P: at most ~16 KB so that the dynamically scheduled
@@ -1831,7 +1945,7 @@ static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaS
     int threads = kThreads;
     if constexpr (VE * sizeof(PT) == 16) {
         if (a.path == kPathTma) {
-            kern = dense_solver_kernel<PT, VE, kPathTma>;
+            kern = dense_tma_kernel<PT, VE>;
             threads = kTmaThreads;
         }
     }
