@@ -197,6 +197,29 @@ def other_configs(rmb, torch, dev):
     return out
 
 
+def paper_envs(rmb, torch):
+    """Secondary lines: the paper's own environments (gen/envs.py),
+    MB-VI to a 1e-6 residual at b = 1 (GS-VI), |S|/10 and |S| (VI): sweeps,
+    time-to-eps and time per batch — the latency-bound regime of SURVEY 6."""
+    from gen import envs
+    out = []
+    for name, f in (("FrozenLake 8x8", envs.frozenlake), ("Taxi", envs.taxi),
+                    ("2D-Maze N=80", lambda: envs.maze(80)), ("2D-Maze N=100", lambda: envs.maze(100))):
+        n, A, rp, col, val, c, _ = f()
+        dev = lambda x: torch.from_numpy(x).cuda()
+        prob = rmb.Problem.csr(n, A, dev(rp), dev(col), dev(val), dev(c), 0.95)
+        prob.vi(n, seed=0, eps=1e-6, max_sweeps=3)
+        rows = []
+        for b in (1, max(1, n // 10), n):
+            sol = prob.vi(b, seed=0, eps=1e-6, max_sweeps=100_000)
+            st = sol.stats
+            rows.append({"b": b, "sweeps": st.sweeps, "time_to_eps_ms": st.seconds * 1e3,
+                         "us_per_batch": st.seconds / max(1, st.batches) * 1e6})
+        out.append({"env": name, "n": n, "A": A, "nnz": int(len(val)), "gamma": 0.95, "vi": rows})
+        prob.close()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -368,6 +391,9 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_other:
         result["other_configs"] = other_configs(rmb, torch, dev)
+
+    if rank == 0 and world == 1 and not args.no_other:
+        result["paper_envs"] = paper_envs(rmb, torch)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, cores, sample = oracle_sample()

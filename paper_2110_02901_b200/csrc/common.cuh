@@ -91,6 +91,10 @@ __device__ __forceinline__ void grid_sync(GridBarrier& g)
         if constexpr (NT == 0) __syncthreads();
         else bar_sync_n<NT>();
     };
+    if (g.nblocks == 1) {  // single-CTA launch (small problems): a CTA barrier is the grid barrier
+        csync();
+        return;
+    }
 #if RMB_BARRIER_VARIANT == 1
     // arrive with a fire-and-forget release reduction, then poll the arrival
     // counter itself (no separate release flag round trip)

@@ -35,6 +35,9 @@
 
 namespace rmb {
 
+constexpr int64_t kSparseSmallBatchNnz = 2048;  // nonzeros per batch up to which a solve runs on one CTA
+
+
 // CTA size per layout: row mode (a lane per action row, short rows, many
 // dependent gathers) wants the warps; vec / strided fit 512 threads without spills
 constexpr int kSWarpsMax = 32;
@@ -625,7 +628,13 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     cudaEventCreate(&e1);
     cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
-    const int grid = pr.num_sms;
+    // tiny batches (<= 2048 nonzeros, e.g. GS-VI on the paper's environments)
+    // are latency-bound: one CTA with CTA barriers beats a 148-CTA grid
+    // barrier per batch (measured: FrozenLake b=1 96 vs 125 ms, maze80 b=1
+    // 5.96 vs 7.35 s; from ~10^4 nonzeros per batch the full grid wins)
+    const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(rq.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
+    int grid = nnz_batch <= kSparseSmallBatchNnz ? 1 : pr.num_sms;
+    if (const char* e = getenv("RMB_SPARSE_GRID")) grid = std::max(1, std::min(pr.num_sms, atoi(e)));
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
             ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, st)
