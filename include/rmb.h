@@ -74,6 +74,9 @@ typedef struct {
 #define RMB_V0_ZERO 0x2u        /* ignore V's content on entry and start from V0 = 0        */
 #define RMB_PI_GIVEN 0x4u       /* rmb_mpi: pi holds the initial policy (else pi_0 = greedy(V0))     */
 #define RMB_VALIDATE 0x8u       /* rmb_create_*: check the MDP on device (RMB_ERR_INVALID_MDP)       */
+#define RMB_DENSE_VGLOBAL 0x20u /* rmb_create_dense: keep V and pi in global memory (L2) even when a
+                                   shared-memory copy fits (automatic for n > ~20k: the TMA path's
+                                   global-V mode); for tests of that mode on small instances    */
 #define RMB_DENSE_NO_TMA 0x10u  /* rmb_create_dense: stream P rows with per-warp register loads instead
                                    of the default TMA (cp.async.bulk) shared-memory ring; results agree
                                    to fp64 rounding (A/B measurement and cross-path tests)            */

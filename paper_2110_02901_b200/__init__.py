@@ -26,7 +26,7 @@ LIB_PATH = os.environ.get("RMB_LIB_PATH") or os.path.join(_HERE, "librmb.so")  #
 # status codes (include/rmb.h)
 OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(9)
 F32, F64 = 0, 1
-ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA = 0x1, 0x2, 0x4, 0x8, 0x10
+ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 
 _lib = None
 
@@ -190,19 +190,21 @@ class Problem:
 
     # ------------------------------------------------------------ creation
     @classmethod
-    def dense(cls, P, c, gamma, stream=None, validate=False, n=None, row_range=None, nccl_comm=None, tma=True):
+    def dense(cls, P, c, gamma, stream=None, validate=False, n=None, row_range=None, nccl_comm=None, tma=True,
+              vglobal=False):
         """P: [n][A][n], c: [n][A] (float32/float64, torch cuda/cpu or numpy).
         Shard handle (multi-GPU): P = the owned rows [r1-r0][A][n], c = [r1-r0][A],
         n = the global state count, row_range = (r0, r1) from shard_range(),
         nccl_comm = comm_init(...) (or None for a logical group on one GPU).
-        tma=False: RMB_DENSE_NO_TMA (register-streaming warp path instead of the TMA ring)."""
+        tma=False: RMB_DENSE_NO_TMA (register-streaming warp path instead of the TMA ring).
+        vglobal=True: RMB_DENSE_VGLOBAL (V and pi in global memory; automatic for large n)."""
         rows, A, ncol = P.shape
         n = ncol if n is None else n
         r0, r1 = row_range if row_range is not None else (0, n)
         assert ncol == n and rows == r1 - r0 and tuple(c.shape) == (rows, A) and c.dtype == P.dtype
         d = _Desc(n, A, float(gamma), _dtype_code(P), F64, r0, r1, nccl_comm, _stream_ptr(stream))
         h = ctypes.c_void_p()
-        flags = (VALIDATE if validate else 0) | (0 if tma else DENSE_NO_TMA)
+        flags = (VALIDATE if validate else 0) | (0 if tma else DENSE_NO_TMA) | (DENSE_VGLOBAL if vglobal else 0)
         _check(lib().rmb_create_dense(ctypes.byref(d), _ptr(P), _ptr(c), flags, ctypes.byref(h)))
         return cls(h, n, A, float(gamma), (P, c))
 

@@ -249,6 +249,7 @@ rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, 
     if (s == RMB_OK) s = device_view(*pr, c, std::max<size_t>(1, rows * pr->A * psz), &pr->c, "copy c to device");
     pr->dense = true;
     pr->no_tma = (flags & RMB_DENSE_NO_TMA) != 0;
+    pr->vglobal = (flags & RMB_DENSE_VGLOBAL) != 0;
     if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
     if (s != RMB_OK) {
         free_problem(pr);

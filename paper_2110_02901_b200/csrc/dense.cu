@@ -46,6 +46,10 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kAG = 4;                     // actions per compute item (min modes)
 constexpr int kPathWarp = 0, kPathCta = 1, kPathRows = 2, kPathTma = 3;  // compute path of a kernel instantiation
+// TMA path with V (and pi) in GLOBAL memory (L2-resident) instead of shared
+// memory: dense n too large for a shared-memory copy of V (n > ~27k)
+constexpr int kPathTmaG = 4;
+__host__ __device__ constexpr bool is_tma(int c) { return c == kPathTma || c == kPathTmaG; }
 constexpr int64_t kRedundantMax = 8192;    // doubles of batch partials reduced by every CTA
 
 // CTA barrier of the 512 compute threads (named barrier 1).  Identical to
@@ -114,6 +118,7 @@ struct DenseArgs {
     int64_t tma_off;     // TMA path: byte offset of the stage ring in dynamic smem
     int tma_nst;         //           ring stages
     int tma_gmin;        //           minimum items per dynamic grab (experiments: RMB_TMA_G)
+    unsigned long long* gred;  // global-V path: 4 reduction slots x 4 words (rmax bits, bad, changed)
     int tma_piece;       //           columns per stage and row slot
     int tma_static;      //           batches with <= tma_static * grid items are dealt statically
     int tma_pf;          //           L2 prefetch of an item's later stages at its start (RMB_TMA_PF=0 disables)
@@ -227,6 +232,13 @@ __device__ __forceinline__ void dot_rows(const PT* __restrict__ row0, int64_t n,
         if constexpr (NA == 2) t = part[g][0] + part[g][1];
         acc[g] += t;
     }
+}
+
+// pi may live in shared memory (copy) or in global memory (global-V path,
+// written by other SMs between phases: read through L2, never a stale L1 line)
+__device__ __forceinline__ int ld_pi(const int32_t* pis, int64_t s)
+{
+    return __isGlobal(pis) ? __ldcg(pis + s) : pis[s];
 }
 
 template <typename PT>
@@ -1188,7 +1200,7 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
             const unsigned ag = rr / C;
             const unsigned ch = rr - ag * C;
             const int64_t s = bt.perm ? (int64_t)__ldcg(bt.perm + bt.lo + i) : bt.lo + i;
-            const int a0 = eval ? pis[s] : (int)ag * NG;
+            const int a0 = eval ? ld_pi(pis, s) : (int)ag * NG;
             const int na = eval ? 1 : min(NG, a.A - a0);
             // columns [c0, c1) (vector aligned) of the group's rows
             const int c1 = (int)((uint64_t)nvecs * (ch + 1) / C) * VB;
@@ -1250,7 +1262,17 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
 // slot offset g * kTmaStage/NG); thread t takes column vectors t, t + 512, ...
 // and, per vector, reads V once and dots it with every row.  Raw partials:
 //   part[((i*NAG + ag)*C + ch)*NG + g] = sum over the item of P(row a0+g) . V
-template <typename PT, bool EVAL>
+template <int VE>
+__device__ __forceinline__ void load_v_global(const double* V, int64_t j, double (&v)[VE])
+{
+#pragma unroll
+    for (int q = 0; q < VE; q += 2) {
+        const double2 x = __ldcg(reinterpret_cast<const double2*>(V + j + q));
+        v[q] = x.x, v[q + 1] = x.y;
+    }
+}
+
+template <typename PT, bool EVAL, bool VGL = false>
 __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Plan& pl, double* part,
                                   const TmaSmem& m, int& st, unsigned& ph)
 {
@@ -1285,7 +1307,8 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
                 const int f = f0 + t;
                 if (f < md.nvec) {
                     double vs[E];
-                    load_v<E>(Vs, md.e + f * E, vs, half);
+                    if constexpr (VGL) load_v_global<E>(Vs, md.e + f * E, vs);
+                    else load_v<E>(Vs, md.e + f * E, vs, half);
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
                         if (g < md.a0) {
@@ -1393,7 +1416,7 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
                 const int ai = (int)(q - kk * Ae);
                 const int64_t i = first + (k0 + kk) * step;
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-                const int act = EVAL ? pis[s] : ai;
+                const int act = EVAL ? ld_pi(pis, s) : ai;
                 const double* pp = part + pbase(i, act);
                 double sum = 0.0;
                 for (int ch = 0; ch < C; ++ch) sum += __ldcg(pp + (int64_t)ch * pstr);
@@ -1405,7 +1428,7 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
                 const int ai = (int)(q - kk * Ae);
                 const int64_t i = first + (k0 + kk) * step;
                 const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-                const int act = EVAL ? pis[s] : ai;
+                const int act = EVAL ? ld_pi(pis, s) : ai;
                 const double* pp = part + pbase(i, act);
                 double sum = 0.0;
                 for (int ch = lane; ch < C; ch += kWarp) sum += __ldcg(pp + (int64_t)ch * pstr);
@@ -1418,7 +1441,7 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
             const int64_t i = first + (k0 + kk) * step;
             const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
             double best = Qs[kk * Ae];
-            int barg = EVAL ? pis[s] : 0;
+            int barg = EVAL ? ld_pi(pis, s) : 0;
             if (!EVAL)
                 for (int act = 1; act < a.A; ++act) {
                     const double Q = Qs[kk * Ae + act];
@@ -1434,10 +1457,31 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
 // 2: improvement).  CTA 0 also writes the global outputs.
 // KIND 3 / 4 (shard B_b / B_pi,b): the new value goes to this rank's send list
 // (position i) instead of the local V; the exchange + commit apply it.
-template <int KIND>
+template <int KIND, bool VGL = false>
 __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int32_t* pis, int64_t i, int64_t s, double v,
                                             int arg, PhaseAcc& acc)
 {
+    if (VGL) {
+        // global V / pi: every state is patched by exactly one CTA (distributed
+        // combine) and the residual / changed counts are reduced over the grid
+        acc.bad |= !isfinite(v);
+        if (KIND >= 3) {
+            a.send_val[i] = v;
+            a.send_idx[i] = (uint32_t)s;
+            a.send_arg[i] = arg;
+        } else if (KIND == 2) {
+            const double old = __ldcg(a.V + s);
+            acc.rmax = fmax(acc.rmax, fabs(v - old));
+            acc.changed += (arg != __ldcg(a.pi + s));
+            a.pi[s] = arg;
+        } else {
+            const double old = __ldcg(a.V + s);
+            acc.rmax = fmax(acc.rmax, fabs(v - old));
+            a.V[s] = v;
+            if (KIND == 0 && a.pi) a.pi[s] = arg;
+        }
+        return;
+    }
     if (KIND >= 3) {
         acc.bad |= !isfinite(v);
         if (blockIdx.x == 0) {
@@ -1474,6 +1518,7 @@ struct Ctx {
     TmaSmem tm;       // TMA path: ring and the compute threads' position in it
     int tst;
     unsigned tph;
+    long long gred_seq;  // global-V path: grid reductions so far (ring slot)
 };
 
 __device__ __forceinline__ void prof_mark(Ctx& x, long long* slot)
@@ -1525,7 +1570,7 @@ __device__ __forceinline__ void fast_pre(const DenseArgs& a, const uint32_t* per
         if (kk < cnt && act < Ae) {
             const int64_t s = perm ? (int64_t)__ldcg(perm + lo + kk) : lo + kk;
             fp.s[k] = (int)s;
-            const int ac = EVAL ? pis[s] : act;
+            const int ac = EVAL ? ld_pi(pis, s) : act;
             fp.act[k] = ac;
             fp.cost[k] = load_cost<PT>(a, s * a.A + ac);
         }
@@ -1588,7 +1633,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
 {
     constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
-    if constexpr (CTA == kPathTma) {
+    if constexpr (is_tma(CTA)) {
         // the producer may now run one batch ahead of this one (counters are
         // re-armed by the producers themselves)
         if (threadIdx.x == 0) st_release_cta(x.tm.ctl, x.phase);
@@ -1600,8 +1645,8 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     }
     // one compute path per kernel instantiation (register allocation is per
     // kernel: mixing paths made every path spill)
-    if constexpr (CTA == kPathTma)
-        compute_phase_tma<PT, EVAL>(a, Vs, pl, part, x.tm, x.tst, x.tph);
+    if constexpr (is_tma(CTA))
+        compute_phase_tma<PT, EVAL, CTA == kPathTmaG>(a, Vs, pl, part, x.tm, x.tst, x.tph);
     else if constexpr (CTA == kPathRows)
         compute_phase_rows<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     else if constexpr (CTA == kPathCta)
@@ -1630,7 +1675,15 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     timed_sync(x);
     const bool F = pl.C == 1 && !pl.raw;
     auto patch = [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc); };
-    if (fast) {
+    if constexpr (CTA == kPathTmaG) {
+        // global V: CTA x finishes and writes the states x, x + grid, ...; a
+        // second barrier makes the batch visible before the next batch reads
+        reduce_states_S<PT, EVAL>(
+            a, part, pl.C, perm, lo, cnt, blockIdx.x, gridDim.x, pis, Qs,
+            [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND, true>(a, Vs, pis, i, s, v, arg, acc); },
+            true);
+        timed_sync(x);
+    } else if (fast) {
         fast_finish<PT, KIND>(a, Vs, pis, part, pl.C, cnt, L, fp, acc);
     } else if (pl.raw && !pl.redundant) {
         // distributed combine: CTA x finishes the states x, x + grid, ... into
@@ -1693,6 +1746,39 @@ __device__ PhaseAcc block_reduce(PhaseAcc v)
     return r;
 }
 
+// Grid-wide reduction of a PhaseAcc (global-V path, where each CTA saw only
+// its share of the states): CTA partials -> atomics on a ring slot -> barrier.
+__device__ PhaseAcc grid_reduce(const DenseArgs& a, Ctx& x, PhaseAcc v)
+{
+    PhaseAcc r = block_reduce(v);
+    unsigned long long* slot = a.gred + 4 * (x.gred_seq & 3);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // re-arm the slot used two reductions ahead
+        unsigned long long* z = a.gred + 4 * ((x.gred_seq + 2) & 3);
+        atomicExch(z, 0ull);
+        atomicExch(z + 1, 0ull);
+        atomicExch(z + 2, 0ull);
+    }
+    if (threadIdx.x == 0) {
+        atomicMax(slot, (unsigned long long)__double_as_longlong(r.rmax));  // rmax >= 0: bits order = value order
+        if (r.bad) atomicOr(slot + 1, 1ull);
+        if (r.changed) atomicAdd(slot + 2, (unsigned long long)r.changed);
+    }
+    timed_sync(x);
+    PhaseAcc g;
+    g.rmax = __longlong_as_double((long long)ld_acquire_gpu(slot));
+    g.bad = ld_acquire_gpu(slot + 1) != 0;
+    g.changed = (long long)ld_acquire_gpu(slot + 2);
+    ++x.gred_seq;
+    return g;
+}
+
+template <int CTA>
+__device__ __forceinline__ PhaseAcc phase_reduce(const DenseArgs& a, Ctx& x, PhaseAcc v)
+{
+    if constexpr (CTA == kPathTmaG) return grid_reduce(a, x, v);
+    else return block_reduce(v);
+}
+
 // One application of B_b (EVAL = false) or B_{pi,b} (EVAL = true), sweep k.
 template <typename PT, int VE, bool EVAL, int CTA>
 __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, int64_t k, double* Qs)
@@ -1717,7 +1803,7 @@ __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* p
                                          (lo == 0 && !a.identity) ? k + 1 : 0, pn, ln, cn);
         ++x.batches;
     }
-    return block_reduce(acc);
+    return phase_reduce<CTA>(a, x, acc);
 }
 
 template <typename PT, int VE, int CTA>
@@ -1728,7 +1814,7 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
         const int64_t cnt = min(a.imp_sub, a.row1 - lo);
         run_batch<PT, VE, 2, CTA>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
     }
-    return block_reduce(acc);
+    return phase_reduce<CTA>(a, x, acc);
 }
 
 template <typename PT, int VE, int CTA>
@@ -1744,7 +1830,12 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
     const bool shard = a.mode == MODE_SHARD_MIN || a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
 
     Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
-    if constexpr (CTA == kPathTma) {
+    x.gred_seq = 0;
+    if constexpr (CTA == kPathTmaG) {  // V and pi stay in global memory (L2)
+        Vs = a.V;
+        pis = a.pi;
+    }
+    if constexpr (is_tma(CTA)) {
         x.tm = tma_smem(smem_raw, a);
         x.tst = 0;
         x.tph = 0;
@@ -1764,9 +1855,11 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
             return;
         }
     }
-    for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
-        Vs[vs_index(j, a.vs_half)] = a.V[j];
-        if (need_pi) pis[j] = a.pi[j];
+    if constexpr (CTA != kPathTmaG) {
+        for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
+            Vs[vs_index(j, a.vs_half)] = a.V[j];
+            if (need_pi) pis[j] = a.pi[j];
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
     if (!a.identity && a.mode != MODE_IMPROVE && !shard) {
@@ -1792,7 +1885,7 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
             run_batch<PT, VE, 3, CTA>(a, x, Vs, pis, a.olist, 0, cnt, a.plan[0], acc, Qs, 0);
         else
             run_batch<PT, VE, 4, CTA>(a, x, Vs, pis, a.olist, 0, cnt, a.plan[1], acc, Qs, 0);
-        PhaseAcc r = block_reduce(acc);
+        PhaseAcc r = phase_reduce<CTA>(a, x, acc);
         status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
         x.batches = 1;
     } else if (a.mode == MODE_SHARD_IMPROVE) {
@@ -1859,7 +1952,7 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
         a.prof[2] = x.t_comb;
         a.prof[3] = x.n_bar;
     }
-    if constexpr (CTA == kPathTma) {
+    if constexpr (is_tma(CTA)) {
         csync();  // every compute thread is done with the ring
         if (threadIdx.x == 0) st_release_cta(x.tm.ctl + 1, 1);  // the producer drains and exits
     }
@@ -1873,11 +1966,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_solver_kernel(const DenseAr
 }
 
 // TMA ring path: 512 compute threads + the producer warp (17 warps: one SM
-// sub-partition holds 5 of them, so 96 registers per thread)
-template <typename PT, int VE>
+// sub-partition holds 5 of them, so 96 registers per thread).  VGL: V and pi
+// in global memory (dense n too large for a shared-memory copy of V).
+template <typename PT, int VE, bool VGL>
 __global__ void __launch_bounds__(kTmaThreads, 1) dense_tma_kernel(const DenseArgs a)
 {
-    dense_solver_body<PT, VE, kPathTma>(a);
+    dense_solver_body<PT, VE, VGL ? kPathTmaG : kPathTma>(a);
 }
 
 // ------------------------------------------------------------------ host
@@ -1945,7 +2039,10 @@ static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaS
     int threads = kThreads;
     if constexpr (VE * sizeof(PT) == 16) {
         if (a.path == kPathTma) {
-            kern = dense_tma_kernel<PT, VE>;
+            kern = dense_tma_kernel<PT, VE, false>;
+            threads = kTmaThreads;
+        } else if (a.path == kPathTmaG) {
+            kern = dense_tma_kernel<PT, VE, true>;
             threads = kTmaThreads;
         }
     }
@@ -1979,12 +2076,23 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE || rq.mode == MODE_POLICY_VALUE ||
                          rq.mode == MODE_SHARD_EVAL || rq.mode == MODE_SHARD_IMPROVE;
     const int64_t n_pad = (n + 3) & ~int64_t(3);
-    const size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
-    if (smem_v + 12288 > pr.smem_optin) {
-        set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
-                  " B of shared memory for V (limit " + std::to_string(pr.smem_optin) +
-                  "); column panels for larger dense n are not in this build");
-        return RMB_ERR_UNSUPPORTED;
+    size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
+    static const bool tma_env = [] {
+        const char* e = getenv("RMB_DENSE_TMA");
+        return !(e && e[0] == '0');
+    }();
+    // a shared-memory copy of V (and pi) plus a 2-stage ring must fit; else V
+    // and pi stay in global memory (L2-resident) on the TMA path
+    const bool vglob = pr.vglobal || smem_v + 12288 + 2 * 33000 > pr.smem_optin;
+    if (vglob) {
+        if (!(tma_env && !pr.no_tma && VE * psz == 16)) {
+            set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
+                      " B of shared memory for V (limit " + std::to_string(pr.smem_optin) +
+                      "); larger n needs the TMA path (16-byte aligned rows: n % " + std::to_string(16 / psz) +
+                      " == 0, RMB_DENSE_NO_TMA unset)");
+            return RMB_ERR_UNSUPPORTED;
+        }
+        smem_v = 0;
     }
     DenseArgs& a = L.a;
     a = DenseArgs{};
@@ -1995,7 +2103,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.c = static_cast<const char*>(pr.c) - (size_t)row0 * pr.A * psz;
     a.row0 = row0;
     a.row1 = row1;
-    a.vs_half = VE == 4 ? n_pad / 2 : 0;
+    a.vs_half = (VE == 4 && !vglob) ? n_pad / 2 : 0;
     a.n = n;
     a.A = pr.A;
     a.gamma = pr.gamma;
@@ -2066,10 +2174,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     // to V / pi / the reduction scratch.  Chosen from (n, A, dtype, need_pi),
     // never from the shard, so every state's arithmetic is the same for any G.
     {
-        static const bool tma_on = [] {
-            const char* e = getenv("RMB_DENSE_TMA");
-            return !(e && e[0] == '0');
-        }();
+        const bool tma_on = tma_env;
         const int64_t qs_tma = std::min<int64_t>(a.qs_cap, std::max<int64_t>(512, pr.A));  // >= A for the S-mode combine
         const size_t ring_off = (smem_v + (size_t)std::max<int64_t>(qs_tma, 0) * 8 + 127) / 128 * 128;
         const int64_t room = (int64_t)pr.smem_optin - (int64_t)ring_off - 16 - 2048;  // static smem
@@ -2082,7 +2187,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
         a.tma_hint = 1;
         if (const char* e = getenv("RMB_TMA_HINT")) a.tma_hint = atoi(e);
         if (tma_on && !pr.no_tma && a.path == kPathWarp && VE * psz == 16 && nst >= 2 && qs_tma >= pr.A) {
-            a.path = kPathTma;
+            a.path = vglob ? kPathTmaG : kPathTma;
             a.qs_cap = qs_tma;
             a.tma_off = (int64_t)ring_off;
             a.tma_nst = nst;
@@ -2126,6 +2231,10 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
             }
         }
     }
+    if (vglob && a.path != kPathTmaG) {
+        set_error("dense solver: n = " + std::to_string(n) + " needs the global-V TMA path (disable RMB_DENSE_ROWS/CTA)");
+        return RMB_ERR_UNSUPPORTED;
+    }
     const int64_t stride = std::max<int64_t>({plan_doubles(a.plan[0], rq.b, NAG, pr.A),
                                               plan_doubles(a.plan[1], rq.b, 1, 1),
                                               plan_doubles(a.plan[2], a.imp_sub, NAG4, pr.A), 2 * rq.b,
@@ -2151,6 +2260,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.out = reinterpret_cast<long long*>(ctrl + 128);      // [128..136)
     a.prof = reinterpret_cast<long long*>(ctrl + 192);     // [192..196)
     a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256);  // [256]
+    a.gred = ctrl + 320;                                   // [320..336): global-V grid reductions
     a.pctr = reinterpret_cast<unsigned int*>(ctrl + 260);  // [260]
     {
         const char* e = getenv("RMB_PREFETCH_MB");

@@ -98,6 +98,7 @@ struct Problem {
     int32_t* stage_pi = nullptr;  //                 this rank's pi (owned entries meaningful)
     int ell_K = 0;  // > 0: fixed-stride rows (ELL)
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
+    bool vglobal = false; // dense: RMB_DENSE_VGLOBAL (V and pi in global memory)
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 0;

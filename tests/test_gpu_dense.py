@@ -327,3 +327,61 @@ def test_tma_path_mpi_matches_oracle(b, msweeps):
     assert sol.stats.outer_iters == ref.outer
     assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
     assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
+
+
+# ------------------------------------- global-V TMA mode (large dense n)
+@pytest.mark.parametrize("n,A,b,dtype", [(600, 16, 64, np.float32), (1000, 6, 1, np.float32),
+                                         (2048, 16, 2048, np.float32), (512, 5, 37, np.float64),
+                                         (4096, 40, 500, np.float32)])
+def test_global_v_mode_matches_oracle(n, A, b, dtype):
+    """RMB_DENSE_VGLOBAL: V and pi read from L2 by the compute warps, each state
+    finished and written by one CTA, grid-reduced residual — the mode large n
+    (V > shared memory) takes automatically.  Same sweeps, trace, V, pi."""
+    m, _, P, c = make(n, A, seed=41 + n, dtype=dtype, gamma=0.95)
+    prob = rmb.Problem.dense(tdev(P), tdev(c), 0.95, vglobal=True)
+    sol = prob.vi(b, seed=5, eps=1e-8, max_sweeps=400)
+    ref = oracle.vi(m, b, seed=5, eps=1e-8, max_sweeps=400)
+    assert sol.stats.sweeps == ref.sweeps
+    assert_close(sol.trace, ref.trace, 1e-9)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    mask = qgap(m, ref.V) > 1e-6
+    assert np.array_equal(sol.pi.cpu().numpy()[mask], ref.pi[mask])
+
+
+@pytest.mark.parametrize("b,msweeps", [(1, 2), (100, 5), (1024, 3)])
+def test_global_v_mode_mpi_matches_oracle(b, msweeps):
+    n, A = 1024, 8
+    m, _, P, c = make(n, A, seed=78, dtype=np.float32, gamma=0.95)
+    prob = rmb.Problem.dense(tdev(P), tdev(c), 0.95, vglobal=True)
+    sol = prob.mpi(b, msweeps, seed=2, eps=1e-7, max_outer=200)
+    ref = oracle.mpi(m, b, msweeps, seed=2, eps=1e-7, max_outer=200)
+    assert sol.stats.outer_iters == ref.outer
+    assert np.array_equal(sol.changed, ref.changed)
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("b", [1, 1000, 30_000])
+def test_large_n_dense_sampled(b):
+    """n = 30 000 > the shared-memory V limit (|A| = 2, fp32 P 7.2 GB generated
+    on device): one application in the automatic global-V mode, 48 sampled
+    states recomputed by the oracle from host-generated rows."""
+    n, A, gamma = 30_000, 2, 0.99
+    P, c = rmb.generate_dense(n, A, 3)
+    prob = rmb.Problem.dense(P, c, gamma)
+    V0 = np.random.default_rng(1).random(n) * 50
+    V1, arg, r = prob.apply(b, 9, 2, tdev(V0))
+    V1 = V1.cpu().numpy()
+    arg = arg.cpu().numpy()
+    perm = oracle.partition(n, 9, 2)
+    pos = np.empty(n, np.int64)
+    pos[perm] = np.arange(n)
+    for s in np.random.default_rng(b).choice(n, 48, replace=False):
+        earlier = (pos // b) < pos[s] // b
+        Vint = np.where(earlier, V1, V0)
+        Ph, ch = gen.dense(n, A, 3, rows=(s, s + 1))
+        q, a = oracle.backup_dense_row(Ph[0], ch[0], gamma, Vint)
+        assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
+        assert arg[s] == a
+    assert r == pytest.approx(np.abs(V1 - V0).max(), abs=0)
