@@ -194,6 +194,25 @@ def other_configs(rmb, torch, dev):
                 "time_to_eps_ms": st.seconds * 1e3, "backups_per_s": backups / st.seconds})
     del prob, rp, col, val, c
     torch.cuda.empty_cache()
+    # config 5's per-GPU working set on one GPU: dense n = 50 000 (V > shared
+    # memory -> the TMA path's global-V mode), |A| = 4 fp32 = 40 GB = one rank's
+    # 6250 x 32 x 50 000 share; MB-MPI m = 10, b = n/8 (config 5's batch)
+    n, A = 50_000, 4
+    P, c = rmb.generate_dense(n, A, 5)
+    prob = rmb.Problem.dense(P, c, 0.99)
+    prob.vi(n // 8, seed=0, eps=1e-6, max_sweeps=2)
+    sol = prob.vi(n // 8, seed=1, eps=1e-6, max_sweeps=10)
+    st = sol.stats
+    bps = n * A * n * 4 + n * A * 4 + 16 * n + 4 * n
+    mp = prob.mpi(n // 8, 10, seed=1, eps=1e-6, max_outer=3)
+    out.append({"workload": "config 5 per-GPU share on 1 GPU: dense |S|=50000 |A|=4 fp32 (40 GB), gamma=0.99, "
+                            "global-V TMA mode; MB-VI b=n/8 10 sweeps, MB-MPI m=10 b=n/8 3 outer iterations",
+                "vi_ms_per_sweep": st.seconds / st.sweeps * 1e3, "vi_GB_per_s": st.sweeps * bps / st.seconds / 1e9,
+                "vi_backups_per_s": st.sweeps * n * A / st.seconds,
+                "mpi_ms_per_outer": mp.stats.seconds / max(1, mp.stats.outer_iters) * 1e3,
+                "mpi_eval_sweeps": mp.stats.sweeps})
+    del prob, P, c
+    torch.cuda.empty_cache()
     return out
 
 
