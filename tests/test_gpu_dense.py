@@ -385,3 +385,27 @@ def test_large_n_dense_sampled(b):
         assert abs(V1[s] - q) <= 1e-11 * max(1.0, abs(q))
         assert arg[s] == a
     assert r == pytest.approx(np.abs(V1 - V0).max(), abs=0)
+
+
+# ------------------------------ certificate of the returned policy (NEXT #2)
+@pytest.mark.parametrize("b", [1, 60, 600])
+def test_returned_policy_optimality_gap_certificate(b):
+    """evaluate the pi returned by MB-VI exactly on the GPU
+    (rmb_policy_value, B_{pi,b} to 1e-12) and certify it.  With r_K the last
+    residual, ||V_K - J*|| <= a r_K / (1 - a) (reading R6, contraction), and a
+    policy greedy w.r.t. V_K satisfies ||J_pi - J*|| <= 2 a ||V_K - J*|| / (1 - a)
+    (the standard greedy-policy bound behind P:L99).  J* and J_pi also come
+    from the oracle's linear solves (Eq. 4) for the comparison."""
+    n, A, gamma = 600, 16, 0.95
+    m, prob, P, c = make(n, A, seed=90, dtype=np.float32, gamma=gamma)
+    sol = prob.vi(b, seed=7, eps=1e-4)
+    rK = float(sol.trace[-1])
+    pi = sol.pi.clone()
+    Jpi = prob.policy_value(pi, b=b, seed=3, eps=1e-12).V.cpu().numpy()
+    Jpi_or = oracle.policy_value(m, pi.cpu().numpy())
+    assert_close(Jpi, Jpi_or, 1e-9)
+    Jstar, _ = oracle.policy_iteration(m)  # exact J* (finite PI, linear solves)
+    dV = np.abs(sol.V.cpu().numpy() - Jstar).max()
+    assert dV <= gamma * rK / (1 - gamma) * (1 + 1e-9) + 1e-12
+    gap = np.abs(Jpi - Jstar).max()
+    assert gap <= 2 * gamma * dV / (1 - gamma) + 1e-9
