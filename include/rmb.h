@@ -168,9 +168,11 @@ rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellma
  * trace are bitwise identical for any number of ranks.
  * A shard handle is created with desc.row_begin/row_end from rmb_shard_range
  * and P / c pointing at the owned rows only ([row_end-row_begin][A][n] and
- * [row_end-row_begin][A]); V and pi are full-length on every rank (pi entries
- * outside the owned range are unspecified on return).  Dense MDPs only in
- * this build.
+ * [row_end-row_begin][A]) -- for rmb_create_csr: row_ptr [(row_end-row_begin)*A+1]
+ * starting at 0, col holding GLOBAL successor ids, val/c the owned rows; V and
+ * pi are full-length on every rank (pi entries outside the owned range are
+ * unspecified on return).  Dense and sparse (CSR/ELL) MDPs; all ranks of one
+ * solve use the same storage.
  * ------------------------------------------------------------------------ */
 
 /* Owned rows of rank g of G: [begin, end) = [g*ceil(n/G), (g+1)*ceil(n/G)) ∩ [0,n). */

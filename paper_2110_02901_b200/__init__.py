@@ -209,9 +209,13 @@ class Problem:
         return cls(h, n, A, float(gamma), (P, c))
 
     @classmethod
-    def csr(cls, n, A, row_ptr, col, val, c, gamma, stream=None, validate=False):
-        """CSR over rows r = s*A + a: row_ptr int64 [n*A+1], col int32, val float."""
-        d = _Desc(n, A, float(gamma), _dtype_code(val), F64, 0, n, None, _stream_ptr(stream))
+    def csr(cls, n, A, row_ptr, col, val, c, gamma, stream=None, validate=False, row_range=None, nccl_comm=None):
+        """CSR over rows r = s*A + a: row_ptr int64 [n*A+1], col int32, val float.
+        Shard handle (multi-GPU): row_range = (r0, r1) from shard_range(), row_ptr
+        [(r1-r0)*A+1] from 0 over the owned rows, col GLOBAL successor ids, c [r1-r0][A];
+        nccl_comm as for dense()."""
+        r0, r1 = row_range if row_range is not None else (0, n)
+        d = _Desc(n, A, float(gamma), _dtype_code(val), F64, r0, r1, nccl_comm, _stream_ptr(stream))
         h = ctypes.c_void_p()
         _check(lib().rmb_create_csr(ctypes.byref(d), _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(c),
                                     VALIDATE if validate else 0, ctypes.byref(h)))

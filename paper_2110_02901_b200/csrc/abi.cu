@@ -268,12 +268,10 @@ rmb_status rmb_create_csr(const rmb_desc* desc, const int64_t* row_ptr, const in
     rmb_status s = check_desc(desc);
     if (s != RMB_OK) return s;
     if (!row_ptr || !col || !val || !c) return fail(RMB_ERR_INVALID_ARG, "row_ptr, col, val or c is NULL");
-    if (desc->row_begin != 0 || desc->row_end != desc->n_states || desc->nccl_comm)
-        return fail(RMB_ERR_UNSUPPORTED, "sharded (multi-GPU) solves cover dense MDPs in this build");
     Problem* pr = new Problem();
     s = init_problem(*pr, desc);
     pr->dense = false;
-    const int64_t rows = pr->n * pr->A;
+    const int64_t rows = (desc->row_end - desc->row_begin) * (int64_t)desc->n_actions;  // owned rows
     const size_t psz = desc->p_dtype == RMB_F32 ? 4 : 8;
     // row_ptr is inspected on the host (nnz, fixed stride -> ELL)
     std::vector<int64_t> rp;
@@ -470,7 +468,7 @@ static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint3
         const Problem& p0 = *rk[0];
         int64_t b0, b1;
         rmb_shard_range(p0.n, G, g, &b0, &b1);
-        if (p.n != p0.n || p.A != p0.A || p.gamma != p0.gamma || p.pdt != p0.pdt || !p.dense || p.nccl_comm ||
+        if (p.n != p0.n || p.A != p0.A || p.gamma != p0.gamma || p.pdt != p0.pdt || p.dense != p0.dense || p.nccl_comm ||
             p.row_begin != b0 || p.row_end != b1 || p.stream != p0.stream)
             return fail(RMB_ERR_INVALID_ARG, "group handles must share n, A, gamma, dtype, stream and own the "
                                              "rmb_shard_range(n, G, g) rows in rank order");

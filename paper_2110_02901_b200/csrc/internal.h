@@ -122,6 +122,9 @@ rmb_status sharded_solve(Problem** ranks, int G, bool nccl, const SolveRequest& 
 // sparse.cu
 rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                         long long* chg_dev, int64_t chg_len, SolveResult* res);
+rmb_status sparse_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t* olist, const int* ocount,
+                             double* send_val, uint32_t* send_idx, int32_t* send_arg, cudaStream_t st,
+                             long long** out_dev);
 // gen_kernels.cu
 cudaError_t launch_partition(int64_t n, uint64_t seed, int64_t sweep, bool identity, uint32_t* perm,
                              cudaStream_t st);

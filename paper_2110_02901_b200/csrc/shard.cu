@@ -169,10 +169,13 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         ncclResult_t r = nccl().CommCount(comm, &G);
         if (r != ncclSuccess) return nccl_fail(r, "ncclCommCount");
     }
-    if (!p0.dense) {
-        set_error("sharded solves cover dense MDPs in this build");
-        return RMB_ERR_UNSUPPORTED;
-    }
+    for (int r = 0; r < G_local; ++r)
+        if (ranks[r]->dense != p0.dense) {
+            set_error("sharded solve: every rank's handle must have the same storage (dense or CSR)");
+            return RMB_ERR_INVALID_ARG;
+        }
+    // the per-rank step: dense (TMA/warp kernels in MODE_SHARD_*) or sparse
+    auto shard_step = p0.dense ? dense_shard_step : sparse_shard_step;
     // capacity: the largest owned range (identical on every rank: ranges from
     // rmb_shard_range, i.e. ceil(n / G))
     const int64_t max_rows = (n + G - 1) / G;
@@ -248,7 +251,7 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
                 rq.mode = eval ? MODE_SHARD_EVAL : MODE_SHARD_MIN;
                 rq.V = ranks[r]->stage_V;
                 rq.pi = ranks[r]->stage_pi;
-                rmb_status s = dense_shard_step(pr, rq, w.olist, w.ocount,
+                rmb_status s = shard_step(pr, rq, w.olist, w.ocount,
                                                 reinterpret_cast<double*>(w.send + rec.off_val()),
                                                 reinterpret_cast<uint32_t*>(w.send + rec.off_idx()),
                                                 reinterpret_cast<int32_t*>(w.send + rec.off_arg()), st, nullptr);
@@ -296,7 +299,7 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
             rq.mode = MODE_SHARD_IMPROVE;
             rq.V = ranks[r]->stage_V;
             rq.pi = ranks[r]->stage_pi;
-            rmb_status s = dense_shard_step(*ranks[r], rq, nullptr, nullptr, nullptr, nullptr, nullptr, st, &outs[r]);
+            rmb_status s = shard_step(*ranks[r], rq, nullptr, nullptr, nullptr, nullptr, nullptr, st, &outs[r]);
             if (s != RMB_OK) return s;
             ++launches;
             // record: residual bits, changed, status

@@ -554,6 +554,32 @@ static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(SThreads<MODE>::v), args, 0, st);
 }
 
+// Layout of the sparse backup (mode, lanes per state) chosen from the CSR
+// shape; shared by the persistent solver and the shard step so that a state's
+// arithmetic is the same on one GPU and on G.
+static void sparse_layout(const Problem& pr, int& mode, int& GS, int& GSE)
+{
+    const int64_t rows = (pr.row_end - pr.row_begin) * (int64_t)pr.A;
+    const double avg = rows > 0 ? (double)pr.nnz / (double)rows : 1.0;
+    const int64_t AK = (int64_t)pr.A * pr.ell_K;
+    const bool aligned = ((uintptr_t)pr.col % 16 == 0) && ((uintptr_t)pr.val % 16 == 0);
+    mode = SM_STRIDED;
+    GS = 1, GSE = 1;
+    if (pr.ell_K > 0 && pr.ell_K % 8 == 0 && aligned && AK / 8 <= 32 && ((AK / 8) & (AK / 8 - 1)) == 0 &&
+        ((pr.ell_K / 8) & (pr.ell_K / 8 - 1)) == 0) {
+        mode = SM_VEC;
+        GS = (int)(AK / 8);
+        GSE = pr.ell_K / 8;
+    } else if (pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32) {
+        mode = SM_ROW;
+        while (GS < pr.A) GS <<= 1;
+        GSE = 1;  // B_{pi,b}: one row per state -> a lane per state
+    } else {
+        while (GS < 32 && GS < avg) GS <<= 1;
+        GSE = GS;
+    }
+}
+
 rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                         long long* chg_dev, int64_t chg_len, SolveResult* res)
 {
@@ -578,26 +604,8 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
-    const double avg = pr.n * pr.A > 0 ? (double)pr.nnz / (double)(pr.n * pr.A) : 1.0;
-    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
-    const int64_t AK = (int64_t)pr.A * pr.ell_K;
-    const bool aligned = ((uintptr_t)pr.col % 16 == 0) && ((uintptr_t)pr.val % 16 == 0);
-    int mode = SM_STRIDED;
-    int GS = 1, GSE = 1;
-    if (pr.ell_K > 0 && pr.ell_K % 8 == 0 && aligned && AK / 8 <= 32 && ((AK / 8) & (AK / 8 - 1)) == 0 &&
-        ((pr.ell_K / 8) & (pr.ell_K / 8 - 1)) == 0) {
-        mode = SM_VEC;
-        GS = (int)(AK / 8);
-        GSE = pr.ell_K / 8;
-    } else if (pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32) {
-        mode = SM_ROW;
-        while (GS < pr.A) GS <<= 1;
-        GSE = 1;  // B_{pi,b}: one row per state -> a lane per state
-    } else {
-        while (GS < 32 && GS < avg) GS <<= 1;
-        GSE = GS;
-    }
-    (void)psz;
+    int mode, GS, GSE;
+    sparse_layout(pr, mode, GS, GSE);
     a.GS = GS;
     a.GSE = GSE;
 
@@ -670,6 +678,137 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     res->launches = 1;
     for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
     pr.last_launches = 1;
+    return RMB_OK;
+}
+
+// ------------------------------------------------------------ shard step
+// One launch of the multi-GPU protocol (shard.cu) on a sparse
+// shard handle: CSR/ELL rows of the owned states [row0, row0+nloc) with
+// global successor ids, backed up against this rank's replica Vr of the
+// interim V (Eq. 12: the replica holds every earlier batch's
+// committed values).  MIN / EVAL: the states of olist[0..*ocount) -> send
+// record (value, state, argmin).  IMPROVE: greedy over the owned states,
+// ||TV - V|| and #changed into out[] (pi updated in place, owned entries).
+// Per-state arithmetic is backup_state<PT, MODE>, the single-GPU one.
+template <typename PT, int MODE, int SMODE>
+__global__ void __launch_bounds__(256) sparse_shard_kernel(SparseArgs a, int64_t row0, int64_t nloc, const double* Vr,
+                                                           int32_t* pir, const uint32_t* olist, const int* ocount,
+                                                           double* send_val, uint32_t* send_idx, int32_t* send_arg,
+                                                           long long* out)
+{
+    constexpr bool EVAL = SMODE == MODE_SHARD_EVAL;
+    const int GS = EVAL ? a.GSE : a.GS;
+    const int g = threadIdx.x & (GS - 1);
+    const int64_t ngroups = (int64_t)gridDim.x * ((int)blockDim.x / GS);
+    const int64_t gid = (int64_t)blockIdx.x * ((int)blockDim.x / GS) + threadIdx.x / GS;
+    const int64_t wfirst = gid - (threadIdx.x & 31) / GS;
+    const int64_t cnt = SMODE == MODE_SHARD_IMPROVE ? nloc : (int64_t)*ocount;
+    double rmax = 0.0;
+    int bad = 0;
+    long long changed = 0;
+    for (int64_t w0 = wfirst; w0 < cnt; w0 += ngroups) {
+        const int64_t i = w0 + (gid - wfirst);
+        const bool valid = i < cnt;
+        const int64_t s = !valid ? row0 : SMODE == MODE_SHARD_IMPROVE ? row0 + i : (int64_t)olist[i];
+        double v;
+        int arg;
+        backup_state<PT, MODE>(a, Vr, s - row0, EVAL && valid ? pir[s] : (EVAL ? 0 : -1), g, GS, valid, v, arg);
+        if (valid && g == 0) {
+            if (SMODE == MODE_SHARD_IMPROVE) {
+                rmax = fmax(rmax, fabs(v - Vr[s]));
+                bad |= !isfinite(v);
+                changed += (arg != pir[s]);
+                pir[s] = arg;
+            } else {
+                send_val[i] = v;
+                send_idx[i] = (uint32_t)s;
+                send_arg[i] = EVAL ? pir[s] : arg;
+            }
+        }
+    }
+    if (SMODE != MODE_SHARD_IMPROVE) return;
+    __shared__ double sd[8];
+    __shared__ int si[8];
+    __shared__ long long sl[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        changed += __shfl_xor_sync(0xffffffffu, changed, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sd[w] = rmax, si[w] = bad, sl[w] = changed;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        int bb = 0;
+        long long cc = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r = fmax(r, sd[k]), bb |= si[k], cc += sl[k];
+        atomicMax(reinterpret_cast<unsigned long long*>(out + OUT_RESID_BITS), (unsigned long long)__double_as_longlong(r));
+        if (cc) atomicAdd(reinterpret_cast<unsigned long long*>(out + OUT_CHANGED), (unsigned long long)cc);
+        if (bb) atomicExch(reinterpret_cast<unsigned long long*>(out + OUT_STATUS), (unsigned long long)RMB_ERR_NONFINITE);
+    }
+}
+
+template <typename PT, int MODE>
+static cudaError_t launch_sparse_shard(const SparseArgs& a, int smode, int64_t row0, int64_t nloc, const double* Vr,
+                                       int32_t* pir, const uint32_t* olist, const int* ocount, double* sv,
+                                       uint32_t* si, int32_t* sa, long long* out, int grid, cudaStream_t st)
+{
+    if (smode == MODE_SHARD_MIN)
+        sparse_shard_kernel<PT, MODE, MODE_SHARD_MIN><<<grid, 256, 0, st>>>(a, row0, nloc, Vr, pir, olist, ocount, sv, si, sa, out);
+    else if (smode == MODE_SHARD_EVAL)
+        sparse_shard_kernel<PT, MODE, MODE_SHARD_EVAL><<<grid, 256, 0, st>>>(a, row0, nloc, Vr, pir, olist, ocount, sv, si, sa, out);
+    else
+        sparse_shard_kernel<PT, MODE, MODE_SHARD_IMPROVE><<<grid, 256, 0, st>>>(a, row0, nloc, Vr, pir, olist, ocount, sv, si, sa, out);
+    return cudaGetLastError();
+}
+
+rmb_status sparse_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t* olist, const int* ocount,
+                             double* send_val, uint32_t* send_idx, int32_t* send_arg, cudaStream_t st,
+                             long long** out_dev)
+{
+    SparseArgs a{};
+    a.row_ptr = pr.row_ptr;
+    a.col = pr.col;
+    a.val = pr.val;
+    a.c = pr.c;
+    a.n = pr.n;
+    a.A = pr.A;
+    a.K = pr.ell_K;
+    a.gamma = pr.gamma;
+    int mode;
+    sparse_layout(pr, mode, a.GS, a.GSE);
+    if (pr.ctrl.ensure(4096) != cudaSuccess) {
+        set_error("sparse shard step: workspace allocation failed");
+        return RMB_ERR_OOM;
+    }
+    long long* out = static_cast<long long*>(pr.ctrl.p);
+    const int64_t nloc = pr.row_end - pr.row_begin;
+    // work items: the batch's owned states (<= min(b, nloc)) or all owned states
+    const int64_t items = rq.mode == MODE_SHARD_IMPROVE ? nloc : std::min<int64_t>(rq.b, nloc);
+    const int GS = rq.mode == MODE_SHARD_EVAL ? a.GSE : a.GS;
+    const int64_t groups_per_cta = 256 / GS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + groups_per_cta - 1) / groups_per_cta,
+                                                                 (int64_t)pr.num_sms * 8));
+    cudaError_t ce = cudaSuccess;
+    if (rq.mode == MODE_SHARD_IMPROVE) ce = cudaMemsetAsync(out, 0, sizeof(long long) * OUT_N, st);
+    if (ce == cudaSuccess) {
+        const int sm = rq.mode;
+        if (pr.pdt == RMB_F32)
+            ce = mode == SM_VEC   ? launch_sparse_shard<float, SM_VEC>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st)
+                 : mode == SM_ROW ? launch_sparse_shard<float, SM_ROW>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st)
+                                  : launch_sparse_shard<float, SM_STRIDED>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st);
+        else
+            ce = mode == SM_VEC   ? launch_sparse_shard<double, SM_VEC>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st)
+                 : mode == SM_ROW ? launch_sparse_shard<double, SM_ROW>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st)
+                                  : launch_sparse_shard<double, SM_STRIDED>(a, sm, pr.row_begin, nloc, rq.V, rq.pi, olist, ocount, send_val, send_idx, send_arg, out, grid, st);
+    }
+    if (ce != cudaSuccess) {
+        set_error(std::string("sparse shard step: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    if (out_dev) *out_dev = out;
     return RMB_OK;
 }
 

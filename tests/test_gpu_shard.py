@@ -88,3 +88,83 @@ def test_nccl_single_rank_path():
         h.close()
     finally:
         rmb.nccl_comm_destroy(comm)
+
+
+# ------------------------------------------------------------- sparse shards
+def csr_shards(rp, col, val, c, n, A, gamma, G, comm=None):
+    """Owned-row slices of a CSR instance: row_ptr rebased to 0, col kept global."""
+    out = []
+    for g in range(G):
+        r0, r1 = rmb.shard_range(n, G, g)
+        e0, e1 = rp[r0 * A], rp[r1 * A]
+        out.append(rmb.Problem.csr(n, A, tdev(rp[r0 * A:r1 * A + 1] - e0), tdev(col[e0:e1]), tdev(val[e0:e1]),
+                                   tdev(c[r0:r1]), gamma, row_range=(r0, r1), nccl_comm=comm))
+    return out
+
+
+def ragged_csr(n, A, seed):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 41, n * A)
+    rp = np.zeros(n * A + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.random(rp[-1]) + 0.01
+    for r in range(n * A):
+        val[rp[r]:rp[r + 1]] /= val[rp[r]:rp[r + 1]].sum()
+    return rp, col, val, rng.random((n, A))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("kind", ["vec", "row", "strided"])
+def test_sparse_group_vi_is_bitwise_single_gpu(G, kind):
+    """Sparse shards (ELL vec mode, grid row mode, ragged CSR): V, pi, trace bitwise = one handle."""
+    if kind == "vec":
+        n, A, gamma, b = 600, 8, 0.99, 75
+        rp, col, val, c = gen.sparse(n, A, 32, 5, dtype=np.float32)
+    elif kind == "row":
+        N, A, gamma = 24, 4, 0.95
+        n, b = N * N, 100
+        rp, col, val, c = gen.grid(N, dtype=np.float32)
+    else:
+        n, A, gamma, b = 200, 3, 0.9, 31
+        rp, col, val, c = ragged_csr(n, A, 9)
+    ref = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma).vi(b, seed=3, eps=1e-8,
+                                                                                  max_sweeps=60)
+    sol = rmb.vi_group(csr_shards(rp, col, val, c, n, A, gamma, G), b, seed=3, eps=1e-8, max_sweeps=60)
+    assert sol.stats.sweeps == ref.stats.sweeps
+    assert np.array_equal(sol.trace, ref.trace)
+    assert np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi.cpu().numpy())
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sparse_group_mpi_matches_oracle_and_single(G):
+    """Config-4-shaped gridworld MPI (m = 5) over G sparse shards: bitwise = one handle; oracle parity."""
+    N, A, gamma, b, m = 20, 4, 0.95, 57, 5
+    n = N * N
+    rp, col, val, c = gen.grid(N, dtype=np.float32)
+    single = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma).mpi(b, m, seed=4, eps=1e-8)
+    sol = rmb.mpi_group(csr_shards(rp, col, val, c, n, A, gamma, G), b, m, seed=4, eps=1e-8)
+    assert sol.status == rmb.OK and sol.stats.outer_iters == single.stats.outer_iters
+    assert np.array_equal(sol.V.cpu().numpy(), single.V.cpu().numpy())
+    assert np.array_equal(sol.pi.cpu().numpy(), single.pi.cpu().numpy())
+    assert np.array_equal(sol.changed, single.changed)
+    ref = oracle.mpi(oracle.MDP(n, A, gamma, c, row_ptr=rp, col=col, val=val), b, m, seed=4, eps=1e-8)
+    assert np.abs(sol.V.cpu().numpy() - ref.V).max() <= 1e-9 * max(1, np.abs(ref.V).max())
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi)
+
+
+def test_sparse_nccl_single_rank_path():
+    """rmb_vi on a sparse shard handle with a real (1-rank) NCCL communicator (config-3 shape, small n)."""
+    n, A, gamma = 1000, 8, 0.99
+    rp, col, val, c = gen.sparse(n, A, 32, 2, dtype=np.float32)
+    comm = rmb.nccl_comm_init(1, 0, rmb.nccl_unique_id())
+    try:
+        (h,) = csr_shards(rp, col, val, c, n, A, gamma, 1, comm=comm)
+        sol = h.vi(n // 8, seed=1, eps=1e-7)
+        ref = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma).vi(n // 8, seed=1, eps=1e-7)
+        assert sol.status == rmb.OK and np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+        assert np.array_equal(sol.trace, ref.trace)
+        h.close()
+    finally:
+        rmb.nccl_comm_destroy(comm)

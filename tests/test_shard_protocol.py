@@ -25,10 +25,29 @@ import paper_2110_02901_b200 as rmb
 N, A, GAMMA, SEED, EPS = 37, 3, 0.9, 5, 1e-9
 
 
-def sharded_vi(rank, world, b, sweeps):
+K = 6  # successors per (s, a) of the sparse variant
+
+
+def backup_fn(kind, r0, r1):
+    """This rank's backup of a state s (owned rows only: dense rows, or CSR rows
+    generated for [r0, r1) with global successor ids)."""
+    if kind == "dense":
+        P, c = gen.dense(N, A, 11, dtype=np.float64)
+        Pl, cl = P[r0:r1], c[r0:r1]
+        return lambda s, V: oracle.backup_dense_row(Pl[s - r0], cl[s - r0], GAMMA, V)
+    rp, col, val, cl = gen.sparse(N, A, K, 11, dtype=np.float64, rows=(r0, r1))
+
+    def f(s, V):
+        q = s - r0
+        rows = rp[q * A:(q + 1) * A + 1]
+        return oracle.backup_csr_row(N, rows - rows[0], col[rows[0]:rows[-1]], val[rows[0]:rows[-1]], cl[q],
+                                     GAMMA, V)
+    return f
+
+
+def sharded_vi(rank, world, b, sweeps, kind="dense"):
     r0, r1 = rmb.shard_range(N, world, rank)
-    P, c = gen.dense(N, A, 11, dtype=np.float64)
-    Pl, cl = P[r0:r1], c[r0:r1]
+    backup = backup_fn(kind, r0, r1)
     cap = min(b, -(-N // world))
     V = np.zeros(N)
     pi = np.zeros(N, np.int32)
@@ -43,7 +62,7 @@ def sharded_vi(rank, world, b, sweeps):
             rec = torch.zeros(1 + 3 * cap, dtype=torch.float64)
             rec[0] = len(mine)
             for q, s in enumerate(mine):
-                v, a = oracle.backup_dense_row(Pl[s - r0], cl[s - r0], GAMMA, V)
+                v, a = backup(s, V)
                 rec[1 + q], rec[1 + cap + q], rec[1 + 2 * cap + q] = v, s, a
             recs = [torch.zeros_like(rec) for _ in range(world)]
             dist.all_gather(recs, rec)
@@ -60,12 +79,12 @@ def sharded_vi(rank, world, b, sweeps):
     return V, pi, np.array(trace), (r0, r1)
 
 
-def _worker(rank, world, port, b, sweeps, out):
+def _worker(rank, world, port, b, sweeps, out, kind):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        V, pi, tr, (r0, r1) = sharded_vi(rank, world, b, sweeps)
+        V, pi, tr, (r0, r1) = sharded_vi(rank, world, b, sweeps, kind)
         out[rank] = (V, pi[r0:r1], tr, r0, r1)
     finally:
         dist.destroy_process_group()
@@ -79,15 +98,21 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
 @pytest.mark.parametrize("b", [1, 4, 10, N])
-def test_two_rank_gloo_protocol_equals_oracle(b):
+def test_two_rank_gloo_protocol_equals_oracle(b, kind):
     world, sweeps = 2, 6
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_worker, args=(world, _free_port(), b, sweeps, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), b, sweeps, out, kind), nprocs=world, join=True)
         res = dict(out)
-    P, c = gen.dense(N, A, 11, dtype=np.float64)
-    ref = oracle.vi(oracle.MDP(N, A, GAMMA, c, P=P), b, seed=SEED, eps=1e-300, max_sweeps=sweeps)
+    if kind == "dense":
+        P, c = gen.dense(N, A, 11, dtype=np.float64)
+        m = oracle.MDP(N, A, GAMMA, c, P=P)
+    else:
+        rp, col, val, c = gen.sparse(N, A, K, 11, dtype=np.float64)
+        m = oracle.MDP(N, A, GAMMA, c, row_ptr=rp, col=col, val=val)
+    ref = oracle.vi(m, b, seed=SEED, eps=1e-300, max_sweeps=sweeps)
     pi = np.zeros(N, np.int32)
     for rank in range(world):
         V, pil, tr, r0, r1 = res[rank]
