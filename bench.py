@@ -240,6 +240,29 @@ def paper_envs(rmb, torch):
 
 
 # ------------------------------------------------------------------ GPU arm
+def sharded_config3(rmb, torch, dist, comm, world, rank, dev, sweeps=20):
+    """BASELINE config 3 on N GPUs: each rank generates and owns
+    its rmb_shard_range rows of the sparse 10^6 x 8 x 32 instance (col = global
+    ids), V replicated; MB-VI b = n/8 for a fixed number of sweeps (the
+    per-batch NCCL all-gather exchange).  Time = max over ranks of the device
+    time of the solve (events on the solve's stream, inside the library)."""
+    n, A, K = 1_000_000, 8, 32
+    rows = rmb.shard_range(n, world, rank)
+    rp, col, val, c = rmb.generate_sparse(n, A, K, 1, rows=rows)
+    prob = rmb.Problem.csr(n, A, rp, col, val, c, 0.99, row_range=rows, nccl_comm=comm)
+    prob.vi(n // 8, seed=0, eps=1e-300, max_sweeps=2)
+    sol = prob.vi(n // 8, seed=1, eps=1e-300, max_sweeps=sweeps)
+    t = torch.tensor([sol.stats.seconds], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = float(t[0])
+    del prob, rp, col, val, c
+    torch.cuda.empty_cache()
+    return {"workload": f"config 3 sharded over {world} GPUs: sparse random |S|=1e6 |A|=8 K=32 (ELL fp32), "
+                        f"gamma=0.99, MB-VI b=n/8, {sweeps} sweeps", "scaling": "strong",
+            "sweeps": sol.stats.sweeps, "ms_per_sweep": t / max(1, sol.stats.sweeps) * 1e3,
+            "backups_per_s": sol.stats.sweeps * n * A / t}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,6 +433,10 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_other:
         result["other_configs"] = other_configs(rmb, torch, dev)
+    if world > 1 and not args.no_other:
+        line = sharded_config3(rmb, torch, dist, comm, world, rank, dev)
+        if rank == 0:
+            result["other_configs"] = [line]
 
     if rank == 0 and world == 1 and not args.no_other:
         result["paper_envs"] = paper_envs(rmb, torch)

@@ -115,10 +115,13 @@ struct Rec {
 __global__ void copy_count_kernel(const int* ocount, char* send) { *reinterpret_cast<int*>(send) = *ocount; }
 
 // apply all ranks' updates to this rank's replica; residual / nonfinite
+// (max reduced per thread, then per warp: one atomic per warp, not per entry)
 __global__ void commit_kernel(double* V, int32_t* pi, int64_t row0, int64_t row1, const char* recv, int G, Rec rec,
                               unsigned long long* resid_bits, int* bad)
 {
     const int64_t total = (int64_t)G * rec.cap;
+    double rmax = 0.0;
+    int nonfin = 0;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(j / rec.cap);
         const int64_t q = j - (int64_t)r * rec.cap;
@@ -128,10 +131,22 @@ __global__ void commit_kernel(double* V, int32_t* pi, int64_t row0, int64_t row1
         const int64_t s = reinterpret_cast<const uint32_t*>(base + rec.off_idx())[q];
         const int arg = reinterpret_cast<const int32_t*>(base + rec.off_arg())[q];
         const double d = fabs(v - V[s]);
-        atomicMax(resid_bits, (unsigned long long)__double_as_longlong(d));
-        if (!isfinite(v)) atomicOr(bad, 1);
+        // NaN-propagating max (a NaN update also raises the nonfinite flag)
+        rmax = (d > rmax || d != d) ? d : rmax;
+        nonfin |= !isfinite(v);
         V[s] = v;
         if (pi && s >= row0 && s < row1) pi[s] = arg;
+    }
+    unsigned long long bits = (unsigned long long)__double_as_longlong(rmax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
+        bits = ob > bits ? ob : bits;  // non-negative doubles (and NaN) order as their bits
+        nonfin |= __shfl_xor_sync(0xffffffffu, nonfin, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bits) atomicMax(resid_bits, bits);
+        if (nonfin) atomicOr(bad, 1);
     }
 }
 
