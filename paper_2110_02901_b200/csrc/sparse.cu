@@ -45,6 +45,14 @@ template <int MODE>
 struct SThreads {
     static constexpr int v = 512;  // 1024 for row mode: config-4 VI 1.5x faster, config-4 MPI 1.7x slower
 };
+// Two register budgets per layout: MINB = 1 (one 512-thread CTA per SM, no
+// spills) and MINB = 2 (64 registers, two CTAs per SM: twice the gathers in
+// flight, a few spills off the hot loop, a grid barrier over 2x the CTAs).
+// Measured on B200 (tools/sparse_perf.py): MINB = 2 wins for B_b sweeps with
+// large batches (config 3 b = n/8: 1.53 -> 1.41 ms per sweep; config 4 VI
+// b = n: 0.60 -> 0.38 ms) and loses for small batches (barrier cost) and
+// MPI (config 4: 8.9 -> 12.7 s), so it is chosen per solve (sparse_solve).
+constexpr int64_t kSparseWideNnz = int64_t(1) << 24;  // nonzeros per batch from which MINB = 2 pays
 
 struct SparseArgs {
     const int64_t* row_ptr;
@@ -440,8 +448,8 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
     return r;
 }
 
-template <typename PT, int MODE>
-__global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(const SparseArgs a)
+template <typename PT, int MODE, int MINB>
+__global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(const SparseArgs a)
 {
     SCtx x{};
     x.g = GridBarrier{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err};
@@ -542,16 +550,23 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
     }
 }
 
-template <typename PT, int MODE>
-static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
+template <typename PT, int MODE, int MINB>
+static cudaError_t launch_sparse_minb(const SparseArgs& a, int grid, cudaStream_t st)
 {
-    auto kern = sparse_solver_kernel<PT, MODE>;
+    auto kern = sparse_solver_kernel<PT, MODE, MINB>;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SThreads<MODE>::v, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    if (grid > 1) grid *= std::min(per_sm, MINB);
     void* args[] = {const_cast<SparseArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(SThreads<MODE>::v), args, 0, st);
+}
+
+template <typename PT, int MODE>
+static cudaError_t launch_sparse(const SparseArgs& a, int grid, bool wide, cudaStream_t st)
+{
+    return wide ? launch_sparse_minb<PT, MODE, 2>(a, grid, st) : launch_sparse_minb<PT, MODE, 1>(a, grid, st);
 }
 
 // Layout of the sparse backup (mode, lanes per state) chosen from the CSR
@@ -643,15 +658,18 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(rq.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
     int grid = nnz_batch <= kSparseSmallBatchNnz ? 1 : pr.num_sms;
     if (const char* e = getenv("RMB_SPARSE_GRID")) grid = std::max(1, std::min(pr.num_sms, atoi(e)));
+    // two CTAs per SM for B_b sweeps over large batches (see kSparseWideNnz)
+    bool wide = grid > 1 && (rq.mode == MODE_VI || rq.mode == MODE_APPLY) && nnz_batch >= kSparseWideNnz;
+    if (const char* e = getenv("RMB_SPARSE_WIDE")) wide = grid > 1 && atoi(e) != 0;
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
-            ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, st)
-                 : mode == SM_ROW ? launch_sparse<float, SM_ROW>(a, grid, st)
-                                  : launch_sparse<float, SM_STRIDED>(a, grid, st);
+            ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, wide, st)
+                 : mode == SM_ROW ? launch_sparse<float, SM_ROW>(a, grid, wide, st)
+                                  : launch_sparse<float, SM_STRIDED>(a, grid, wide, st);
         else
-            ce = mode == SM_VEC   ? launch_sparse<double, SM_VEC>(a, grid, st)
-                 : mode == SM_ROW ? launch_sparse<double, SM_ROW>(a, grid, st)
-                                  : launch_sparse<double, SM_STRIDED>(a, grid, st);
+            ce = mode == SM_VEC   ? launch_sparse<double, SM_VEC>(a, grid, wide, st)
+                 : mode == SM_ROW ? launch_sparse<double, SM_ROW>(a, grid, wide, st)
+                                  : launch_sparse<double, SM_STRIDED>(a, grid, wide, st);
     }
     if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
     long long out[OUT_N + 4] = {0};

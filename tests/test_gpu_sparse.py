@@ -199,3 +199,24 @@ def test_policy_value_on_grid():
     for k in range(1, 6):
         V, _, ro = oracle.sweep(m, V, 37, oracle.partition(m.n, 2, k), pi)
         assert abs(sol.trace[k - 1] - ro) <= 1e-11 * max(1.0, np.abs(V).max())
+
+
+@pytest.mark.parametrize("name", ["ell32", "grid", "ragged"])
+@pytest.mark.parametrize("b", [1, 37, None])
+def test_two_ctas_per_sm_variant_is_bitwise_default(name, b, monkeypatch):
+    """The MINB = 2 build of the persistent solver (2 CTAs/SM, chosen for large
+    batches) forced at small sizes: V, pi and trace bitwise = the MINB = 1 build
+    (grid-free per-state arithmetic), and the oracle within the solve bar."""
+    m, prob = INSTANCES[name]()
+    b = m.n if b is None else b
+    monkeypatch.setenv("RMB_SPARSE_GRID", "148")  # full grid even for tiny batches
+    monkeypatch.setenv("RMB_SPARSE_WIDE", "0")
+    one = prob.vi(b, seed=5, eps=1e-8, max_sweeps=40)
+    monkeypatch.setenv("RMB_SPARSE_WIDE", "1")
+    two = prob.vi(b, seed=5, eps=1e-8, max_sweeps=40)
+    assert one.stats.sweeps == two.stats.sweeps
+    assert np.array_equal(one.trace, two.trace)
+    assert np.array_equal(one.V.cpu().numpy(), two.V.cpu().numpy())
+    assert np.array_equal(one.pi.cpu().numpy(), two.pi.cpu().numpy())
+    ref = oracle.vi(m, b, seed=5, eps=1e-8, max_sweeps=40)
+    assert_close(two.V.cpu().numpy(), ref.V, 1e-9)
