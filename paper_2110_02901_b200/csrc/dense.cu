@@ -2046,12 +2046,20 @@ static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaS
             threads = kTmaThreads;
         }
     }
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // under stream capture (the sharded protocol's graph of a sweep) the
+    // attribute and occupancy were set / checked by the eager warm-up sweep
+    // with the same plan; these calls are not permitted while capturing
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(st, &cs);
     if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    if (cs == cudaStreamCaptureStatusNone) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    }
     void* args[] = {const_cast<DenseArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st);
 }

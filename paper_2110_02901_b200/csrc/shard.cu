@@ -21,6 +21,8 @@
 #include <dlfcn.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -242,24 +244,23 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
     cudaEventRecord(e0, st);
     int64_t launches = 0;
 
-    // one operator application (B_b if !eval, else B_{pi,b}) with sweep index k
-    auto sweep = [&](int64_t k, bool eval, double* r_out, bool* bad_out) -> rmb_status {
+    // the batch sequence of one operator application (B_b if !eval, else
+    // B_{pi,b}) against the partition already drawn into every rank's perm
+    auto enqueue_batches = [&](bool eval, cudaStream_t qs) -> rmb_status {
         for (int r = 0; r < G_local; ++r) {
             RankWs& w = ws[r];
-            cudaError_t e = launch_partition(n, rq0.seed, k, rq0.identity, w.perm, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(w.resid, 0, 8, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(w.bad, 0, sizeof(int), st);
-            if (rmb_status s = check(e, "shard partition"); s != RMB_OK) return s;
-            ++launches;
+            cudaError_t e = cudaMemsetAsync(w.resid, 0, 8, qs);
+            if (e == cudaSuccess) e = cudaMemsetAsync(w.bad, 0, sizeof(int), qs);
+            if (rmb_status s = check(e, "shard residual reset"); s != RMB_OK) return s;
         }
         for (int64_t lo = 0; lo < n; lo += rq0.b) {
             const int64_t cnt = std::min<int64_t>(rq0.b, n - lo);
             for (int r = 0; r < G_local; ++r) {
                 RankWs& w = ws[r];
                 Problem& pr = *w.pr;
-                cudaError_t e = cudaMemsetAsync(w.ocount, 0, sizeof(int), st);
+                cudaError_t e = cudaMemsetAsync(w.ocount, 0, sizeof(int), qs);
                 if (e != cudaSuccess) return check(e, "shard compact");
-                compact_owned_kernel<<<blocks_for(cnt), 256, 0, st>>>(w.perm, lo, cnt, pr.row_begin, pr.row_end, w.olist,
+                compact_owned_kernel<<<blocks_for(cnt), 256, 0, qs>>>(w.perm, lo, cnt, pr.row_begin, pr.row_end, w.olist,
                                                                        w.ocount);
                 if (rmb_status s = check(cudaGetLastError(), "shard compact"); s != RMB_OK) return s;
                 SolveRequest rq = rq0;
@@ -267,34 +268,116 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
                 rq.V = ranks[r]->stage_V;
                 rq.pi = ranks[r]->stage_pi;
                 rmb_status s = shard_step(pr, rq, w.olist, w.ocount,
-                                                reinterpret_cast<double*>(w.send + rec.off_val()),
-                                                reinterpret_cast<uint32_t*>(w.send + rec.off_idx()),
-                                                reinterpret_cast<int32_t*>(w.send + rec.off_arg()), st, nullptr);
+                                          reinterpret_cast<double*>(w.send + rec.off_val()),
+                                          reinterpret_cast<uint32_t*>(w.send + rec.off_idx()),
+                                          reinterpret_cast<int32_t*>(w.send + rec.off_arg()), qs, nullptr);
                 if (s != RMB_OK) return s;
-                copy_count_kernel<<<1, 1, 0, st>>>(w.ocount, w.send);
+                copy_count_kernel<<<1, 1, 0, qs>>>(w.ocount, w.send);
                 launches += 3;
             }
             if (use_nccl) {
-                ncclResult_t nr = nccl().AllGather(ws[0].send, ws[0].recv, rec.chunk, ncclUint8, comm, st);
+                ncclResult_t nr = nccl().AllGather(ws[0].send, ws[0].recv, rec.chunk, ncclUint8, comm, qs);
                 if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather");
             } else {
                 for (int r = 0; r < G_local; ++r)
                     for (int q = 0; q < G_local; ++q) {
                         cudaError_t e = cudaMemcpyAsync(ws[r].recv + (size_t)q * rec.chunk, ws[q].send, rec.chunk,
-                                                        cudaMemcpyDeviceToDevice, st);
+                                                        cudaMemcpyDeviceToDevice, qs);
                         if (e != cudaSuccess) return check(e, "logical exchange");
                     }
             }
             for (int r = 0; r < G_local; ++r) {
                 RankWs& w = ws[r];
                 Problem& pr = *w.pr;
-                commit_kernel<<<blocks_for((int64_t)G * rec.cap), 256, 0, st>>>(
+                commit_kernel<<<blocks_for((int64_t)G * rec.cap), 256, 0, qs>>>(
                     pr.stage_V, eval ? nullptr : pr.stage_pi, pr.row_begin, pr.row_end, w.recv, G, rec, w.resid, w.bad);
                 if (rmb_status s = check(cudaGetLastError(), "shard commit"); s != RMB_OK) return s;
                 ++launches;
             }
-            ++res->batches;
         }
+        return RMB_OK;
+    };
+
+    // CUDA graphs: the batch sequence of a sweep is the same stream work every
+    // sweep (only the perm contents change, drawn by the partition kernel
+    // launched before it), so after one eager sweep per kind (which also sizes
+    // every workspace: no allocation may happen under capture) it is captured
+    // once and replayed -- one host launch per sweep instead of ~5 per batch
+    // per rank.  Any capture failure falls back to the eager sequence (the
+    // same kernels).  RMB_SHARD_NO_GRAPH=1 disables.
+    const int64_t nbatches = (n + rq0.b - 1) / rq0.b;
+    bool graph_on = true;
+    if (const char* e = getenv("RMB_SHARD_NO_GRAPH")) graph_on = atoi(e) == 0;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t gkern[2] = {0, 0};
+    int warm[2] = {0, 0};
+    bool gfail[2] = {false, false};
+    struct GraphGuard {
+        cudaGraphExec_t* g;
+        ~GraphGuard()
+        {
+            for (int i = 0; i < 2; ++i)
+                if (g[i]) cudaGraphExecDestroy(g[i]);
+        }
+    } gguard{gexec};
+    // capture needs a stream other than the legacy default stream (which is
+    // what torch's current stream usually is): a private non-blocking stream
+    cudaStream_t gst = nullptr;
+    struct StreamGuard {
+        cudaStream_t* s;
+        ~StreamGuard()
+        {
+            if (*s) cudaStreamDestroy(*s);
+        }
+    } sguard{&gst};
+
+    auto run_batches = [&](bool eval) -> rmb_status {
+        const int kind = eval ? 1 : 0;
+        if (graph_on && !gfail[kind] && warm[kind] >= 1) {
+            if (!gexec[kind]) {
+                const int64_t l0 = launches;
+                cudaGraph_t g = nullptr;
+                cudaError_t e = gst ? cudaSuccess : cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking);
+                if (e == cudaSuccess) e = cudaStreamBeginCapture(gst, cudaStreamCaptureModeThreadLocal);
+                rmb_status s = e == cudaSuccess ? enqueue_batches(eval, gst) : RMB_ERR_CUDA;
+                cudaError_t e2 = e == cudaSuccess ? cudaStreamEndCapture(gst, &g) : e;
+                if (s == RMB_OK && e2 == cudaSuccess && g) e2 = cudaGraphInstantiate(&gexec[kind], g, 0);
+                if (g) cudaGraphDestroy(g);
+                gkern[kind] = launches - l0;
+                launches = l0;
+                if (s != RMB_OK || e2 != cudaSuccess || !gexec[kind]) {
+                    if (getenv("RMB_SHARD_GRAPH_DEBUG"))
+                        fprintf(stderr, "rmb shard graph capture failed (%s): %s\n", cudaGetErrorString(e2),
+                                s != RMB_OK ? rmb_last_error() : "");
+                    gfail[kind] = true;
+                    gexec[kind] = nullptr;
+                    cudaGetLastError();  // clear the capture error; run eagerly below
+                }
+            }
+            if (gexec[kind]) {
+                if (getenv("RMB_SHARD_GRAPH_DEBUG") && warm[kind] == 1) {
+                    fprintf(stderr, "rmb shard graph in use (%s, %lld kernels per sweep)\n", eval ? "eval" : "min",
+                            (long long)gkern[kind]);
+                    ++warm[kind];
+                }
+                if (rmb_status s = check(cudaGraphLaunch(gexec[kind], st), "shard graph launch"); s != RMB_OK) return s;
+                launches += gkern[kind];
+                return RMB_OK;
+            }
+        }
+        ++warm[kind];
+        return enqueue_batches(eval, st);
+    };
+
+    // one operator application (B_b if !eval, else B_{pi,b}) with sweep index k
+    auto sweep = [&](int64_t k, bool eval, double* r_out, bool* bad_out) -> rmb_status {
+        for (int r = 0; r < G_local; ++r) {
+            cudaError_t e = launch_partition(n, rq0.seed, k, rq0.identity, ws[r].perm, st);
+            if (rmb_status s = check(e, "shard partition"); s != RMB_OK) return s;
+            ++launches;
+        }
+        if (rmb_status s = run_batches(eval); s != RMB_OK) return s;
+        res->batches += nbatches;
         unsigned long long rb = 0;
         int bb = 0;
         cudaError_t e = cudaMemcpyAsync(&rb, ws[0].resid, 8, cudaMemcpyDeviceToHost, st);

@@ -168,3 +168,30 @@ def test_sparse_nccl_single_rank_path():
         h.close()
     finally:
         rmb.nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_graph_replayed_sweeps_equal_eager(sparse, monkeypatch):
+    """The sharded sweep's batch sequence replayed from a CUDA graph (default)
+    equals the eager launch sequence (RMB_SHARD_NO_GRAPH=1) bit for bit, VI and MPI."""
+    if sparse:
+        N, A, gamma = 16, 4, 0.95
+        n = N * N
+        rp, col, val, c = gen.grid(N, dtype=np.float32)
+        make = lambda: csr_shards(rp, col, val, c, n, A, gamma, 3)  # noqa: E731
+    else:
+        n, A, gamma = 240, 6, 0.95
+        P, c = gen.dense(n, A, 12, dtype=np.float32)
+        make = lambda: shards(P, c, gamma, 3)  # noqa: E731
+    b = 23
+    monkeypatch.setenv("RMB_SHARD_NO_GRAPH", "1")
+    ev = rmb.vi_group(make(), b, seed=6, eps=1e-9, max_sweeps=50)
+    em = rmb.mpi_group(make(), b, 4, seed=6, eps=1e-9)
+    monkeypatch.setenv("RMB_SHARD_NO_GRAPH", "0")
+    gv = rmb.vi_group(make(), b, seed=6, eps=1e-9, max_sweeps=50)
+    gm = rmb.mpi_group(make(), b, 4, seed=6, eps=1e-9)
+    for e, g in ((ev, gv), (em, gm)):
+        assert e.stats.sweeps == g.stats.sweeps and e.stats.batches == g.stats.batches
+        assert np.array_equal(e.trace, g.trace)
+        assert np.array_equal(e.V.cpu().numpy(), g.V.cpu().numpy())
+        assert np.array_equal(e.pi.cpu().numpy(), g.pi.cpu().numpy())
