@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(s) > os.path.getmtime(_SO) for s in src + [os.path.join(_HERE, "rmb_gen.h")]
     ):
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-o", _SO] + src
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fopenmp", "-o", _SO] + src
         )
     return _SO
 

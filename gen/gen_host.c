@@ -13,6 +13,10 @@ int gen_dense_rows(int kind, uint64_t seed, int64_t n, int32_t A, int64_t s0, in
                    int f32, void* P, void* c)
 {
     if (n <= 0 || A <= 0 || s0 < 0 || s1 > n || s0 > s1) return 1;
+    if (kind != RMBGEN_DENSE_RANDOM && kind != RMBGEN_DENSE_DYADIC) return 1;
+    /* rows are independent: threads over states (each row's content is a
+       function of (seed, s, a, j) only) */
+#pragma omp parallel for schedule(dynamic, 16)
     for (int64_t s = s0; s < s1; ++s) {
         for (int32_t a = 0; a < A; ++a) {
             size_t row = (size_t)((s - s0) * A + a);
@@ -33,8 +37,6 @@ int gen_dense_rows(int kind, uint64_t seed, int64_t n, int32_t A, int64_t s0, in
                     else ((double*)P)[row * (size_t)n + (size_t)j] = p;
                 }
                 cost = rmbgen_dyadic_cost(seed, s, a);
-            } else {
-                return 1;
             }
             if (f32) ((float*)c)[row] = (float)cost;
             else ((double*)c)[row] = cost;
@@ -49,6 +51,7 @@ int gen_sparse_rows(uint64_t seed, int64_t n, int32_t A, int32_t K, int64_t s0, 
                     int f32, int64_t* row_ptr, int32_t* col, void* val, void* c)
 {
     if (n <= 0 || A <= 0 || K <= 0 || K > n || s0 < 0 || s1 > n || s0 > s1) return 1;
+#pragma omp parallel for schedule(dynamic, 256)
     for (int64_t s = s0; s < s1; ++s) {
         for (int32_t a = 0; a < A; ++a) {
             size_t row = (size_t)((s - s0) * A + a);
@@ -78,6 +81,7 @@ int gen_grid_rows(int64_t N, int64_t s0, int64_t s1, int f32, int64_t* row_ptr, 
     const int32_t A = 4, K = RMBGEN_GRID_W;
     int64_t n = N * N;
     if (N <= 1 || s0 < 0 || s1 > n || s0 > s1) return 1;
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t s = s0; s < s1; ++s) {
         for (int32_t a = 0; a < A; ++a) {
             size_t row = (size_t)((s - s0) * A + a);

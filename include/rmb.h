@@ -80,6 +80,18 @@ typedef struct {
 #define RMB_DENSE_NO_TMA 0x10u  /* rmb_create_dense: stream P rows with per-warp register loads instead
                                    of the default TMA (cp.async.bulk) shared-memory ring; results agree
                                    to fp64 rounding (A/B measurement and cross-path tests)            */
+#define RMB_CHUNKED_T 0x40u     /* rmb_vi / rmb_apply: "VI*" of P:L570, L577 (Sec. IV-B) -- every sweep is
+                                   the Bellman operator T computed in chunks of b states (the batches of
+                                   the sweep's partition), each chunk "using the old values": all chunks
+                                   read the sweep-start V, the new values land at the end of the sweep.
+                                   One barrier per chunk, like B_b; the result is T V for any b, order
+                                   and chunking (DESIGN reading R21).  Not for sharded handles.        */
+/* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
+#define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
+#define RMB_SPARSE_WIDE_OFF 0x100u  /* sparse: one 512-thread CTA per SM for every solve           */
+#define RMB_SPARSE_WIDE_ON 0x200u   /* sparse: two CTAs per SM (64 registers) for B_b solves       */
+#define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly
+                                       instead of replaying it from a captured CUDA graph          */
 
 /* Create a handle over a DENSE MDP.
  *   P: [n][A][n] row-major, P[(s*A + a)*n + j] = p(j | s, a), dtype desc->p_dtype.
@@ -114,6 +126,7 @@ typedef struct {
 /* MB-VI: V <- V0 (V's content, or 0 with RMB_V0_ZERO); for sweeps
  * k = 1, 2, ...: draw the partition of sweep k (seed, k), apply B_b, record
  * r_k = ||V_k - V_{k-1}||_inf; stop at the first r_k <= eps.
+ *   flags: RMB_ORDER_IDENTITY, RMB_V0_ZERO, RMB_CHUNKED_T (VI*: T in chunks).
  *   b in [1, n]; eps > 0; max_sweeps >= 1.
  *   V: [n] float64 in/out.  pi: [n] int32 out (the argmin of each state's
  *   final-sweep backup).  trace: HOST [max_sweeps] or NULL (r_k, k = 1..).
@@ -140,7 +153,9 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
 /* One application of B_b (pi_or_null == NULL) or B_{pi,b} with the
  * partition of sweep number `sweep` (>= 1): V_out = B V_in.  V_in and V_out
  * may alias.  argmin_out ([n] int32, may be NULL) receives the argmin (or
- * pi).  resid_out (HOST, may be NULL) receives ||V_out - V_in||_inf. */
+ * pi).  resid_out (HOST, may be NULL) receives ||V_out - V_in||_inf.
+ * pi_or_null entries outside [0, A) return RMB_ERR_INVALID_ARG (checked on
+ * the device before the sweep).  flags: RMB_ORDER_IDENTITY, RMB_CHUNKED_T. */
 rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uint32_t flags,
                      const int32_t* pi_or_null, const void* V_in, void* V_out, int32_t* argmin_out,
                      double* resid_out);
@@ -229,6 +244,10 @@ rmb_status rmb_generate_grid(int64_t N, int64_t s0, int64_t s1, rmb_dtype dtype,
 /* Kernel launches issued by the last solve/apply/improve call on this handle
  * (evidence for bench.py's gpu_launches). */
 int64_t rmb_last_launch_count(rmb_problem h);
+
+/* Sharded solves: sweeps of the last solve replayed from a captured CUDA graph
+ * (0 when every sweep was launched eagerly). */
+int64_t rmb_last_graph_launches(rmb_problem h);
 
 /* Phase breakdown of the last solve as seen by CTA 0 of the persistent
  * kernel (globaltimer): ns4[0] compute (streaming P), ns4[1] waiting in grid

@@ -28,7 +28,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liboracle.so")
+# RMB_ORACLE_SO: a prebuilt alternative oracle (tools/mutation_check.py loads
+# deliberately broken builds to show that the pins catch each mutation)
+_SO = os.environ.get("RMB_ORACLE_SO") or os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 OK, INVALID_ARG, NOT_CONVERGED, NONFINITE, OOM = 0, 1, 3, 4, 7
@@ -36,10 +38,13 @@ OK, INVALID_ARG, NOT_CONVERGED, NONFINITE, OOM = 0, 1, 3, 4, 7
 
 def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
+    if os.environ.get("RMB_ORACLE_SO"):
+        return _SO
     if force or not os.path.exists(_SO) or os.path.getmtime(src) > os.path.getmtime(_SO):
         # -ffp-contract=off: no FMA contraction — every product and sum is
         # rounded exactly as written in oracle.c
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off",
+        # -fopenmp: optional worker threads across the states of one batch
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fopenmp",
                                "-o", _SO, src, "-lm"])
     return _SO
 
@@ -64,15 +69,18 @@ def _load():
         lib.orc_partition.argtypes = [i64, u64, i64, ctypes.c_int, vp]
         lib.orc_partition_inverse.argtypes = [i64, u64, i64, ctypes.c_int, vp]
         lib.orc_sweep.argtypes = [pm, i64, vp, vp, vp, vp, vp]
+        lib.orc_sweep_chunked.argtypes = [pm, i64, vp, vp, vp, vp, vp]
+        lib.orc_set_threads.argtypes, lib.orc_set_threads.restype = [ctypes.c_int], None
+        lib.orc_get_threads.argtypes, lib.orc_get_threads.restype = [], ctypes.c_int
         lib.orc_improve.argtypes = [pm, vp, vp, vp, vp]
-        lib.orc_vi.argtypes = [pm, i64, u64, ctypes.c_int, i64, dbl, i64, vp, vp, vp, vp]
+        lib.orc_vi.argtypes = [pm, i64, u64, ctypes.c_int, i64, dbl, i64, ctypes.c_int, vp, vp, vp, vp]
         lib.orc_mpi.argtypes = [pm, i64, i32, u64, ctypes.c_int, i64, dbl, i64, ctypes.c_int,
                                 vp, vp, vp, vp, vp, vp]
         lib.orc_backup_dense_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, i32, vp]
         lib.orc_backup_dense_row.restype = dbl
         lib.orc_backup_csr_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, vp, vp, i32, vp]
         lib.orc_backup_csr_row.restype = dbl
-        for f in (lib.orc_partition, lib.orc_partition_inverse, lib.orc_sweep, lib.orc_improve,
+        for f in (lib.orc_partition, lib.orc_partition_inverse, lib.orc_sweep, lib.orc_sweep_chunked, lib.orc_improve,
                   lib.orc_vi, lib.orc_mpi):
             f.restype = ctypes.c_int
         _lib = lib
@@ -130,6 +138,16 @@ class MDP:
         return P.reshape(self.n, self.A, self.n)
 
 
+def set_threads(w: int) -> None:
+    """Worker threads for the states of one batch / the improvement (results
+    are bitwise independent of w: every per-state row sum stays sequential)."""
+    _load().orc_set_threads(int(w))
+
+
+def get_threads() -> int:
+    return int(_load().orc_get_threads())
+
+
 # ---------------------------------------------------------------- partition
 def mix64(z: int) -> int:
     return int(_load().orc_mix64(z & (2**64 - 1)))
@@ -166,6 +184,20 @@ def sweep(m: MDP, V: np.ndarray, b: int, perm: np.ndarray, pi: np.ndarray | None
     return V, arg, r.value
 
 
+def sweep_chunked(m: MDP, V: np.ndarray, c: int, perm: np.ndarray, pi: np.ndarray | None = None):
+    """VI*'s operator: T (or T_pi) in chunks of c states against the
+    old values; returns (V', argmin, r)."""
+    V = np.array(V, dtype=np.float64, copy=True)
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    arg = np.zeros(m.n, dtype=np.int32)
+    pi_c = np.ascontiguousarray(pi, dtype=np.int32) if pi is not None else None
+    r = ctypes.c_double()
+    rc = _load().orc_sweep_chunked(ctypes.byref(m._s), c, _p(perm), _p(pi_c), _p(V), _p(arg), ctypes.byref(r))
+    if rc not in (OK, NONFINITE):
+        raise ValueError(f"sweep_chunked: status {rc}")
+    return V, arg, r.value
+
+
 def improve(m: MDP, V: np.ndarray, pi: np.ndarray):
     """Policy improvement: returns (pi', ||TV-V||_inf, changed)."""
     V = np.ascontiguousarray(V, dtype=np.float64)
@@ -189,14 +221,16 @@ class Result:
 
 
 def vi(m: MDP, b: int, seed: int = 0, eps: float = 1e-6, max_sweeps: int = 100000,
-       V0: np.ndarray | None = None, identity: bool = False, first_sweep: int = 1) -> Result:
-    """MB-VI (P:L186) to ||V_k - V_{k-1}||_inf <= eps."""
+       V0: np.ndarray | None = None, identity: bool = False, first_sweep: int = 1,
+       chunked: bool = False) -> Result:
+    """MB-VI (P:L186) to ||V_k - V_{k-1}||_inf <= eps; chunked=True: VI* (P:L577),
+    T in chunks of b states against the old values."""
     V = np.zeros(m.n) if V0 is None else np.array(V0, dtype=np.float64, copy=True)
     pi = np.zeros(m.n, dtype=np.int32)
     tr = np.zeros(max_sweeps)
     sw = ctypes.c_int64()
     st = _load().orc_vi(ctypes.byref(m._s), b, seed, int(identity), first_sweep, eps, max_sweeps,
-                        _p(V), _p(pi), _p(tr), ctypes.byref(sw))
+                        int(chunked), _p(V), _p(pi), _p(tr), ctypes.byref(sw))
     if st == INVALID_ARG:
         raise ValueError("vi: invalid argument")
     return Result(st, V, pi, tr[: sw.value], sw.value)

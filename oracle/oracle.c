@@ -12,7 +12,12 @@
  *     exactly to double on load);
  *   - every row sum is accumulated sequentially in storage order (dense: j
  *     ascending; CSR: row order), Q = c + gamma * sum;
- *   - no blocking, fusion, reordering or threads.
+ *   - no blocking, fusion or reordering.  Optional worker threads
+ *     (orc_set_threads, OpenMP) split the states of ONE batch (or of the
+ *     improvement) among workers; each state's backup is still one
+ *     sequential row sum written to its own slot, and every reduction
+ *     (residual max, changed count) stays a sequential loop afterwards,
+ *     so results are bitwise independent of the thread count.
  *
  * References are PAPER.md line numbers ("P:Lxxx") with the equation /
  * algorithm they fall in, and the DESIGN.md readings R1..R21 (= SURVEY
@@ -24,6 +29,7 @@
  * "Oracle pins".
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -34,6 +40,11 @@
 #define ORC_NOT_CONVERGED 3
 #define ORC_NONFINITE 4
 #define ORC_OOM 7
+
+/* Worker threads for the within-batch loops (1 = plain sequential). */
+static int orc_nthreads = 1;
+void orc_set_threads(int w) { orc_nthreads = w < 1 ? 1 : w; }
+int orc_get_threads(void) { return orc_nthreads; }
 
 /* ------------------------------------------------------------------ */
 /* MDP description (Sec. II-A: the tuple (S, U, P, g, alpha)).  */
@@ -212,7 +223,9 @@ int orc_sweep(const orc_mdp* m, int64_t b, const uint32_t* perm, const int32_t* 
     int nonfinite = 0;
     for (int64_t lo = 0; lo < m->n; lo += b) {
         int64_t hi = lo + b < m->n ? lo + b : m->n;
-        /* every state of the batch is backed up against the same interim V */
+        /* every state of the batch is backed up against the same interim V
+           (order-free within the batch: workers may share the loop) */
+#pragma omp parallel for schedule(static) num_threads(orc_nthreads) if (orc_nthreads > 1 && hi - lo > 1)
         for (int64_t p = lo; p < hi; ++p) {
             int64_t s = perm[p];
             if (pi_fixed) {
@@ -239,6 +252,49 @@ int orc_sweep(const orc_mdp* m, int64_t b, const uint32_t* perm, const int32_t* 
 }
 
 /* ------------------------------------------------------------------ */
+/* "VI*" of P:L570, L577 (Sec. IV-B): the Bellman operator T computed   */
+/* in chunks of c states "using the old values" -- the chunks are the   */
+/* batches of the partition, but every chunk reads the values V had at  */
+/* the start of the application; all new values are written at the end */
+/* (DESIGN reading R21).  pi_fixed != NULL: T_pi in chunks.             */
+/* ------------------------------------------------------------------ */
+int orc_sweep_chunked(const orc_mdp* m, int64_t c, const uint32_t* perm, const int32_t* pi_fixed,
+                      double* V, int32_t* pi_out, double* resid)
+{
+    if (!m || !perm || !V || c < 1 || c > m->n) return ORC_INVALID_ARG;
+    double* newv = (double*)malloc(sizeof(double) * (size_t)m->n);
+    int32_t* newa = (int32_t*)malloc(sizeof(int32_t) * (size_t)m->n);
+    if (!newv || !newa) { free(newv); free(newa); return ORC_OOM; }
+    for (int64_t lo = 0; lo < m->n; lo += c) {
+        int64_t hi = lo + c < m->n ? lo + c : m->n;
+        /* chunk [lo, hi) against the OLD values: V is not touched here */
+#pragma omp parallel for schedule(static) num_threads(orc_nthreads) if (orc_nthreads > 1 && hi - lo > 1)
+        for (int64_t p = lo; p < hi; ++p) {
+            int64_t s = perm[p];
+            if (pi_fixed) {
+                newa[s] = pi_fixed[s];
+                newv[s] = q_value(m, s, pi_fixed[s], V);
+            } else {
+                newv[s] = q_min(m, s, V, &newa[s]);
+            }
+        }
+    }
+    double r = 0.0;
+    int nonfinite = 0;
+    for (int64_t s = 0; s < m->n; ++s) {
+        double d = fabs(newv[s] - V[s]);
+        if (!isfinite(newv[s])) nonfinite = 1;
+        if (d > r) r = d;
+        V[s] = newv[s];
+        if (pi_out) pi_out[s] = newa[s];
+    }
+    free(newv);
+    free(newa);
+    if (resid) *resid = r;
+    return nonfinite ? ORC_NONFINITE : ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
 /* Policy improvement of Algorithm 1, all states, against  */
 /* V, no V write: pi'(s) = argmin_u Q(s,u) (lowest index on ties).      */
 /* bellman_resid = max_s |min_u Q(s,u) - V(s)| = ||TV - V||_inf.        */
@@ -247,18 +303,24 @@ int orc_sweep(const orc_mdp* m, int64_t b, const uint32_t* perm, const int32_t* 
 int orc_improve(const orc_mdp* m, const double* V, int32_t* pi, double* bellman_resid, int64_t* changed)
 {
     if (!m || !V || !pi) return ORC_INVALID_ARG;
+    double* q = (double*)malloc(sizeof(double) * (size_t)m->n);
+    int32_t* a = (int32_t*)malloc(sizeof(int32_t) * (size_t)m->n);
+    if (!q || !a) { free(q); free(a); return ORC_OOM; }
+    /* greedy action of every state against V (state-parallel, no writes to V) */
+#pragma omp parallel for schedule(static) num_threads(orc_nthreads) if (orc_nthreads > 1)
+    for (int64_t s = 0; s < m->n; ++s) q[s] = q_min(m, s, V, &a[s]);
     double r = 0.0;
     int64_t ch = 0;
     int nonfinite = 0;
     for (int64_t s = 0; s < m->n; ++s) {
-        int32_t a;
-        double q = q_min(m, s, V, &a);
-        if (!isfinite(q)) nonfinite = 1;
-        double d = fabs(q - V[s]);
+        if (!isfinite(q[s])) nonfinite = 1;
+        double d = fabs(q[s] - V[s]);
         if (d > r) r = d;
-        if (a != pi[s]) ++ch;
-        pi[s] = a;
+        if (a[s] != pi[s]) ++ch;
+        pi[s] = a[s];
     }
+    free(q);
+    free(a);
     if (bellman_resid) *bellman_resid = r;
     if (changed) *changed = ch;
     return nonfinite ? ORC_NONFINITE : ORC_OK;
@@ -270,9 +332,12 @@ int orc_improve(const orc_mdp* m, const double* V, int32_t* pi, double* bellman_
 /* partition of sweep k, apply B_b, record r_k; stop at the first r_k   */
 /* <= eps (reading R6) or after max_sweeps.  pi = argmins of the final  */
 /* sweep (reading R9).  trace[i] = r_{first_sweep+i}.                   */
+/* chunked != 0: VI* of P:L577 instead -- every application is T in     */
+/* chunks of b states against the old values (orc_sweep_chunked).       */
 /* ------------------------------------------------------------------ */
 int orc_vi(const orc_mdp* m, int64_t b, uint64_t seed, int identity, int64_t first_sweep,
-           double eps, int64_t max_sweeps, double* V, int32_t* pi, double* trace, int64_t* sweeps_out)
+           double eps, int64_t max_sweeps, int chunked, double* V, int32_t* pi, double* trace,
+           int64_t* sweeps_out)
 {
     if (!m || !V || !pi || b < 1 || b > m->n || max_sweeps < 1 || !(eps > 0.0)) return ORC_INVALID_ARG;
     uint32_t* perm = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m->n);
@@ -282,7 +347,8 @@ int orc_vi(const orc_mdp* m, int64_t b, uint64_t seed, int identity, int64_t fir
     while (it < max_sweeps) {
         double r;
         orc_partition(m->n, seed, first_sweep + it, identity, perm);
-        int rc = orc_sweep(m, b, perm, NULL, V, pi, &r);
+        int rc = chunked ? orc_sweep_chunked(m, b, perm, NULL, V, pi, &r)
+                         : orc_sweep(m, b, perm, NULL, V, pi, &r);
         if (trace) trace[it] = r;
         ++it;
         if (rc == ORC_NONFINITE) { st = ORC_NONFINITE; break; }

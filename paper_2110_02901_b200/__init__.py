@@ -27,6 +27,8 @@ LIB_PATH = os.environ.get("RMB_LIB_PATH") or os.path.join(_HERE, "librmb.so")  #
 OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM, UNSUPPORTED = range(9)
 F32, F64 = 0, 1
 ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+CHUNKED_T = 0x40
+SPARSE_FULL_GRID, SPARSE_WIDE_OFF, SPARSE_WIDE_ON, SHARD_NO_GRAPH = 0x80, 0x100, 0x200, 0x400
 
 _lib = None
 
@@ -81,6 +83,7 @@ _SIGS = {
     "rmb_generate_grid": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "rmb_last_launch_count": ([ctypes.c_void_p], ctypes.c_int64),
+    "rmb_last_graph_launches": ([ctypes.c_void_p], ctypes.c_int64),
     "rmb_shard_range": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                          ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "rmb_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
@@ -147,6 +150,21 @@ def _ptr(x):
     return ctypes.c_void_p(x.data_ptr())
 
 
+def _vec(x, n, kind, what):
+    """Check a V (kind "f64") or pi (kind "i32") buffer: dtype and length n.
+    The library reads / writes exactly n elements of that type."""
+    if x is None:
+        return x
+    import torch
+    want = {"f64": (np.float64, torch.float64), "i32": (np.int32, torch.int32)}[kind]
+    if x.dtype not in want:
+        raise TypeError(f"{what} must be {'float64' if kind == 'f64' else 'int32'}, got {x.dtype}")
+    numel = x.size if isinstance(x, np.ndarray) else x.numel()
+    if numel != n:
+        raise ValueError(f"{what} must have n = {n} elements, got {numel}")
+    return x
+
+
 def _dtype_code(x):
     import torch
     dt = x.dtype
@@ -191,7 +209,7 @@ class Problem:
     # ------------------------------------------------------------ creation
     @classmethod
     def dense(cls, P, c, gamma, stream=None, validate=False, n=None, row_range=None, nccl_comm=None, tma=True,
-              vglobal=False):
+              vglobal=False, flags=0):
         """P: [n][A][n], c: [n][A] (float32/float64, torch cuda/cpu or numpy).
         Shard handle (multi-GPU): P = the owned rows [r1-r0][A][n], c = [r1-r0][A],
         n = the global state count, row_range = (r0, r1) from shard_range(),
@@ -204,21 +222,22 @@ class Problem:
         assert ncol == n and rows == r1 - r0 and tuple(c.shape) == (rows, A) and c.dtype == P.dtype
         d = _Desc(n, A, float(gamma), _dtype_code(P), F64, r0, r1, nccl_comm, _stream_ptr(stream))
         h = ctypes.c_void_p()
-        flags = (VALIDATE if validate else 0) | (0 if tma else DENSE_NO_TMA) | (DENSE_VGLOBAL if vglobal else 0)
+        flags |= (VALIDATE if validate else 0) | (0 if tma else DENSE_NO_TMA) | (DENSE_VGLOBAL if vglobal else 0)
         _check(lib().rmb_create_dense(ctypes.byref(d), _ptr(P), _ptr(c), flags, ctypes.byref(h)))
         return cls(h, n, A, float(gamma), (P, c))
 
     @classmethod
-    def csr(cls, n, A, row_ptr, col, val, c, gamma, stream=None, validate=False, row_range=None, nccl_comm=None):
+    def csr(cls, n, A, row_ptr, col, val, c, gamma, stream=None, validate=False, row_range=None, nccl_comm=None,
+            flags=0):
         """CSR over rows r = s*A + a: row_ptr int64 [n*A+1], col int32, val float.
         Shard handle (multi-GPU): row_range = (r0, r1) from shard_range(), row_ptr
         [(r1-r0)*A+1] from 0 over the owned rows, col GLOBAL successor ids, c [r1-r0][A];
-        nccl_comm as for dense()."""
+        nccl_comm as for dense().  flags: extra create flags (SPARSE_*, SHARD_NO_GRAPH)."""
         r0, r1 = row_range if row_range is not None else (0, n)
         d = _Desc(n, A, float(gamma), _dtype_code(val), F64, r0, r1, nccl_comm, _stream_ptr(stream))
         h = ctypes.c_void_p()
         _check(lib().rmb_create_csr(ctypes.byref(d), _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(c),
-                                    VALIDATE if validate else 0, ctypes.byref(h)))
+                                    (VALIDATE if validate else 0) | flags, ctypes.byref(h)))
         return cls(h, n, A, float(gamma), (row_ptr, col, val, c))
 
     def close(self):
@@ -245,15 +264,17 @@ class Problem:
             V = torch.zeros(self.n, dtype=torch.float64, device=device)
         if pi is None:
             pi = torch.zeros(self.n, dtype=torch.int32, device=device)
-        return V, pi
+        return _vec(V, self.n, "f64", "V"), _vec(pi, self.n, "i32", "pi")
 
     def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-           device="cuda"):
-        """MB-VI: V, pi updated in place (torch cuda/cpu or numpy)."""
+           device="cuda", chunked=False):
+        """MB-VI: V, pi updated in place (torch cuda/cpu or numpy).
+        chunked=True: VI* -- every sweep is T computed in chunks of b
+        states against the sweep-start values (RMB_CHUNKED_T)."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_sweeps)
         st = Stats()
-        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
         s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         return Solution(V, pi, tr[: st.sweeps], s, st)
@@ -272,16 +293,21 @@ class Problem:
         o = st.outer_iters
         return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
 
-    def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False):
+    def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False, chunked=False):
         """One application of B_b (pi None) or B_{pi,b}: returns (V_out, argmin, residual)."""
         import torch
+        _vec(V_in, self.n, "f64", "V_in")
+        _vec(pi, self.n, "i32", "pi")
         if V_out is None:
             V_out = torch.empty_like(V_in) if not isinstance(V_in, np.ndarray) else np.empty_like(V_in)
+        _vec(V_out, self.n, "f64", "V_out")
         if argmin is None:
             argmin = (torch.empty(self.n, dtype=torch.int32, device=V_out.device)
                       if not isinstance(V_out, np.ndarray) else np.empty(self.n, np.int32))
+        _vec(argmin, self.n, "i32", "argmin")
         r = ctypes.c_double()
-        s = lib().rmb_apply(self._h, b, seed, sweep, ORDER_IDENTITY if identity else 0, _ptr(pi), _ptr(V_in),
+        flags = (ORDER_IDENTITY if identity else 0) | (CHUNKED_T if chunked else 0)
+        s = lib().rmb_apply(self._h, b, seed, sweep, flags, _ptr(pi), _ptr(V_in),
                             _ptr(V_out), _ptr(argmin), ctypes.byref(r))
         _check(s, (OK, NONFINITE))
         return V_out, argmin, r.value
@@ -291,6 +317,8 @@ class Problem:
         """J_pi by B_{pi,b} iteration to ||V_k - V_{k-1}|| <= eps (Eq. 4 / Lemma 4)."""
         import torch
         V = torch.zeros(self.n, dtype=torch.float64, device=device) if V is None else V
+        _vec(V, self.n, "f64", "V")
+        _vec(pi, self.n, "i32", "pi")
         tr = np.zeros(min(max_sweeps, 1 << 20))
         st = Stats()
         flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
@@ -301,6 +329,8 @@ class Problem:
 
     def improve(self, V, pi):
         """Policy improvement (Alg. 1): pi in place; returns (pi, ||TV-V||, changed)."""
+        _vec(V, self.n, "f64", "V")
+        _vec(pi, self.n, "i32", "pi")
         r, ch = ctypes.c_double(), ctypes.c_int64()
         s = lib().rmb_improve(self._h, _ptr(V), _ptr(pi), ctypes.byref(r), ctypes.byref(ch))
         _check(s, (OK, NONFINITE))
@@ -308,6 +338,9 @@ class Problem:
 
     def last_launch_count(self):
         return int(lib().rmb_last_launch_count(self._h))
+
+    def last_graph_launches(self):
+        return int(lib().rmb_last_graph_launches(self._h))
 
     def last_phase_times(self):
         """(compute_ns, barrier_ns, combine_ns, n_barriers) of the last solve, CTA 0's view."""
@@ -355,6 +388,8 @@ def vi_group(problems, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None,
     n = problems[0].n
     V = torch.zeros(n, dtype=torch.float64, device=device) if V is None else V
     pi = torch.zeros(n, dtype=torch.int32, device=device) if pi is None else pi
+    _vec(V, n, "f64", "V")
+    _vec(pi, n, "i32", "pi")
     tr = np.zeros(max_sweeps)
     st = Stats()
     flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
@@ -371,6 +406,8 @@ def mpi_group(problems, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=Non
     n = problems[0].n
     V = torch.zeros(n, dtype=torch.float64, device=device) if V is None else V
     pi = torch.zeros(n, dtype=torch.int32, device=device) if pi is None else pi
+    _vec(V, n, "f64", "V")
+    _vec(pi, n, "i32", "pi")
     tr = np.zeros(max_outer * (m + 1))
     ch = np.zeros(max_outer, dtype=np.int64)
     st = Stats()

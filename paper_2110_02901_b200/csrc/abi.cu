@@ -126,6 +126,28 @@ static rmb_status validate_mdp(Problem& pr)
     return RMB_OK;
 }
 
+// pi (device) must hold actions in [0, A) on [lo, hi): an out-of-range entry
+// would index a row past the end of P (checked on the device, on the stream)
+static rmb_status check_policy(Problem& pr, const int32_t* pi_dev, int64_t lo, int64_t hi)
+{
+    if (pr.aux.ensure(256) != cudaSuccess) return fail(RMB_ERR_OOM, "policy check: allocation failed");
+    int* bad = static_cast<int*>(pr.aux.p);
+    cudaError_t e = launch_check_policy(pi_dev, lo, hi, pr.A, bad, pr.stream);
+    int h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "policy check");
+    if (h) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
+    return RMB_OK;
+}
+
+static void apply_create_flags(Problem& pr, uint32_t flags)
+{
+    pr.sparse_full_grid = (flags & RMB_SPARSE_FULL_GRID) != 0;
+    pr.sparse_wide = (flags & RMB_SPARSE_WIDE_ON) ? 1 : (flags & RMB_SPARSE_WIDE_OFF) ? 0 : -1;
+    pr.shard_no_graph = (flags & RMB_SHARD_NO_GRAPH) != 0;
+}
+
 static bool is_shard(const Problem& pr) { return pr.nccl_comm || pr.row_begin != 0 || pr.row_end != pr.n; }
 
 static rmb_status solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t tl, long long* chg_dev,
@@ -250,6 +272,7 @@ rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, 
     pr->dense = true;
     pr->no_tma = (flags & RMB_DENSE_NO_TMA) != 0;
     pr->vglobal = (flags & RMB_DENSE_VGLOBAL) != 0;
+    apply_create_flags(*pr, flags);
     if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
     if (s != RMB_OK) {
         free_problem(pr);
@@ -271,6 +294,7 @@ rmb_status rmb_create_csr(const rmb_desc* desc, const int64_t* row_ptr, const in
     Problem* pr = new Problem();
     s = init_problem(*pr, desc);
     pr->dense = false;
+    apply_create_flags(*pr, flags);
     const int64_t rows = (desc->row_end - desc->row_begin) * (int64_t)desc->n_actions;  // owned rows
     const size_t psz = desc->p_dtype == RMB_F32 ? 4 : 8;
     // row_ptr is inspected on the host (nnz, fixed stride -> ELL)
@@ -320,6 +344,11 @@ int64_t rmb_last_launch_count(rmb_problem h)
     return h ? reinterpret_cast<Problem*>(h)->last_launches : 0;
 }
 
+int64_t rmb_last_graph_launches(rmb_problem h)
+{
+    return h ? reinterpret_cast<Problem*>(h)->last_graph_launches : 0;
+}
+
 rmb_status rmb_last_phase_times(rmb_problem h, int64_t* ns4)
 {
     if (!h || !ns4) return fail(RMB_ERR_INVALID_ARG, "handle or ns4 is NULL");
@@ -348,11 +377,13 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     rq.seed = seed;
     rq.k0 = 1;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.chunked = flags & RMB_CHUNKED_T;
     rq.eps = eps;
     rq.max_iter = max_sweeps;
     rq.V = sg.V;
     rq.pi = sg.pi;
     SolveResult r;
+    if (is_shard(pr) && rq.chunked) return fail(RMB_ERR_UNSUPPORTED, "RMB_CHUNKED_T on a row-range (sharded) handle");
     if (is_shard(pr)) {  // multi-GPU: this rank's rows, NCCL exchange per batch
         if (!pr.nccl_comm) return fail(RMB_ERR_INVALID_ARG, "a row-range handle needs nccl_comm (or rmb_vi_group)");
         pr.stage_V = sg.V;
@@ -395,13 +426,9 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     Staged sg;
     rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
     if (s != RMB_OK) return s;
-    if (pi_given) {  // validate the given policy (the owned entries) on the host side of the copy
-        std::vector<int32_t> hp((size_t)pr.n);
-        cudaError_t e = cudaMemcpyAsync(hp.data(), sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
-        if (e != cudaSuccess) return cuda_fail(e, "read pi");
-        for (int64_t q = pr.row_begin; q < pr.row_end; ++q)
-            if (hp[q] < 0 || hp[q] >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
+    if (pi_given) {  // the given policy's owned entries must be actions in [0, A)
+        s = check_policy(pr, sg.pi, pr.row_begin, pr.row_end);
+        if (s != RMB_OK) return s;
     }
     const int64_t tl = max_outer * (int64_t)(m + 1);
     if (pr.trace.ensure((size_t)tl * 8) != cudaSuccess || pr.chg.ensure((size_t)max_outer * 8) != cudaSuccess)
@@ -441,7 +468,8 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     s = stage_out(pr, V, pi, sg);
     if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.outer * (int64_t)(m + 1));
     if (s == RMB_OK && changed && r.outer > 0) {
-        cudaError_t e = cudaMemcpy(changed, pr.chg.p, (size_t)r.outer * 8, cudaMemcpyDeviceToHost);
+        cudaError_t e = cudaMemcpyAsync(changed, pr.chg.p, (size_t)r.outer * 8, cudaMemcpyDeviceToHost, pr.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
         if (e != cudaSuccess) s = cuda_fail(e, "changed copy");
     }
     if (s != RMB_OK) return s;
@@ -490,6 +518,10 @@ static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint3
         if (e == cudaSuccess) e = rq.pi_given ? cudaMemcpyAsync(p.stage_pi, pi, pb, cudaMemcpyDefault, st)
                                               : cudaMemsetAsync(p.stage_pi, 0, pb, st);
         if (e != cudaSuccess) return cuda_fail(e, "group staging");
+        if (rq.pi_given) {
+            rmb_status cs = check_policy(p, p.stage_pi, p.row_begin, p.row_end);
+            if (cs != RMB_OK) return cs;
+        }
     }
     SolveResult r;
     rmb_status s = sharded_solve(rk.data(), G, false, rq, trace, tl, changed, cl, &r);
@@ -581,6 +613,10 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
         pw = is_device_ptr(argmin_out) ? argmin_out : static_cast<int32_t*>(pr.pistage.p);
     }
     if (e != cudaSuccess) return cuda_fail(e, "rmb_apply staging");
+    if (pi_or_null) {
+        rmb_status cs = check_policy(pr, pw, 0, pr.n);
+        if (cs != RMB_OK) return cs;
+    }
     if (pr.trace.ensure(64) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.mode = pi_or_null ? MODE_APPLY_PI : MODE_APPLY;
@@ -588,6 +624,7 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
     rq.seed = seed;
     rq.k0 = sweep;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.chunked = flags & RMB_CHUNKED_T;
     rq.eps = -1.0;
     rq.max_iter = 1;
     rq.V = Vw;
@@ -648,14 +685,8 @@ rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_
     Staged sg;
     rmb_status s = stage_in(pr, V, const_cast<int32_t*>(pi), flags & RMB_V0_ZERO, true, sg);
     if (s != RMB_OK) return s;
-    {
-        std::vector<int32_t> hp((size_t)pr.n);
-        cudaError_t e = cudaMemcpyAsync(hp.data(), sg.pi, (size_t)pr.n * 4, cudaMemcpyDeviceToHost, pr.stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
-        if (e != cudaSuccess) return cuda_fail(e, "read pi");
-        for (int32_t a : hp)
-            if (a < 0 || a >= pr.A) return fail(RMB_ERR_INVALID_ARG, "pi holds an action outside [0, A)");
-    }
+    s = check_policy(pr, sg.pi, 0, pr.n);
+    if (s != RMB_OK) return s;
     if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.mode = MODE_POLICY_VALUE;

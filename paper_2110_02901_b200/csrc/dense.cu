@@ -45,7 +45,7 @@ namespace rmb {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kAG = 4;                     // actions per compute item (min modes)
-constexpr int kPathWarp = 0, kPathCta = 1, kPathRows = 2, kPathTma = 3;  // compute path of a kernel instantiation
+constexpr int kPathWarp = 0, kPathTma = 3;  // compute path of a kernel instantiation
 // TMA path with V (and pi) in GLOBAL memory (L2-resident) instead of shared
 // memory: dense n too large for a shared-memory copy of V (n > ~27k)
 constexpr int kPathTmaG = 4;
@@ -61,8 +61,6 @@ struct Plan {
     int Lc;         // chunk length (elements)
     int C;          // chunks per row
     int redundant;  // 1: every CTA reduces every state (single barrier)
-    int cta;        // 1: CTA-cooperative tile pipeline, 0: warp-owned items
-    int rows;       // 1: CTA-per-state rows mode (whole rows, C = 1, ng = A)
     int ng;         // action rows per warp item in min modes (4, or 1 for short-tail batches)
     int raw;        // 1 (TMA path): items store raw row dot products part[(i*Ae + a)*C + ch]; costs,
                     //   chunk sums and min/argmin are all done by the combine (S-mode, even at C == 1)
@@ -87,6 +85,7 @@ struct DenseArgs {
     int msweeps;
     Plan plan[3];        // 0 = B_b sweep, 1 = B_{pi,b} sweep, 2 = improvement
     int64_t imp_sub;     // improvement sub-batch (states)
+    double* vnext;       // chunked T (VI*): new values of the sweep, applied at its end; null = B_b
     uint32_t* perm;      // 3 * n (triple-buffered by sweep index)
     double* part;        // 2 * part_stride
     int64_t part_stride;
@@ -101,9 +100,7 @@ struct DenseArgs {
     int64_t chg_len;
     long long* out;
     unsigned int* wctr;  // [2] work-stealing counters (phase parity)
-    int path;            // compute path (kPathWarp / kPathCta / kPathRows)
-    unsigned int* pctr;  // [2] tail-prefetch counters (phase parity)
-    int64_t pf_bytes;    // tail-prefetch budget per batch (bytes of P)
+    int path;            // compute path (kPathWarp / kPathTma / kPathTmaG)
     int64_t vs_half;     // smem V: offset of the hi plane (VE == 4), 0 = linear
     // multi-GPU shard steps
     int64_t row0, row1;        // owned states (P and c are offset so that global state ids index them)
@@ -117,13 +114,10 @@ struct DenseArgs {
     long long* prof;     // [0] compute ns, [1] barrier ns, [2] combine ns, [3] barriers (CTA 0)
     int64_t tma_off;     // TMA path: byte offset of the stage ring in dynamic smem
     int tma_nst;         //           ring stages
-    int tma_gmin;        //           minimum items per dynamic grab (experiments: RMB_TMA_G)
     unsigned long long* gred;  // global-V path: 4 reduction slots x 4 words (rmax bits, bad, changed)
     int tma_piece;       //           columns per stage and row slot
     int tma_static;      //           batches with <= tma_static * grid items are dealt statically
-    int tma_pf;          //           L2 prefetch of an item's later stages at its start (RMB_TMA_PF=0 disables)
     int tma_slot;        //           bytes per ring slot (piece bytes rounded up to 128)
-    int tma_hint;        //           L2 evict-first hint on the bulk copies (RMB_TMA_HINT=0 disables)
 };
 
 // ---------------------------------------------------------------- loads
@@ -385,21 +379,10 @@ __device__ __forceinline__ void item_epilogue(const DenseArgs& a, const Plan& pl
     }
 }
 
-// Tail prefetch: a warp that finds no more items in this batch asks a second
-// counter for items of the NEXT batch (same decomposition, grabbed in the same
-// order there) and issues one cp.async.bulk.prefetch.L2 per row chunk, so the
-// HBM bandwidth the end-of-batch tail leaves idle fetches the next batch's
-// first items into L2 (a bounded budget so they are still there when used).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 template <typename PT, int VE, bool EVAL, int NGT>
 __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
-                              int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr,
-                              const uint32_t* perm_next = nullptr, int64_t lo_next = 0, int64_t cnt_next = 0,
-                              unsigned int* pctr = nullptr)
+                              int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
 {
     const int lane = threadIdx.x & 31;
     const int C = pl.C;
@@ -461,437 +444,6 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
         it = it_next;
         s_cur = s_next;
     }
-    if (cnt_next > 0 && pctr && VE > 1 && a.pf_bytes > 0) {
-        const int64_t items_next = cnt_next * per_state;
-        const int64_t item_bytes = (int64_t)NG * Lc * (int64_t)sizeof(PT);
-        const int64_t budget = min(items_next, max((int64_t)1, a.pf_bytes / item_bytes));
-        while (true) {
-            unsigned int r = 0;
-            if (lane == 0) r = atomicAdd(pctr, 1u);
-            r = __shfl_sync(0xffffffffu, r, 0);
-            if ((int64_t)r >= budget) break;
-            const int64_t i = (int64_t)r / per_state;
-            const int rr = (int)((int64_t)r - i * per_state);
-            const int ag = rr / C;
-            const int ch = rr - ag * C;
-            const int64_t s = min(a.n - 1, perm_next ? (int64_t)__ldcg(perm_next + lo_next + i) : lo_next + i);
-            const int a0 = EVAL ? pis[s] : ag * NG;
-            const int na = EVAL ? 1 : min(NG, a.A - a0);
-            const int64_t j0 = (int64_t)ch * Lc;
-            const int64_t j1 = min(a.n, j0 + Lc);
-            if (lane < na)
-                prefetch_l2(P + ((int64_t)s * a.A + a0 + lane) * a.n + j0, (uint32_t)((j1 - j0) * sizeof(PT)));
-        }
-    }
-}
-
-// ------------------------------------------------- CTA tile pipeline
-// The compute phase as a per-SM pipeline: a TILE = (state i, action group of
-// NG rows, column chunk) is streamed by all 512 threads of the CTA together
-// (thread t takes vectors t, t+512, ...), so a tile completes ~16x sooner than
-// if one warp owned it and the end-of-batch tail shrinks accordingly.  Each
-// thread keeps D slots of NG*U2 = 4 vector loads in flight and keeps issuing
-// across tile boundaries; per tile one __syncthreads joins the 16 warp sums
-// (fixed warp order -> reproducible) while the next tile's loads are already
-// in flight.  Tiles are taken from a global work-stealing counter by thread 0,
-// five tiles ahead, with their state id / costs prefetched into a smem ring.
-constexpr int kRing = 8;
-constexpr int kD = 1;                      // slots in flight per thread
-constexpr int kSlotLoads = 8;              // vector loads per thread per slot
-constexpr int kCW = kWarps - 1;            // streaming warps (warp kCW is the producer)
-constexpr int kCT = kCW * kWarp;           // streaming threads
-
-struct TileRing {
-    long long it[kRing];  // item index, -1 = end
-    long long s[kRing];   // state
-    long long i[kRing];   // batch position
-    int a0[kRing], na[kRing], ch[kRing], R[kRing];
-    long long j0[kRing];
-    int nvec[kRing];
-    double cost[kRing][kAG];
-    double red[kRing][kCW][kAG];
-    volatile int ready[kRing];    // tile number whose descriptor the slot holds
-    volatile int allowed[kRing];  // next tile number the producer may write into the slot
-    int arrive[kRing];            // streaming warps done with the slot's tile
-};
-
-// ------------------------------------------------- CTA tile pipeline
-// A TILE = (state i, group of NG action rows, column chunk) is streamed by the
-// 480 streaming threads of the CTA together (thread t takes vectors t, t+480,
-// ...), so it completes ~15x sooner than a warp-owned item and the end-of-
-// batch tail shrinks accordingly.  Each streaming thread keeps kD slots of 4
-// vector loads in flight and keeps issuing across tile boundaries.
-// Warp specialisation: warp 15 is the PRODUCER — it takes tiles from the
-// global work-stealing counter (one atomic per tile), resolves the state id
-// and costs, and publishes descriptors into a smem ring up to kRing tiles
-// ahead.  Streaming warps never touch global control data: at the end of a
-// tile each adds its warp sum to the tile's smem slot and bumps the arrival
-// counter; the last arriver sums the 15 partials in warp order (reproducible),
-// writes the tile result and frees the ring slot.  No CTA-wide barrier per tile.
-template <typename PT, int VE, bool EVAL>
-__device__ void compute_phase_cta(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
-                                  int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
-{
-    using VT = typename Vec<PT, VE>::T;
-    constexpr int NG = EVAL ? 1 : kAG;
-    constexpr int U2 = kSlotLoads / NG;  // vectors per row per slot
-    constexpr int kStep = kCT * U2;
-    __shared__ TileRing tr;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int C = pl.C;
-    const int64_t Lc = pl.Lc;
-    const int NAG = EVAL ? 1 : (a.A + kAG - 1) / kAG;
-    const int64_t per_state = (int64_t)NAG * C;
-    const int64_t items = cnt * per_state;
-    const PT* P = static_cast<const PT*>(a.P);
-    const int64_t rowvec = a.n / VE;  // row stride in vectors
-
-    csync();  // the previous phase is done with tr
-    if (tid < kRing) {
-        tr.arrive[tid] = 0;
-        tr.ready[tid] = -1;  // stale tile numbers of the previous phase must not match
-        tr.allowed[tid] = tid;
-    }
-    csync();
-
-    if (warp == kCW) {
-        // ------------------------------------------------ producer warp
-        if (lane == 0) {
-            for (int q = 0;; ++q) {
-                const int sl = q & (kRing - 1);
-                while (tr.allowed[sl] != q) {
-                }
-                const long long it = (long long)atomicAdd(ctr, 1u);
-                if (it >= items) {
-                    tr.it[sl] = -1;
-                } else {
-                    const int64_t i = it / per_state;
-                    const int rr = (int)(it - i * per_state);
-                    const int ag = rr / C;
-                    const int ch = rr - ag * C;
-                    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-                    const int a0 = EVAL ? pis[s] : ag * kAG;
-                    const int na = EVAL ? 1 : min(kAG, a.A - a0);
-                    const int64_t j0 = (int64_t)ch * Lc;
-                    const int64_t j1 = min(a.n, j0 + Lc);
-                    const int nvec = (int)((j1 - j0) / VE);
-                    tr.it[sl] = it;
-                    tr.s[sl] = s;
-                    tr.i[sl] = i;
-                    tr.a0[sl] = a0;
-                    tr.na[sl] = na;
-                    tr.ch[sl] = ch;
-                    tr.j0[sl] = j0;
-                    tr.nvec[sl] = nvec;
-                    tr.R[sl] = max(1, (nvec + kStep - 1) / kStep);
-                    for (int g = 0; g < kAG; ++g) tr.cost[sl][g] = g < na ? load_cost<PT>(a, s * a.A + a0 + g) : 0.0;
-                }
-                __threadfence_block();
-                tr.ready[sl] = q;
-                if (it >= items) break;
-            }
-        }
-        csync();
-        return;
-    }
-
-    // ------------------------------------------------ streaming warps
-    // Readers spin on the slot's ready flag and read the fields with volatile
-    // shared loads (in order per thread); no fence — a fence would drain this
-    // thread's in-flight P loads at every tile boundary.
-    auto wait_ready = [&](int q) -> int {
-        const int sl = q & (kRing - 1);
-        while (tr.ready[sl] != q) {
-        }
-        return sl;
-    };
-    const volatile TileRing& vt = tr;
-
-    const VT* ip[NG];
-    int ileft = 0, ina = 0, islots = 0, iq = 0;
-    bool ilive = false;
-    auto begin_issue = [&](int q) {
-        const int sl = wait_ready(q);
-        ilive = vt.it[sl] >= 0;
-        if (!ilive) return;
-        const VT* row = reinterpret_cast<const VT*>(P + (vt.s[sl] * a.A + vt.a0[sl]) * a.n + vt.j0[sl]) + tid;
-#pragma unroll
-        for (int g = 0; g < NG; ++g) ip[g] = row + (int64_t)g * rowvec;
-        ileft = vt.nvec[sl] - tid;
-        ina = vt.na[sl];
-        islots = vt.R[sl];
-    };
-    int cvo = 0, cleft = 0, cna = 0, cslots = 0, cq = 0;
-    bool clive = false;
-    auto begin_consume = [&](int q) {
-        const int sl = wait_ready(q);
-        clive = vt.it[sl] >= 0;
-        if (!clive) return;
-        cvo = (int)vt.j0[sl] + tid * VE;
-        cleft = vt.nvec[sl] - tid;
-        cna = vt.na[sl];
-        cslots = vt.R[sl];
-    };
-
-    VT buf[kD][kSlotLoads];
-    double acc[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) acc[g] = 0.0;
-    begin_issue(0);
-    begin_consume(0);
-
-    auto issue = [&](VT (&b)[kSlotLoads]) {
-        if (!ilive) return;
-#pragma unroll
-        for (int u = 0; u < U2; ++u) {
-            const bool ok = ileft > kCT * u;
-#pragma unroll
-            for (int g = 0; g < NG; ++g)
-                if (ok && g < ina) b[u * NG + g] = ld_stream(ip[g] + kCT * u);
-        }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) ip[g] += kStep;
-        ileft -= kStep;
-        if (--islots == 0) begin_issue(++iq);
-    };
-    auto consume = [&](const VT (&b)[kSlotLoads]) {
-#pragma unroll
-        for (int u = 0; u < U2; ++u) {
-            if (cleft > kCT * u) {
-                double vs[VE];
-                load_v<VE>(Vs, cvo + kCT * VE * u, vs, a.vs_half);
-#pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    if (g < cna) {
-                        double pv[VE];
-                        Vec<PT, VE>::get(b[u * NG + g], pv);
-#pragma unroll
-                        for (int e = 0; e < VE; ++e) acc[g] = fma(pv[e], vs[e], acc[g]);
-                    }
-                }
-            }
-        }
-        cvo += kStep * VE;
-        cleft -= kStep;
-    };
-    auto finalize = [&]() {
-        const int sl = cq & (kRing - 1);
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            const double w = warp_sum(acc[g]);
-            if (lane == 0) tr.red[sl][warp][g] = w;
-            acc[g] = 0.0;
-        }
-        // shared-memory stores and atomics of one thread are performed in
-        // order; the last arriver reads the partials with volatile loads
-        int last = 0;
-        if (lane == 0) last = atomicAdd(&tr.arrive[sl], 1) == kCW - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {  // this warp runs the tile's (cheap) epilogue
-            const int64_t i = vt.i[sl];
-            const int a0 = vt.a0[sl], na = vt.na[sl], ch = vt.ch[sl];
-            if (lane == 0) {
-                double tot[NG];
-                for (int g = 0; g < NG; ++g) {
-                    tot[g] = 0.0;
-                    for (int w = 0; w < kCW; ++w) tot[g] += vt.red[sl][w][g];
-                }
-                if (C == 1) {
-                    if (EVAL) {
-                        part[i] = vt.cost[sl][0] + a.gamma * tot[0];
-                    } else {
-                        double best = 0.0;
-                        int barg = a0;
-                        for (int g = 0; g < NG; ++g)
-                            if (g < na) {
-                                const double Q = vt.cost[sl][g] + a.gamma * tot[g];
-                                if (g == 0 || Q < best) best = Q, barg = a0 + g;
-                            }
-                        part[2 * (i * NAG + a0 / kAG)] = best;
-                        part[2 * (i * NAG + a0 / kAG) + 1] = (double)barg;
-                    }
-                } else if (EVAL) {
-                    part[i * C + ch] = tot[0];
-                } else {
-                    for (int g = 0; g < NG; ++g)
-                        if (g < na) part[(i * a.A + a0 + g) * C + ch] = tot[g];
-                }
-            }
-            if (!pl.redundant) {
-                if (per_state == 1) {
-                    if (lane == 0) {
-                        a.lval[i] = EVAL ? part[i] : part[2 * i];
-                        a.larg[i] = EVAL ? a0 : (int)part[2 * i + 1];
-                    }
-                } else {
-                    unsigned int prev = 0;
-                    if (lane == 0) {
-                        __threadfence();
-                        prev = atomicAdd(a.scnt + i, 1u);
-                    }
-                    prev = __shfl_sync(0xffffffffu, prev, 0);
-                    if (prev == (unsigned int)(per_state - 1)) {
-                        __threadfence();
-                        finish_state_warp<PT, EVAL>(a, part, C, i, vt.s[sl], a0);
-                        if (lane == 0) a.scnt[i] = 0u;
-                    }
-                }
-            }
-            if (lane == 0) {
-                tr.arrive[sl] = 0;
-                tr.allowed[sl] = cq + kRing;  // the producer may reuse the slot
-            }
-            __syncwarp();
-        }
-        begin_consume(++cq);
-    };
-
-#pragma unroll
-    for (int d = 0; d < kD; ++d) issue(buf[d]);
-    while (clive) {
-#pragma unroll
-        for (int d = 0; d < kD; ++d) {
-            if (!clive) break;
-            consume(buf[d]);
-            issue(buf[d]);
-            if (--cslots == 0) finalize();
-        }
-    }
-    csync();  // pairs with the producer's; every epilogue is complete
-}
-
-// ------------------------------------------------ CTA-per-state rows mode
-// For batches that offer >= 4 states per SM: an ITEM is g = max(1, 16/A)
-// whole states; the CTA's 16 warps take its action rows (warp w: rows w,
-// w+16, ...) and stream each WHOLE row with 8 x 128-bit loads in flight per
-// lane (one warp reduction per row, as in the warp-item path).  A state's
-// (min Q, argmin) is taken in shared memory by the last warp to finish the
-// item, in action order (lowest index on ties).  An item is ~15 us of one SM's
-// HBM share, so the end-of-batch tail is ~4x shorter than with warp-owned
-// 4-row items, and no per-state partials or global atomics are needed.
-// Items come from the global work-stealing counter through a 4-deep smem ring
-// refilled by the last warp of each item.
-constexpr int kRR = 4;          // ring depth
-constexpr int kRowsMax = 64;    // actions per state supported by rows mode
-
-struct RowsRing {
-    long long it[kRR];
-    int ready[kRR];
-    int arrive[kRR];
-    double q[kRR][kRowsMax];
-};
-
-template <typename PT, int VE, bool EVAL>
-__device__ void compute_phase_rows(const DenseArgs& a, const double* Vs, const int32_t* pis, const uint32_t* perm,
-                                   int64_t lo, int64_t cnt, const Plan& pl, double* part, unsigned int* ctr)
-{
-    __shared__ RowsRing rr;
-    __shared__ long long r_base;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int Ae = EVAL ? 1 : a.A;
-    const int gst = max(1, kWarps / Ae);  // states per item
-    const int64_t items = (cnt + gst - 1) / gst;
-    const PT* P = static_cast<const PT*>(a.P);
-    csync();  // the previous phase is done with rr
-    if (threadIdx.x < kRR) {
-        rr.arrive[threadIdx.x] = 0;
-        rr.ready[threadIdx.x] = -1;
-    }
-    if (threadIdx.x == 0) r_base = (long long)atomicAdd(ctr, (unsigned int)kRR);
-    csync();
-    if (threadIdx.x < kRR) {
-        rr.it[threadIdx.x] = r_base + threadIdx.x;
-        rr.ready[threadIdx.x] = threadIdx.x;
-    }
-    csync();
-    volatile RowsRing& vr = rr;
-    // a grab issued by this warp's last epilogue, published after its next
-    // row so that the atomic's latency hides behind the streaming
-    bool pending = false;
-    int pend_sl = 0, pend_q = 0;
-    unsigned int pend_it = 0;
-    auto publish = [&]() {
-        if (pending && lane == 0) {
-            vr.it[pend_sl] = (long long)pend_it;  // smem stores of one thread land in order:
-            vr.ready[pend_sl] = pend_q;           // the slot is complete once ready is seen
-        }
-        pending = false;
-    };
-    for (int q = 0;; ++q) {
-        const int sl = q & (kRR - 1);
-        while (vr.ready[sl] != q) {
-        }
-        const long long it = vr.it[sl];
-        if (it >= items) {
-            publish();
-            break;
-        }
-        const int64_t i0 = it * gst;
-        const int ns = (int)min((int64_t)gst, cnt - i0);
-        for (int r = warp; r < ns * Ae; r += kWarps) {
-            const int ist = r / Ae;
-            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i0 + ist) : lo + i0 + ist;
-            const int act = EVAL ? pis[s] : r - ist * Ae;
-            double acc[1] = {0.0};
-            dot_rows<PT, VE, 1, 8>(P + ((int64_t)s * a.A + act) * a.n, a.n, 1, 0, a.n, Vs, lane, acc, a.vs_half);
-            const double d = warp_sum(acc[0]);
-            if (lane == 0) rr.q[sl][r] = load_cost<PT>(a, s * a.A + act) + a.gamma * d;
-            publish();
-        }
-        publish();
-        int last = 0;
-        if (lane == 0) last = atomicAdd(&rr.arrive[sl], 1) == kWarps - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-#ifndef RMB_ROWS_VARIANT
-#define RMB_ROWS_VARIANT 1
-#endif
-        if (last && lane == 0) {
-            for (int ist = 0; ist < ns; ++ist) {
-                const int64_t i = i0 + ist;
-                double best = vr.q[sl][ist * Ae];
-                int barg = 0;
-                if (EVAL) {
-                    const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
-                    barg = pis[s];
-                } else {
-                    for (int act = 1; act < Ae; ++act) {
-                        const double Q = vr.q[sl][ist * Ae + act];
-                        if (Q < best) best = Q, barg = act;
-                    }
-                }
-                if (pl.redundant) {
-                    if (EVAL) {
-                        part[i] = best;
-                    } else {
-                        part[2 * i] = best;
-                        part[2 * i + 1] = (double)barg;
-                    }
-                } else {
-                    a.lval[i] = best;
-                    a.larg[i] = barg;
-                }
-            }
-            vr.arrive[sl] = 0;
-#if RMB_ROWS_VARIANT == 2
-            pend_it = atomicAdd(ctr, 1u);  // consumed at publish()
-            pend_sl = sl;
-            pend_q = q + kRR;
-            pending = true;
-#else
-            vr.it[sl] = (long long)atomicAdd(ctr, 1u);
-#if RMB_ROWS_VARIANT == 0
-            __threadfence_block();
-#endif
-            vr.ready[sl] = q + kRR;
-#endif
-        }
-        pending = __shfl_sync(0xffffffffu, pending ? 1 : 0, 0) != 0;
-        __syncwarp();
-    }
-    csync();
 }
 
 // ------------------------------------------------- TMA ring path (default)
@@ -919,17 +471,11 @@ __device__ void compute_phase_rows(const DenseArgs& a, const double* Vs, const i
 // Work counters: a producer leaves a batch with exactly one failing grab; the
 // one that draws items + grid - 1 (the last) re-arms the counter, before its
 // end-of-batch marker, hence before that batch's grid barrier (2 counters).
-#ifndef RMB_TMA_STAGE
-#define RMB_TMA_STAGE 32768
-#endif
-constexpr int kTmaStage = RMB_TMA_STAGE;   // bytes per ring stage
+constexpr int kTmaStage = 32768;           // bytes per ring stage
 constexpr int kTmaMaxStages = 24;
 constexpr int kTmaVecs = kTmaStage / 16;   // 16-byte vectors per stage
 constexpr int kTmaThreads = kThreads + kWarp;
-#ifndef RMB_TMA_CW
-#define RMB_TMA_CW 16
-#endif
-constexpr int kTmaCW = RMB_TMA_CW;          // compute warps that consume the ring (the others idle to the barrier)
+constexpr int kTmaCW = 16;                 // compute warps that consume the ring
 
 struct TmaMeta {         // one per stage, written by the producer before its arrive
     long long i;         // batch position (END marker: batch sequence number)
@@ -1005,19 +551,9 @@ struct SpinGuard {
     }
 };
 
-#ifndef RMB_TMA_EXP
-#define RMB_TMA_EXP 0
-#endif
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                          uint64_t pol)
 {
-#if RMB_TMA_EXP == 1
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-    return;
-#endif
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_addr(dst)),
@@ -1119,10 +655,7 @@ template <typename PT>
 __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSmem& m)
 {
     uint64_t pol;
-    if (a.tma_hint)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    else
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     const PT* P = static_cast<const PT*>(a.P);
     constexpr int VB = 16 / (int)sizeof(PT);  // elements per 16-byte vector
     const int n = (int)a.n;
@@ -1179,7 +712,7 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
         const bool stat = items <= (unsigned)a.tma_static * G;
         const unsigned spi = max(1u, (unsigned)(n / C / w));  // ~stages per item
         unsigned g = 1;
-        if (!stat) g = max((unsigned)a.tma_gmin, min((4u + spi - 1) / spi, max(1u, items / (4u * G))));
+        if (!stat) g = max(1u, min((4u + spi - 1) / spi, max(1u, items / (4u * G))));
         unsigned int* ctr = a.wctr + (q & 1);
         // failing grabs return multiples of g from fail0 on; each producer does
         // exactly one, and the last of them re-arms the counter
@@ -1206,12 +739,6 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
             const int c1 = (int)((uint64_t)nvecs * (ch + 1) / C) * VB;
             const PT* rowp = P + ((int64_t)s * a.A + a0) * n;
             const int c0 = (int)((uint64_t)nvecs * ch / C) * VB;
-            if (a.tma_pf && c1 - c0 > w) {
-                // the item's stages after the first go through L2 first: HBM
-                // latency leaves the ring round trip, more bytes in flight
-                for (int gg = 0; gg < na; ++gg)
-                    prefetch_l2(rowp + (int64_t)gg * n + c0 + w, (uint32_t)((c1 - c0 - w) * (int)sizeof(PT)));
-            }
             for (int col = c0; col < c1 && !stop; col += w) {
                 const int len = min(w, c1 - col);
                 if (!acquire()) { stop = true; break; }
@@ -1301,7 +828,7 @@ __device__ void compute_phase_tma(const DenseArgs& a, const double* Vs, const Pl
             break;
         }
         const VT* stg = reinterpret_cast<const VT*>(m.ring + (size_t)st * kTmaStage);
-        if (RMB_TMA_EXP != 2) {
+        {
 #pragma unroll
             for (int f0 = 0; f0 < RV; f0 += kTmaCW * kWarp) {
                 const int f = f0 + t;
@@ -1465,7 +992,11 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
         // global V / pi: every state is patched by exactly one CTA (distributed
         // combine) and the residual / changed counts are reduced over the grid
         acc.bad |= !isfinite(v);
-        if (KIND >= 3) {
+        if (KIND == 0 && a.vnext) {  // chunked T: V stays at the sweep-start values
+            acc.rmax = fmax(acc.rmax, fabs(v - __ldcg(a.V + s)));
+            a.vnext[s] = v;
+            if (a.pi) a.pi[s] = arg;
+        } else if (KIND >= 3) {
             a.send_val[i] = v;
             a.send_idx[i] = (uint32_t)s;
             a.send_arg[i] = arg;
@@ -1496,7 +1027,12 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
     acc.rmax = fmax(acc.rmax, fabs(v - old));
     acc.bad |= !isfinite(v);
     const bool writer = blockIdx.x == 0;
-    if (KIND == 2) {
+    if (KIND == 0 && a.vnext) {  // chunked T (VI*): the smem V keeps the sweep-start values
+        if (writer) {
+            a.vnext[s] = v;
+            if (a.pi) a.pi[s] = arg;
+        }
+    } else if (KIND == 2) {
         acc.changed += (arg != pis[s]);
         pis[s] = arg;
         if (writer) a.pi[s] = arg;
@@ -1628,8 +1164,7 @@ __device__ __forceinline__ void fast_finish(const DenseArgs& a, double* Vs, int3
 // One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
 template <typename PT, int VE, int KIND, int CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
-                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k,
-                          const uint32_t* perm_next = nullptr, int64_t lo_next = 0, int64_t cnt_next = 0)
+                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
 {
     constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
@@ -1641,19 +1176,13 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
         // the other parity's work counter was last used before the previous
         // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
         atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
-        atomicExch(a.pctr + ((x.phase + 1) & 1), 0u);
     }
     // one compute path per kernel instantiation (register allocation is per
     // kernel: mixing paths made every path spill)
     if constexpr (is_tma(CTA))
         compute_phase_tma<PT, EVAL, CTA == kPathTmaG>(a, Vs, pl, part, x.tm, x.tst, x.tph);
-    else if constexpr (CTA == kPathRows)
-        compute_phase_rows<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
-    else if constexpr (CTA == kPathCta)
-        compute_phase_cta<PT, VE, EVAL>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     else
-        compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1), perm_next,
-                                         lo_next, cnt_next, a.pctr + (x.phase & 1));
+        compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
@@ -1788,20 +1317,27 @@ __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* p
     PhaseAcc acc{0.0, 0, 0};
     for (int64_t lo = 0; lo < a.n; lo += a.b) {
         const int64_t cnt = min(a.b, a.n - lo);
-        // next batch for the tail prefetch: later in this sweep, or the first
-        // batch of the next sweep (its order was generated in batch 0)
-        const uint32_t* pn = perm;
-        int64_t ln = lo + a.b, cn = 0;
-        if (ln < a.n) {
-            cn = min(a.b, a.n - ln);
-        } else if (a.b < a.n && a.mode == MODE_VI) {
-            pn = a.identity ? nullptr : a.perm + ((k + 1) % 3) * a.n;
-            ln = 0;
-            cn = a.b;
-        }
         run_batch<PT, VE, EVAL ? 1 : 0, CTA>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
-                                         (lo == 0 && !a.identity) ? k + 1 : 0, pn, ln, cn);
+                                         (lo == 0 && !a.identity) ? k + 1 : 0);
         ++x.batches;
+    }
+    if (!EVAL && a.vnext) {
+        // chunked T (VI*): every chunk read the sweep-start values; the
+        // new values were parked in vnext and land now, for the next sweep
+        timed_sync(x);
+        if constexpr (CTA == kPathTmaG) {
+            const int64_t stride = (int64_t)gridDim.x * kThreads;
+            for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < a.n; j += stride)
+                a.V[j] = __ldcg(a.vnext + j);
+            timed_sync(x);
+        } else {
+            for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
+                const double v = __ldcg(a.vnext + j);
+                Vs[vs_index(j, a.vs_half)] = v;
+                if (blockIdx.x == 0) a.V[j] = v;
+            }
+            csync();
+        }
     }
     return phase_reduce<CTA>(a, x, acc);
 }
@@ -1987,28 +1523,10 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     const int64_t maxC = std::max<int64_t>(1, (n + unit - 1) / unit);
     const int64_t lc_target = std::max<int64_t>(unit, (int64_t(16) << 10) / ((int64_t)ng * psz));
     int64_t c = 1;
-    static const bool use_cta = [] {
-        const char* e = getenv("RMB_DENSE_CTA");
-        return e && e[0] == '1';
-    }();
-    // RMB_DENSE_IPW=k (experiment): split rows until a batch offers >= k items per warp
-    static const int64_t ipw = [] {
-        const char* e = getenv("RMB_DENSE_IPW");
-        return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
-    }();
-    if (allow_split && ipw > 1 && rows < ipw * 16LL * num_sms) {
-        (void)lc_target;
-        c = std::max<int64_t>(1, (ipw * 16LL * num_sms + rows - 1) / rows);
-        c = std::min<int64_t>(c, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, cnt * A_eff)));
-        c = std::min(std::max<int64_t>(c, 1), maxC);
-    } else if (allow_split && rows < 16LL * num_sms) {
-        (void)lc_target;
+    (void)lc_target;
+    if (allow_split && rows < 16LL * num_sms) {
         // at most one item per warp (the dynamic deal then has no second round)
         c = std::max<int64_t>(1, (16LL * num_sms) / rows);
-        if (use_cta) {  // CTA tiles: at least one full slot (512 threads x 4 vectors) per tile
-            const int64_t min_lc = (int64_t)kCT * VE * (kSlotLoads / ng);
-            c = std::min<int64_t>(c, std::max<int64_t>(1, n / min_lc));
-        }
         // bound the partial-sum scratch (A_eff * C doubles per state) to 64 MB
         c = std::min<int64_t>(c, std::max<int64_t>(1, (int64_t(1) << 23) / std::max<int64_t>(1, cnt * A_eff)));
         c = std::min(std::max<int64_t>(c, 1), maxC);
@@ -2020,7 +1538,6 @@ static Plan plan_chunks(int64_t n, int64_t cnt, int64_t groups_per_state, int A_
     p.C = (int)((n + L - 1) / L);
     const int64_t per_state = p.C == 1 ? (A_eff == 1 ? 1 : 2 * groups_per_state) : (int64_t)A_eff * p.C;
     p.redundant = cnt * per_state <= kRedundantMax ? 1 : 0;
-    p.cta = use_cta ? 1 : 0;
     return p;
 }
 
@@ -2033,9 +1550,7 @@ static int64_t plan_doubles(const Plan& p, int64_t cnt, int64_t groups_per_state
 template <typename PT, int VE>
 static cudaError_t launch_typed(const DenseArgs& a, size_t smem, int grid, cudaStream_t st)
 {
-    auto kern = a.path == kPathRows ? dense_solver_kernel<PT, VE, kPathRows>
-                : a.path == kPathCta ? dense_solver_kernel<PT, VE, kPathCta>
-                                     : dense_solver_kernel<PT, VE, kPathWarp>;
+    auto kern = dense_solver_kernel<PT, VE, kPathWarp>;
     int threads = kThreads;
     if constexpr (VE * sizeof(PT) == 16) {
         if (a.path == kPathTma) {
@@ -2080,20 +1595,19 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     const int64_t n = pr.n;
     const int psz = pr.pdt == RMB_F32 ? 4 : 8;
     int VE = 16 / psz;
-    if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
+    // 16-byte vectors need aligned rows; a shard uses the whole problem's
+    // choice (g_aligned: every rank aligned), so its arithmetic is the same
+    const bool aligned = (reinterpret_cast<uintptr_t>(pr.P) & 15u) == 0 && (!pr.g_set || pr.g_aligned);
+    if ((n % VE) != 0 || !aligned) VE = 1;
     const bool need_pi = rq.mode == MODE_MPI || rq.mode == MODE_APPLY_PI || rq.mode == MODE_IMPROVE || rq.mode == MODE_POLICY_VALUE ||
                          rq.mode == MODE_SHARD_EVAL || rq.mode == MODE_SHARD_IMPROVE;
     const int64_t n_pad = (n + 3) & ~int64_t(3);
     size_t smem_v = (size_t)n_pad * 8 + (need_pi ? ((size_t)n * 4 + 15) / 16 * 16 : 0);
-    static const bool tma_env = [] {
-        const char* e = getenv("RMB_DENSE_TMA");
-        return !(e && e[0] == '0');
-    }();
     // a shared-memory copy of V (and pi) plus a 2-stage ring must fit; else V
     // and pi stay in global memory (L2-resident) on the TMA path
     const bool vglob = pr.vglobal || smem_v + 12288 + 2 * 33000 > pr.smem_optin;
     if (vglob) {
-        if (!(tma_env && !pr.no_tma && VE * psz == 16)) {
+        if (!(!pr.no_tma && VE * psz == 16)) {
             set_error("dense solver: n = " + std::to_string(n) + " needs " + std::to_string(smem_v) +
                       " B of shared memory for V (limit " + std::to_string(pr.smem_optin) +
                       "); larger n needs the TMA path (16-byte aligned rows: n % " + std::to_string(16 / psz) +
@@ -2142,59 +1656,23 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.plan[0].ng = ng_b;
     a.plan[1] = plan_chunks(n, rq.b, 1, 1, VE, sms, split_ok, 1, psz);
     a.plan[1].ng = 1;
-    // CTA-per-state rows mode for batches with >= 4 items (state groups) per SM
-    auto rows_plan = [&](Plan& p, int64_t cnt, int Ae) {
-        // measured: equal to the warp path at b = 1000 (tail 4x shorter, streaming
-        // ~9 % slower), slower at b = n -> opt-in
-        const char* e = getenv("RMB_DENSE_ROWS");
-        if (!(e && e[0] == '1')) return;
-        const int gst = std::max(1, kWarps / Ae);
-        if (pr.A > kRowsMax || p.cta || (cnt + gst - 1) / gst < 4LL * sms) return;
-        p.rows = 1;
-        p.C = 1;
-        p.Lc = (int)n;
-        p.ng = Ae;  // one (min, argmin) pair per state
-        p.redundant = cnt * (Ae == 1 ? 1 : 2) <= kRedundantMax ? 1 : 0;
-    };
-    Plan rp[3] = {a.plan[0], a.plan[1], a.plan[2]};
-    rows_plan(rp[0], rq.b, pr.A);
-    rows_plan(rp[1], rq.b, 1);
     // improvement (no V write): as few sub-batches as a bounded scratch allows
     const int64_t NAG4 = (pr.A + kAG - 1) / kAG;
     a.imp_sub = n * NAG4 * 2 <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / (2 * NAG4));
     a.plan[2] = plan_chunks(n, a.imp_sub, NAG4, pr.A, VE, sms, split_ok, kAG, psz);
     a.plan[2].ng = kAG;
-    rp[2] = a.plan[2];
-    rows_plan(rp[2], a.imp_sub, pr.A);
-    // the plans a launch uses must all be on one compute path (one kernel
-    // instantiation each): rows if every used plan qualifies, else warp / CTA
-    bool rows = false;
-    switch (rq.mode) {
-    case MODE_VI: case MODE_APPLY: case MODE_SHARD_MIN: rows = rp[0].rows; break;
-    case MODE_APPLY_PI: case MODE_SHARD_EVAL: case MODE_POLICY_VALUE: rows = rp[1].rows; break;
-    case MODE_IMPROVE: case MODE_SHARD_IMPROVE: rows = rp[2].rows; break;
-    default: rows = rp[1].rows && rp[2].rows; break;  // MPI
-    }
-    if (rows)
-        for (int q = 0; q < 3; ++q) a.plan[q] = rp[q];
-    a.path = rows ? kPathRows : a.plan[0].cta ? kPathCta : kPathWarp;
+    a.path = kPathWarp;
     // TMA ring path (default): 16-byte rows (VE full) and >= 2 ring stages next
     // to V / pi / the reduction scratch.  Chosen from (n, A, dtype, need_pi),
     // never from the shard, so every state's arithmetic is the same for any G.
     {
-        const bool tma_on = tma_env;
         const int64_t qs_tma = std::min<int64_t>(a.qs_cap, std::max<int64_t>(512, pr.A));  // >= A for the S-mode combine
         const size_t ring_off = (smem_v + (size_t)std::max<int64_t>(qs_tma, 0) * 8 + 127) / 128 * 128;
         const int64_t room = (int64_t)pr.smem_optin - (int64_t)ring_off - 16 - 2048;  // static smem
         // ring slots of kTmaStage bytes: NG row slots of one column window
         const int64_t piece = kTmaStage / psz, slot = kTmaStage;
         int nst = (int)std::min<int64_t>(kTmaMaxStages, std::max<int64_t>(0, room / (slot + kTmaPerStageX)));
-        if (const char* e = getenv("RMB_TMA_NST")) nst = std::min(nst, atoi(e));
-        a.tma_gmin = 1;
-        if (const char* e = getenv("RMB_TMA_G")) a.tma_gmin = std::max(1, atoi(e));
-        a.tma_hint = 1;
-        if (const char* e = getenv("RMB_TMA_HINT")) a.tma_hint = atoi(e);
-        if (tma_on && !pr.no_tma && a.path == kPathWarp && VE * psz == 16 && nst >= 2 && qs_tma >= pr.A) {
+        if (!pr.no_tma && a.path == kPathWarp && VE * psz == 16 && nst >= 2 && qs_tma >= pr.A) {
             a.path = vglob ? kPathTmaG : kPathTma;
             a.qs_cap = qs_tma;
             a.tma_off = (int64_t)ring_off;
@@ -2206,20 +1684,11 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
             a.imp_sub = n * pr.A <= (int64_t(1) << 22) ? n : std::max<int64_t>(1, (int64_t(1) << 22) / pr.A);
             a.plan[2] = plan_chunks(n, a.imp_sub, NAG4, pr.A, VE, sms, split_ok, kAG, psz);
             a.plan[2].ng = kAG;
-            static const int64_t red_max = [] {
-                const char* e = getenv("RMB_TMA_REDUNDANT_MAX");
-                return e ? (int64_t)atoll(e) : int64_t(2048);
-            }();
-            // items = contiguous chunks of a state's action-group range (or of
-            // its row pi(s)): C chunks per group, >= 8 items per SM per batch
-            static const int64_t ipsm = [] {  // target items per SM per batch
-                const char* e = getenv("RMB_TMA_IPSM");
-                return e ? std::max<int64_t>(1, atoll(e)) : int64_t(1);
-            }();
+            // partial volumes up to red_max doubles are combined redundantly by
+            // every CTA (one barrier); items = contiguous chunks of a state's
+            // action-group range (or of its row pi(s)): >= ipsm items per SM
+            const int64_t red_max = 2048, ipsm = 1;
             a.tma_static = 16;
-            a.tma_pf = 0;  // measured: slower (the prefetches compete with the ring's own loads)
-            if (const char* e = getenv("RMB_TMA_PF")) a.tma_pf = atoi(e);
-            if (const char* e = getenv("RMB_TMA_STATIC")) a.tma_static = atoi(e);
             const int64_t cnts[3] = {rq.b, rq.b, a.imp_sub};
             const int64_t grp[3] = {NAG, 1, NAG4};
             const int na_min = (pr.A % kAG) ? pr.A % kAG : kAG;
@@ -2251,8 +1720,10 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     L.lcap = std::max<int64_t>(rq.b, a.imp_sub);
     L.VE = VE;
 
+    const bool chunked = rq.chunked && (rq.mode == MODE_VI || rq.mode == MODE_APPLY) && rq.b < n;
+    const size_t part_bytes = (size_t)2 * a.part_stride * 8 + (size_t)L.lcap * 16 + 64;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess ||
-        pr.part.ensure((size_t)2 * a.part_stride * 8 + (size_t)L.lcap * 16 + 64) != cudaSuccess ||
+        pr.part.ensure(part_bytes + (chunked ? (size_t)n * 8 : 0)) != cudaSuccess ||
         pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("dense solver: workspace allocation failed");
         return RMB_ERR_OOM;
@@ -2262,6 +1733,7 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.lval = a.part + 2 * a.part_stride;
     a.larg = reinterpret_cast<int32_t*>(a.lval + L.lcap);
     a.scnt = reinterpret_cast<unsigned int*>(a.larg + L.lcap);
+    a.vnext = chunked ? reinterpret_cast<double*>(static_cast<char*>(pr.part.p) + part_bytes) : nullptr;
     unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
     a.bar = ctrl;                                          // [0], [32]
     a.err = reinterpret_cast<int*>(ctrl + 64);             // [64]
@@ -2269,11 +1741,6 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.prof = reinterpret_cast<long long*>(ctrl + 192);     // [192..196)
     a.wctr = reinterpret_cast<unsigned int*>(ctrl + 256);  // [256]
     a.gred = ctrl + 320;                                   // [320..336): global-V grid reductions
-    a.pctr = reinterpret_cast<unsigned int*>(ctrl + 260);  // [260]
-    {
-        const char* e = getenv("RMB_PREFETCH_MB");
-        a.pf_bytes = (int64_t)(e ? atof(e) : 0.0) * (1 << 20);  // measured: no gain at b = 1000 -> opt-in
-    }
     a.trace = trace_dev;
     a.trace_len = trace_len;
     a.chg = chg_dev;

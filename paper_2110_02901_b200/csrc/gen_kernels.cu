@@ -251,3 +251,23 @@ extern "C" rmb_status rmb_generate_grid(int64_t N, int64_t s0, int64_t s1, rmb_d
     }
     return RMB_OK;
 }
+
+namespace rmb {
+// Policy range check: *bad = 1 if some pi[s], s in [lo, hi), is outside [0, A)
+// (an out-of-range action would index a row beyond P).
+__global__ void check_policy_kernel(const int32_t* pi, int64_t lo, int64_t hi, int A, int* bad)
+{
+    for (int64_t s = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < hi; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = pi[s];
+        if (a < 0 || a >= A) atomicExch(bad, 1);
+    }
+}
+
+cudaError_t launch_check_policy(const int32_t* pi, int64_t lo, int64_t hi, int A, int* bad, cudaStream_t st)
+{
+    cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+    if (e != cudaSuccess || hi <= lo) return e;
+    check_policy_kernel<<<grid_for(hi - lo, 256), 256, 0, st>>>(pi, lo, hi, A, bad);
+    return cudaGetLastError();
+}
+}  // namespace rmb

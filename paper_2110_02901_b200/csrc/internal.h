@@ -40,6 +40,7 @@ struct SolveRequest {
     uint64_t seed = 0;
     int64_t k0 = 1;          // first sweep index
     bool identity = false;   // RMB_ORDER_IDENTITY
+    bool chunked = false;    // RMB_CHUNKED_T: VI* (T in chunks of b against the sweep-start values)
     double eps = -1.0;       // < 0: no convergence test
     int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
     int msweeps = 1;         // MPI evaluation sweeps per outer iteration
@@ -97,6 +98,18 @@ struct Problem {
     double* stage_V = nullptr;    // sharded solves: this rank's replica of V (device)
     int32_t* stage_pi = nullptr;  //                 this rank's pi (owned entries meaningful)
     int ell_K = 0;  // > 0: fixed-stride rows (ELL)
+    // multi-GPU layout consensus (shard.cu): the shape of the WHOLE problem, so
+    // that every shard picks the layout (and hence the arithmetic) a single
+    // handle over all rows would pick; g_set == false: use this handle's own
+    bool g_set = false;
+    int64_t g_nnz = 0, g_rows = 0;
+    int g_ell_K = 0;
+    bool g_aligned = true;
+    // A/B and test switches from the create flags (never needed for correctness)
+    bool sparse_full_grid = false;  // RMB_SPARSE_FULL_GRID
+    int sparse_wide = -1;           // RMB_SPARSE_WIDE_OFF (0) / _ON (1), -1 = automatic
+    bool shard_no_graph = false;    // RMB_SHARD_NO_GRAPH
+    int64_t last_graph_launches = 0;
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
     bool vglobal = false; // dense: RMB_DENSE_VGLOBAL (V and pi in global memory)
     cudaStream_t stream = nullptr;
@@ -129,6 +142,7 @@ rmb_status sparse_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t
 cudaError_t launch_partition(int64_t n, uint64_t seed, int64_t sweep, bool identity, uint32_t* perm,
                              cudaStream_t st);
 cudaError_t launch_validate(const Problem& pr, int* bad_dev, cudaStream_t st);
+cudaError_t launch_check_policy(const int32_t* pi, int64_t lo, int64_t hi, int A, int* bad, cudaStream_t st);
 
 // abi.cu
 void set_error(const std::string& msg);

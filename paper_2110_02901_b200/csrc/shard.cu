@@ -20,8 +20,10 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -43,6 +45,8 @@ struct NcclApi {
     ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -70,6 +74,8 @@ static NcclApi& nccl()
         RMB_SYM("ncclCommCount", CommCount);
         RMB_SYM("ncclCommUserRank", CommUserRank);
         RMB_SYM("ncclAllGather", AllGather);
+        RMB_SYM("ncclCommGetAsyncError", CommGetAsyncError);
+        RMB_SYM("ncclCommAbort", CommAbort);
         RMB_SYM("ncclGetErrorString", GetErrorString);
 #undef RMB_SYM
         x.ok = true;
@@ -82,6 +88,50 @@ static rmb_status nccl_fail(ncclResult_t r, const char* where)
 {
     set_error(std::string(where) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
     return RMB_ERR_NCCL;
+}
+
+// Wait for the stream while watching the communicator (failure
+// detection): a peer that died or an NCCL failure surfaces as an async error
+// -> the communicator is aborted (its kernels exit) and RMB_ERR_NCCL returned
+// instead of hanging in the exchange forever.  Also bounded in time.
+static rmb_status wait_stream(cudaStream_t st, ncclComm_t comm, const char* where)
+{
+    constexpr double kTimeoutS = 900.0;
+    if (!comm) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) return RMB_OK;
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return RMB_ERR_CUDA;
+    }
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+    const auto t0 = std::chrono::steady_clock::now();
+    unsigned spins = 0;
+    while (e == cudaSuccess) {
+        e = cudaEventQuery(ev);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) break;
+        e = cudaSuccess;
+        ncclResult_t ar = ncclSuccess;
+        ncclResult_t r = nccl().CommGetAsyncError(comm, &ar);
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (r != ncclSuccess || ar != ncclSuccess || el > kTimeoutS) {
+            nccl().CommAbort(comm);
+            cudaEventDestroy(ev);
+            set_error(std::string(where) + ": " +
+                      (el > kTimeoutS ? std::string("exchange timed out; communicator aborted")
+                                      : std::string("NCCL async error (") +
+                                            nccl().GetErrorString(r != ncclSuccess ? r : ar) +
+                                            "); communicator aborted"));
+            return RMB_ERR_NCCL;
+        }
+        if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    cudaEventDestroy(ev);
+    if (e == cudaSuccess) return RMB_OK;
+    set_error(std::string(where) + ": " + cudaGetErrorString(e));
+    return RMB_ERR_CUDA;
 }
 
 // ---------------------------------------------------------------- kernels
@@ -163,8 +213,8 @@ struct RankWs {
     char* recv;
     unsigned long long* resid;
     int* bad;
-    char* imp_send;  // improvement record: double resid | int64 changed | int64 status (24 B)
-    char* imp_recv;
+    char* imp_send;  // improvement record: double resid | int64 changed | int64 status | pad (32 B);
+    char* imp_recv;  //   also the layout-consensus record at the start of a solve
 };
 
 static int blocks_for(int64_t work) { return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8)); }
@@ -211,7 +261,7 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         RankWs& w = ws[r];
         w.pr = ranks[r];
         const size_t need = (size_t)n * 4 + (size_t)rec.cap * 4 + 256 + rec.chunk + (size_t)G * rec.chunk + 256 +
-                            256 + 24 * (size_t)G + 256;
+                            256 + 32 * (size_t)G + 256;
         if (w.pr->aux.ensure(need + 1024) != cudaSuccess) {
             set_error("sharded solve: workspace allocation failed");
             return RMB_ERR_OOM;
@@ -229,8 +279,53 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         w.recv = take((size_t)G * rec.chunk);
         w.resid = reinterpret_cast<unsigned long long*>(take(16));
         w.bad = reinterpret_cast<int*>(take(16));
-        w.imp_send = take(24);
-        w.imp_recv = take(24 * (size_t)G);
+        w.imp_send = take(32);
+        w.imp_recv = take(32 * (size_t)G);
+    }
+
+    // Layout consensus (every rank must pick the layout -- hence the summation
+    // order -- a single handle over ALL rows would pick): gather each rank's
+    // (nnz, rows, ELL width, 16-byte aligned) and combine.
+    {
+        std::vector<long long> all(4 * (size_t)G);
+        auto local_rec = [](const Problem& p, long long* r) {
+            r[0] = p.dense ? 0 : p.nnz;
+            r[1] = (p.row_end - p.row_begin) * (long long)p.A;
+            r[2] = p.dense ? 0 : p.ell_K;
+            r[3] = p.dense ? ((reinterpret_cast<uintptr_t>(p.P) & 15u) == 0)
+                           : ((uintptr_t)p.col % 16 == 0 && (uintptr_t)p.val % 16 == 0);
+        };
+        if (use_nccl) {
+            long long mine[4];
+            local_rec(p0, mine);
+            cudaError_t e = cudaMemcpyAsync(ws[0].imp_send, mine, 32, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) { set_error(std::string("layout consensus: ") + cudaGetErrorString(e)); return RMB_ERR_CUDA; }
+            ncclResult_t nr = nccl().AllGather(ws[0].imp_send, ws[0].imp_recv, 32, ncclUint8, comm, st);
+            if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather(layout)");
+            e = cudaMemcpyAsync(all.data(), ws[0].imp_recv, 32 * (size_t)G, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) { set_error(std::string("layout consensus: ") + cudaGetErrorString(e)); return RMB_ERR_CUDA; }
+            if (rmb_status s = wait_stream(st, comm, "layout consensus"); s != RMB_OK) return s;
+        } else {
+            for (int r = 0; r < G_local; ++r) local_rec(*ranks[r], all.data() + 4 * r);
+        }
+        long long nnz = 0, rows = 0, K = -1;
+        bool aligned = true;
+        for (int r = 0; r < G; ++r) {
+            nnz += all[4 * r];
+            rows += all[4 * r + 1];
+            aligned = aligned && all[4 * r + 3] != 0;
+            if (all[4 * r + 1] == 0) continue;  // a rank owning no rows does not constrain the ELL width
+            if (K < 0) K = all[4 * r + 2];
+            else if (all[4 * r + 2] != K) K = 0;  // widths differ: not ELL as a whole
+        }
+        K = std::max(K, 0LL);
+        for (int r = 0; r < G_local; ++r) {
+            ranks[r]->g_set = true;
+            ranks[r]->g_nnz = nnz;
+            ranks[r]->g_rows = rows;
+            ranks[r]->g_ell_K = (int)K;
+            ranks[r]->g_aligned = aligned;
+        }
     }
 
     auto check = [&](cudaError_t e, const char* where) -> rmb_status {
@@ -303,11 +398,16 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
     // launched before it), so after one eager sweep per kind (which also sizes
     // every workspace: no allocation may happen under capture) it is captured
     // once and replayed -- one host launch per sweep instead of ~5 per batch
-    // per rank.  Any capture failure falls back to the eager sequence (the
-    // same kernels).  RMB_SHARD_NO_GRAPH=1 disables.
+    // per rank.  The decision is the same on every rank (it depends on the
+    // create flag RMB_SHARD_NO_GRAPH and on nothing rank-local).  A capture
+    // failure in a logical group (one process, no NCCL) falls back to the eager
+    // sequence (the same kernels); under NCCL it is an error: the failed
+    // capture may already hold recorded collectives, and one rank replaying
+    // while another runs eagerly would desynchronise the communicator.
     const int64_t nbatches = (n + rq0.b - 1) / rq0.b;
     bool graph_on = true;
-    if (const char* e = getenv("RMB_SHARD_NO_GRAPH")) graph_on = atoi(e) == 0;
+    for (int r = 0; r < G_local; ++r) graph_on = graph_on && !ranks[r]->shard_no_graph;
+    int64_t graph_launches = 0;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int64_t gkern[2] = {0, 0};
     int warm[2] = {0, 0};
@@ -346,22 +446,20 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
                 gkern[kind] = launches - l0;
                 launches = l0;
                 if (s != RMB_OK || e2 != cudaSuccess || !gexec[kind]) {
-                    if (getenv("RMB_SHARD_GRAPH_DEBUG"))
-                        fprintf(stderr, "rmb shard graph capture failed (%s): %s\n", cudaGetErrorString(e2),
-                                s != RMB_OK ? rmb_last_error() : "");
                     gfail[kind] = true;
                     gexec[kind] = nullptr;
-                    cudaGetLastError();  // clear the capture error; run eagerly below
+                    cudaGetLastError();  // clear the capture error
+                    if (use_nccl) {
+                        set_error(std::string("sharded solve: CUDA graph capture of the sweep failed (") +
+                                  cudaGetErrorString(e2) + "); create the handles with RMB_SHARD_NO_GRAPH");
+                        return RMB_ERR_CUDA;
+                    }
                 }
             }
             if (gexec[kind]) {
-                if (getenv("RMB_SHARD_GRAPH_DEBUG") && warm[kind] == 1) {
-                    fprintf(stderr, "rmb shard graph in use (%s, %lld kernels per sweep)\n", eval ? "eval" : "min",
-                            (long long)gkern[kind]);
-                    ++warm[kind];
-                }
                 if (rmb_status s = check(cudaGraphLaunch(gexec[kind], st), "shard graph launch"); s != RMB_OK) return s;
                 launches += gkern[kind];
+                ++graph_launches;
                 return RMB_OK;
             }
         }
@@ -382,8 +480,8 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         int bb = 0;
         cudaError_t e = cudaMemcpyAsync(&rb, ws[0].resid, 8, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(&bb, ws[0].bad, 4, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return check(e, "shard residual");
+        if (rmb_status s = wait_stream(st, comm, "shard sweep"); s != RMB_OK) return s;
         memcpy(r_out, &rb, 8);
         *bad_out = bb != 0;
         return RMB_OK;
@@ -408,28 +506,28 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
                 e = cudaMemcpyAsync(ws[r].imp_send + 16, outs[r] + OUT_STATUS, 8, cudaMemcpyDeviceToDevice, st);
             if (e != cudaSuccess) return check(e, "shard improve record");
         }
-        std::vector<long long> all(3 * (size_t)G);
+        std::vector<long long> all(4 * (size_t)G);  // 32-byte records
         if (use_nccl) {
-            ncclResult_t nr = nccl().AllGather(ws[0].imp_send, ws[0].imp_recv, 24, ncclUint8, comm, st);
+            ncclResult_t nr = nccl().AllGather(ws[0].imp_send, ws[0].imp_recv, 32, ncclUint8, comm, st);
             if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather(improve)");
-            cudaError_t e = cudaMemcpyAsync(all.data(), ws[0].imp_recv, 24 * (size_t)G, cudaMemcpyDeviceToHost, st);
+            cudaError_t e = cudaMemcpyAsync(all.data(), ws[0].imp_recv, 32 * (size_t)G, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return check(e, "improve gather");
         } else {
             for (int r = 0; r < G_local; ++r) {
-                cudaError_t e = cudaMemcpyAsync(all.data() + 3 * r, ws[r].imp_send, 24, cudaMemcpyDeviceToHost, st);
+                cudaError_t e = cudaMemcpyAsync(all.data() + 4 * r, ws[r].imp_send, 24, cudaMemcpyDeviceToHost, st);
                 if (e != cudaSuccess) return check(e, "improve gather");
             }
         }
-        if (rmb_status s = check(cudaStreamSynchronize(st), "improve sync"); s != RMB_OK) return s;
+        if (rmb_status s = wait_stream(st, comm, "shard improve"); s != RMB_OK) return s;
         double rmax = 0.0;
         long long ch = 0;
         bool bad = false;
         for (int r = 0; r < G; ++r) {
             double d;
-            memcpy(&d, &all[3 * r], 8);
-            if (!std::isfinite(d) || all[3 * r + 2] == RMB_ERR_NONFINITE) bad = true;
+            memcpy(&d, &all[4 * r], 8);
+            if (!std::isfinite(d) || all[4 * r + 2] == RMB_ERR_NONFINITE) bad = true;
             rmax = std::max(rmax, d);
-            ch += all[3 * r + 1];
+            ch += all[4 * r + 1];
         }
         *r_out = rmax;
         *changed_out = ch;
@@ -499,7 +597,10 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
     res->changed = changed;
     res->ms = ms;
     res->launches = (int)launches;
-    for (int r = 0; r < G_local; ++r) ranks[r]->last_launches = launches;
+    for (int r = 0; r < G_local; ++r) {
+        ranks[r]->last_launches = launches;
+        ranks[r]->last_graph_launches = graph_launches;
+    }
     return RMB_OK;
 }
 

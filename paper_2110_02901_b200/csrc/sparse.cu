@@ -80,6 +80,7 @@ struct SparseArgs {
     double eps;
     int64_t max_iter;
     int msweeps;
+    int chunked;     // RMB_CHUNKED_T (VI*): every batch reads the sweep-start values
     uint32_t* perm;  // 3 * n
     unsigned long long* bar;
     int* err;
@@ -309,6 +310,9 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
         atomicExch(a.red + 8 + z, 0ull);
     }
     const bool single = a.b >= a.n;  // one batch per sweep: every state rewritten each batch
+    // chunked T (VI*): every chunk reads X_cur = the sweep-start
+    // values and writes X_next; no re-copies, X flips once per sweep
+    const bool chunked = !EVAL && a.chunked && !single;
     double rmax = 0.0;
     int bad = 0;
     for (int64_t lo = 0; lo < a.n; lo += a.b) {
@@ -367,10 +371,11 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
         x.prev_perm = single ? nullptr : perm;
         x.prev_lo = lo;
         x.prev_cnt = cnt;
-        x.prev_valid = !single;
-        ++x.gb;
+        x.prev_valid = !single && !chunked;
+        if (!chunked) ++x.gb;
         ++x.batches;
     }
+    if (chunked) ++x.gb;
     return read_slot(a, slot);
 }
 
@@ -574,18 +579,22 @@ static cudaError_t launch_sparse(const SparseArgs& a, int grid, bool wide, cudaS
 // arithmetic is the same on one GPU and on G.
 static void sparse_layout(const Problem& pr, int& mode, int& GS, int& GSE)
 {
-    const int64_t rows = (pr.row_end - pr.row_begin) * (int64_t)pr.A;
-    const double avg = rows > 0 ? (double)pr.nnz / (double)rows : 1.0;
-    const int64_t AK = (int64_t)pr.A * pr.ell_K;
-    const bool aligned = ((uintptr_t)pr.col % 16 == 0) && ((uintptr_t)pr.val % 16 == 0);
+    // shape of the whole problem: this handle's own rows on one GPU, the
+    // agreed global shape on a shard (shard.cu layout consensus)
+    const int64_t rows = pr.g_set ? pr.g_rows : (pr.row_end - pr.row_begin) * (int64_t)pr.A;
+    const int64_t nnz = pr.g_set ? pr.g_nnz : pr.nnz;
+    const int ellK = pr.g_set ? pr.g_ell_K : pr.ell_K;
+    const double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
+    const int64_t AK = (int64_t)pr.A * ellK;
+    const bool aligned = ((uintptr_t)pr.col % 16 == 0) && ((uintptr_t)pr.val % 16 == 0) && (!pr.g_set || pr.g_aligned);
     mode = SM_STRIDED;
     GS = 1, GSE = 1;
-    if (pr.ell_K > 0 && pr.ell_K % 8 == 0 && aligned && AK / 8 <= 32 && ((AK / 8) & (AK / 8 - 1)) == 0 &&
-        ((pr.ell_K / 8) & (pr.ell_K / 8 - 1)) == 0) {
+    if (ellK > 0 && ellK % 8 == 0 && aligned && AK / 8 <= 32 && ((AK / 8) & (AK / 8 - 1)) == 0 &&
+        ((ellK / 8) & (ellK / 8 - 1)) == 0) {
         mode = SM_VEC;
         GS = (int)(AK / 8);
-        GSE = pr.ell_K / 8;
-    } else if (pr.ell_K > 0 && pr.ell_K <= 8 && pr.A <= 32) {
+        GSE = ellK / 8;
+    } else if (ellK > 0 && ellK <= 8 && pr.A <= 32) {
         mode = SM_ROW;
         while (GS < pr.A) GS <<= 1;
         GSE = 1;  // B_{pi,b}: one row per state -> a lane per state
@@ -619,6 +628,7 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
+    a.chunked = rq.chunked ? 1 : 0;
     int mode, GS, GSE;
     sparse_layout(pr, mode, GS, GSE);
     a.GS = GS;
@@ -656,11 +666,10 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     // barrier per batch (measured: FrozenLake b=1 96 vs 125 ms, maze80 b=1
     // 5.96 vs 7.35 s; from ~10^4 nonzeros per batch the full grid wins)
     const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(rq.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
-    int grid = nnz_batch <= kSparseSmallBatchNnz ? 1 : pr.num_sms;
-    if (const char* e = getenv("RMB_SPARSE_GRID")) grid = std::max(1, std::min(pr.num_sms, atoi(e)));
+    int grid = nnz_batch <= kSparseSmallBatchNnz && !pr.sparse_full_grid ? 1 : pr.num_sms;
     // two CTAs per SM for B_b sweeps over large batches (see kSparseWideNnz)
     bool wide = grid > 1 && (rq.mode == MODE_VI || rq.mode == MODE_APPLY) && nnz_batch >= kSparseWideNnz;
-    if (const char* e = getenv("RMB_SPARSE_WIDE")) wide = grid > 1 && atoi(e) != 0;
+    if (pr.sparse_wide >= 0) wide = grid > 1 && pr.sparse_wide == 1;
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
             ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, wide, st)

@@ -21,13 +21,13 @@ def tdev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def shards(P, c, gamma, G, comm=None):
+def shards(P, c, gamma, G, comm=None, flags=0):
     n = P.shape[0]
     out = []
     for g in range(G):
         r0, r1 = rmb.shard_range(n, G, g)
         out.append(rmb.Problem.dense(tdev(P[r0:r1]), tdev(c[r0:r1]), gamma, n=n, row_range=(r0, r1),
-                                     nccl_comm=comm))
+                                     nccl_comm=comm, flags=flags))
     return out
 
 
@@ -91,14 +91,14 @@ def test_nccl_single_rank_path():
 
 
 # ------------------------------------------------------------- sparse shards
-def csr_shards(rp, col, val, c, n, A, gamma, G, comm=None):
+def csr_shards(rp, col, val, c, n, A, gamma, G, comm=None, flags=0):
     """Owned-row slices of a CSR instance: row_ptr rebased to 0, col kept global."""
     out = []
     for g in range(G):
         r0, r1 = rmb.shard_range(n, G, g)
         e0, e1 = rp[r0 * A], rp[r1 * A]
         out.append(rmb.Problem.csr(n, A, tdev(rp[r0 * A:r1 * A + 1] - e0), tdev(col[e0:e1]), tdev(val[e0:e1]),
-                                   tdev(c[r0:r1]), gamma, row_range=(r0, r1), nccl_comm=comm))
+                                   tdev(c[r0:r1]), gamma, row_range=(r0, r1), nccl_comm=comm, flags=flags))
     return out
 
 
@@ -171,27 +171,66 @@ def test_sparse_nccl_single_rank_path():
 
 
 @pytest.mark.parametrize("sparse", [False, True])
-def test_graph_replayed_sweeps_equal_eager(sparse, monkeypatch):
+def test_graph_replayed_sweeps_equal_eager(sparse):
     """The sharded sweep's batch sequence replayed from a CUDA graph (default)
-    equals the eager launch sequence (RMB_SHARD_NO_GRAPH=1) bit for bit, VI and MPI."""
+    equals the eager launch sequence (RMB_SHARD_NO_GRAPH) bit for bit, VI and
+    MPI -- and the graph really was replayed (rmb_last_graph_launches)."""
     if sparse:
         N, A, gamma = 16, 4, 0.95
         n = N * N
         rp, col, val, c = gen.grid(N, dtype=np.float32)
-        make = lambda: csr_shards(rp, col, val, c, n, A, gamma, 3)  # noqa: E731
+        make = lambda f: csr_shards(rp, col, val, c, n, A, gamma, 3, flags=f)  # noqa: E731
     else:
         n, A, gamma = 240, 6, 0.95
         P, c = gen.dense(n, A, 12, dtype=np.float32)
-        make = lambda: shards(P, c, gamma, 3)  # noqa: E731
+        make = lambda f: shards(P, c, gamma, 3, flags=f)  # noqa: E731
     b = 23
-    monkeypatch.setenv("RMB_SHARD_NO_GRAPH", "1")
-    ev = rmb.vi_group(make(), b, seed=6, eps=1e-9, max_sweeps=50)
-    em = rmb.mpi_group(make(), b, 4, seed=6, eps=1e-9)
-    monkeypatch.setenv("RMB_SHARD_NO_GRAPH", "0")
-    gv = rmb.vi_group(make(), b, seed=6, eps=1e-9, max_sweeps=50)
-    gm = rmb.mpi_group(make(), b, 4, seed=6, eps=1e-9)
+    he, hg = make(rmb.SHARD_NO_GRAPH), make(0)
+    ev = rmb.vi_group(he, b, seed=6, eps=1e-9, max_sweeps=50)
+    assert he[0].last_graph_launches() == 0
+    gv = rmb.vi_group(hg, b, seed=6, eps=1e-9, max_sweeps=50)
+    assert hg[0].last_graph_launches() == gv.stats.sweeps - 1  # every sweep after the eager warm-up one
+    em = rmb.mpi_group(he, b, 4, seed=6, eps=1e-9)
+    gm = rmb.mpi_group(hg, b, 4, seed=6, eps=1e-9)
+    assert hg[0].last_graph_launches() > 0
     for e, g in ((ev, gv), (em, gm)):
         assert e.stats.sweeps == g.stats.sweeps and e.stats.batches == g.stats.batches
         assert np.array_equal(e.trace, g.trace)
         assert np.array_equal(e.V.cpu().numpy(), g.V.cpu().numpy())
         assert np.array_equal(e.pi.cpu().numpy(), g.pi.cpu().numpy())
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sparse_skewed_shards_keep_single_gpu_layout(G):
+    """Shards whose own row lengths differ from the whole problem's (rank 0:
+    long ragged rows, the rest: short rows) must still use the layout -- and
+    hence the summation order -- of one handle over all rows (layout
+    consensus): bitwise equal V, pi, trace."""
+    n, A, gamma, b = 240, 3, 0.9, 29
+    rng = np.random.default_rng(17)
+    r0, r1 = rmb.shard_range(n, G, 0)
+    lens = np.where(np.arange(n * A) < r1 * A, rng.integers(30, 41, n * A), rng.integers(1, 4, n * A))
+    rp = np.zeros(n * A + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.random(rp[-1]) + 0.01
+    for r in range(n * A):
+        val[rp[r]:rp[r + 1]] /= val[rp[r]:rp[r + 1]].sum()
+    c = rng.random((n, A))
+    ref = rmb.Problem.csr(n, A, tdev(rp), tdev(col), tdev(val), tdev(c), gamma).vi(b, seed=3, eps=1e-9,
+                                                                                  max_sweeps=80)
+    sol = rmb.vi_group(csr_shards(rp, col, val, c, n, A, gamma, G), b, seed=3, eps=1e-9, max_sweeps=80)
+    assert sol.stats.sweeps == ref.stats.sweeps
+    assert np.array_equal(sol.trace, ref.trace)
+    assert np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi.cpu().numpy())
+
+
+def test_group_rejects_out_of_range_given_policy():
+    n, A, gamma = 120, 4, 0.9
+    P, c = gen.dense(n, A, 2, dtype=np.float32)
+    pi = np.zeros(n, np.int32)
+    pi[-1] = A
+    with pytest.raises(rmb.RmbError) as e:
+        rmb.mpi_group(shards(P, c, gamma, 2), 10, 2, pi=tdev(pi), pi_given=True)
+    assert e.value.status == rmb.INVALID_ARG

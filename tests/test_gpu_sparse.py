@@ -2,7 +2,7 @@
 
 Same bar as test_gpu_dense.py: single applications to 1e-11 * max(1,|V|),
 solves to 1e-9 * max(1,|V|), identical sweep counts and residual traces,
-policies bit-exact where the Q-gap exceeds 1e-6.
+policies bit-exact where the Q-gap exceeds 1e-9.
 """
 import numpy as np
 import pytest
@@ -88,7 +88,7 @@ def test_apply_matches_oracle(name, bfrac, policy):
     assert_close(Vg.cpu().numpy(), Vo, 1e-11)
     assert abs(rg - ro) <= 1e-11 * max(1.0, np.abs(Vo).max())
     gap = qgap(m, Vo)
-    mask = gap > 1e-6 if gap is not None else np.ones(m.n, bool)
+    mask = gap > 1e-9 if gap is not None else np.ones(m.n, bool)
     assert np.array_equal(argg.cpu().numpy()[mask], argo[mask])
 
 
@@ -114,7 +114,7 @@ def test_config4_shape_mpi(b, msweeps):
     assert np.array_equal(sol.changed, ref.changed)
     assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
     gap = qgap(m, ref.V)
-    assert np.array_equal(sol.pi.cpu().numpy()[gap > 1e-6], ref.pi[gap > 1e-6])
+    assert np.array_equal(sol.pi.cpu().numpy()[gap > 1e-9], ref.pi[gap > 1e-9])
 
 
 def test_ragged_vi_and_improve():
@@ -201,22 +201,73 @@ def test_policy_value_on_grid():
         assert abs(sol.trace[k - 1] - ro) <= 1e-11 * max(1.0, np.abs(V).max())
 
 
+def _instance_with_flags(name, flags):
+    """Rebuild INSTANCES[name]'s CSR arrays into a handle created with `flags`."""
+    m, _ = INSTANCES[name]()
+    prob = rmb.Problem.csr(m.n, m.A, tdev(m.row_ptr), tdev(m.col), tdev(m.val), tdev(m.c), m.gamma, flags=flags)
+    return m, prob
+
+
 @pytest.mark.parametrize("name", ["ell32", "grid", "ragged"])
 @pytest.mark.parametrize("b", [1, 37, None])
-def test_two_ctas_per_sm_variant_is_bitwise_default(name, b, monkeypatch):
+def test_two_ctas_per_sm_variant_is_bitwise_default(name, b):
     """The MINB = 2 build of the persistent solver (2 CTAs/SM, chosen for large
     batches) forced at small sizes: V, pi and trace bitwise = the MINB = 1 build
     (grid-free per-state arithmetic), and the oracle within the solve bar."""
-    m, prob = INSTANCES[name]()
+    m, p1 = _instance_with_flags(name, rmb.SPARSE_FULL_GRID | rmb.SPARSE_WIDE_OFF)
+    _, p2 = _instance_with_flags(name, rmb.SPARSE_FULL_GRID | rmb.SPARSE_WIDE_ON)
     b = m.n if b is None else b
-    monkeypatch.setenv("RMB_SPARSE_GRID", "148")  # full grid even for tiny batches
-    monkeypatch.setenv("RMB_SPARSE_WIDE", "0")
-    one = prob.vi(b, seed=5, eps=1e-8, max_sweeps=40)
-    monkeypatch.setenv("RMB_SPARSE_WIDE", "1")
-    two = prob.vi(b, seed=5, eps=1e-8, max_sweeps=40)
+    one = p1.vi(b, seed=5, eps=1e-8, max_sweeps=40)
+    two = p2.vi(b, seed=5, eps=1e-8, max_sweeps=40)
     assert one.stats.sweeps == two.stats.sweeps
     assert np.array_equal(one.trace, two.trace)
     assert np.array_equal(one.V.cpu().numpy(), two.V.cpu().numpy())
     assert np.array_equal(one.pi.cpu().numpy(), two.pi.cpu().numpy())
     ref = oracle.vi(m, b, seed=5, eps=1e-8, max_sweeps=40)
     assert_close(two.V.cpu().numpy(), ref.V, 1e-9)
+
+
+# ------------------------------------------------------------ VI* (P:L577)
+@pytest.mark.parametrize("name", list(INSTANCES))
+@pytest.mark.parametrize("bfrac", [0, 0.013, 0.25])
+def test_chunked_T_apply_is_bellman(name, bfrac):
+    """RMB_CHUNKED_T: T in chunks of b states against the sweep-start values.
+    Bitwise equal to the one-batch sweep B_n on the device (both read only the
+    old values; per-state arithmetic identical) and to the oracle's chunked T."""
+    m, prob = INSTANCES[name]()
+    b = max(1, int(bfrac * m.n))
+    V0 = np.random.default_rng(1).random(m.n) * 10
+    Vc, ac, rc = prob.apply(b, 4, 2, tdev(V0), chunked=True)
+    Vn, an, rn = prob.apply(m.n, 4, 2, tdev(V0))
+    assert np.array_equal(Vc.cpu().numpy(), Vn.cpu().numpy()) and np.array_equal(ac.cpu().numpy(), an.cpu().numpy())
+    assert rc == rn
+    Vo, ao, ro = oracle.sweep_chunked(m, V0, b, oracle.partition(m.n, 4, 2))
+    assert_close(Vc.cpu().numpy(), Vo, 1e-11)
+
+
+@pytest.mark.parametrize("name", ["ell32", "grid"])
+def test_vi_star_solve_equals_bellman_vi(name):
+    m, prob = INSTANCES[name]()
+    b = max(1, m.n // 7)
+    star = prob.vi(b, seed=2, eps=1e-8, max_sweeps=3000, chunked=True)
+    bell = prob.vi(m.n, seed=2, eps=1e-8, max_sweeps=3000)
+    assert star.stats.sweeps == bell.stats.sweeps and np.array_equal(star.trace, bell.trace)
+    assert np.array_equal(star.V.cpu().numpy(), bell.V.cpu().numpy())
+    assert star.stats.batches == star.stats.sweeps * -(-m.n // b)  # one barrier per chunk
+    ref = oracle.vi(m, b, seed=2, eps=1e-8, max_sweeps=3000, chunked=True)
+    assert star.stats.sweeps == ref.sweeps
+    assert_close(star.V.cpu().numpy(), ref.V, 1e-9)
+
+
+def test_apply_rejects_out_of_range_policy():
+    m, prob = INSTANCES["grid"]()
+    pi = np.zeros(m.n, np.int32)
+    pi[m.n // 2] = m.A  # one action past the end
+    with pytest.raises(rmb.RmbError) as e:
+        prob.apply(10, 1, 1, tdev(np.zeros(m.n)), pi=tdev(pi))
+    assert e.value.status == rmb.INVALID_ARG
+    pi[m.n // 2] = -1
+    with pytest.raises(rmb.RmbError):
+        prob.policy_value(tdev(pi))
+    # the handle is still usable afterwards (no device fault)
+    assert prob.vi(m.n, eps=1e-6).status == rmb.OK
