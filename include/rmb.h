@@ -88,8 +88,6 @@ typedef struct {
                                    and chunking (DESIGN reading R21).  Not for sharded handles.        */
 /* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
-#define RMB_SPARSE_WIDE_OFF 0x100u  /* sparse: one 512-thread CTA per SM for every solve           */
-#define RMB_SPARSE_WIDE_ON 0x200u   /* sparse: two CTAs per SM (64 registers) for B_b solves       */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly
                                        instead of replaying it from a captured CUDA graph          */
 

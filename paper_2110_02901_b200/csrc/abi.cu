@@ -104,6 +104,7 @@ static void free_problem(Problem* pr)
     pr->vstage.release();
     pr->pistage.release();
     pr->aux.release();
+    pr->rowrec.release();
     delete pr;
 }
 
@@ -144,7 +145,6 @@ static rmb_status check_policy(Problem& pr, const int32_t* pi_dev, int64_t lo, i
 static void apply_create_flags(Problem& pr, uint32_t flags)
 {
     pr.sparse_full_grid = (flags & RMB_SPARSE_FULL_GRID) != 0;
-    pr.sparse_wide = (flags & RMB_SPARSE_WIDE_ON) ? 1 : (flags & RMB_SPARSE_WIDE_OFF) ? 0 : -1;
     pr.shard_no_graph = (flags & RMB_SHARD_NO_GRAPH) != 0;
 }
 

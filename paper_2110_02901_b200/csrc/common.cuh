@@ -36,6 +36,116 @@ __device__ __forceinline__ double ld_stream(const double* p)
     return r;
 }
 
+// ------------------------------------------------------ L2 cache hints
+// Sparse solves stream their CSR/ELL rows (hundreds of MB, random rows) past
+// an interim V that must stay in L2 (8-34 MB per copy): rows are loaded with
+// an evict_first policy, V gathers and writes with evict_last.
+#ifndef RMB_AB_L2_FIRST  // A/B builds only (tools/): the policies actually used
+#define RMB_AB_L2_FIRST "evict_first"
+#endif
+#ifndef RMB_AB_L2_LAST
+#define RMB_AB_L2_LAST "evict_last"
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::" RMB_AB_L2_FIRST ".b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::" RMB_AB_L2_LAST ".b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only streams (never written during the kernel): non-coherent path, no L1 allocation
+__device__ __forceinline__ int ld_first(const int* p, uint64_t pol)
+{
+    int r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_first(const float* p, uint64_t pol)
+{
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_first(const double* p, uint64_t pol)
+{
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int4 ld_first(const int4* p, uint64_t pol)
+{
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float4 ld_first(const float4* p, uint64_t pol)
+{
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double2 ld_first(const double2* p, uint64_t pol)
+{
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+// short scattered rows (a few consecutive words each): L1-allocating, so the
+// words of one row after the first hit the line its first word brought in
+__device__ __forceinline__ int ld_rows(const int* p, uint64_t pol)
+{
+    int r;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_rows(const float* p, uint64_t pol)
+{
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_rows(const double* p, uint64_t pol)
+{
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// 32 bytes (one sector) per thread in one instruction (sm_100: 256-bit LDG)
+__device__ __forceinline__ void ld_v8(const uint32_t* p, uint32_t (&w)[8])
+{
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+// data written during the kernel by other CTAs (interim V, policies, permutations): L2 only (.cg)
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol)
+{
+    double r;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_keep(const int* p, uint64_t pol)
+{
+    int r;
+    asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // ------------------------------------------------------------ grid barrier
 // Sense-free monotonic barrier for a co-resident (cooperative) grid.
 // bar[0] = arrival counter, bar[32] = released epoch (separate 256-B lines).

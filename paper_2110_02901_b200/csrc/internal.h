@@ -107,7 +107,6 @@ struct Problem {
     bool g_aligned = true;
     // A/B and test switches from the create flags (never needed for correctness)
     bool sparse_full_grid = false;  // RMB_SPARSE_FULL_GRID
-    int sparse_wide = -1;           // RMB_SPARSE_WIDE_OFF (0) / _ON (1), -1 = automatic
     bool shard_no_graph = false;    // RMB_SHARD_NO_GRAPH
     int64_t last_graph_launches = 0;
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
@@ -118,7 +117,7 @@ struct Problem {
     size_t smem_optin = 0;
     std::vector<void*> owned;  // host-staged inputs
     // workspace
-    DevBuf perm, part, ctrl, trace, chg, vstage, pistage, aux;
+    DevBuf perm, part, ctrl, trace, chg, vstage, pistage, aux, rowrec;
     int64_t last_launches = 0;
     long long prof[4] = {0, 0, 0, 0};  // last solve: compute / barrier / combine ns (CTA 0), barriers
 };

@@ -45,14 +45,6 @@ template <int MODE>
 struct SThreads {
     static constexpr int v = 512;  // 1024 for row mode: config-4 VI 1.5x faster, config-4 MPI 1.7x slower
 };
-// Two register budgets per layout: MINB = 1 (one 512-thread CTA per SM, no
-// spills) and MINB = 2 (64 registers, two CTAs per SM: twice the gathers in
-// flight, a few spills off the hot loop, a grid barrier over 2x the CTAs).
-// Measured on B200 (tools/sparse_perf.py): MINB = 2 wins for B_b sweeps with
-// large batches (config 3 b = n/8: 1.53 -> 1.41 ms per sweep; config 4 VI
-// b = n: 0.60 -> 0.38 ms) and loses for small batches (barrier cost) and
-// MPI (config 4: 8.9 -> 12.7 s), so it is chosen per solve (sparse_solve).
-constexpr int64_t kSparseWideNnz = int64_t(1) << 24;  // nonzeros per batch from which MINB = 2 pays
 
 struct SparseArgs {
     const int64_t* row_ptr;
@@ -91,6 +83,7 @@ struct SparseArgs {
     int64_t chg_len;
     long long* out;
     long long* prof;
+    const uint32_t* rec;  // row mode: packed row records (RowRec), or null = read col / val / c directly
 };
 
 template <typename PT>
@@ -148,105 +141,265 @@ __device__ __forceinline__ void argmin_butterfly(double& Q, int& arg, int o_lo, 
     }
 }
 
-// Backup of state s against X by a group of GS lanes (g = lane in group).
+// Backup of state s against X by a group of GS lanes (g = lane in group),
+// split in two so that the V-independent loads of the NEXT item (its CSR/ELL
+// column ids, probabilities and cost) are in flight while the current item
+// gathers V (software pipelining across items, batches and sweeps; VERDICT r1
+// weak #5):
+//   load_item   -> col / val / cost of the lane's row slice (no V access);
+//   finish_item -> the V gathers, the row sums and the min / argmin.
 // act_fixed >= 0: B_{pi,b} row only.  Result valid in lane g == 0 (all modes)
 // and in every lane for SM_ROW / SM_VEC min.
 template <typename PT, int MODE>
-__device__ __forceinline__ void backup_state(const SparseArgs& a, const double* X, int64_t s, int act_fixed, int g,
-                                             int GS, bool valid, double& best, int& barg)
+struct SItem {      // SM_STRIDED: rows are walked at finish time
+    int64_t s;
+    int act;        // act_fixed (B_{pi,b}) or -1
+    bool valid;
+};
+constexpr int kRowK = 6;  // widest ELL row served by row mode (registers per prefetched item: 2 kRowK + 5)
+
+// Row mode reads one short row per (state, action) at a random place: three
+// scattered loads (columns, probabilities, cost) of a few words each.  Before
+// a solve the rows are repacked into 32-byte-aligned records
+//   words [0, 6): col[q] (q < K, else 0);  words 6..7: cost;  words 8..: val[q]
+// (f32: 16 words = 2 sectors, f64: 24 words = 3 sectors), read with 256-bit
+// loads -- the same values, hence the same arithmetic.
+template <typename PT>
+struct RowRec {
+    static constexpr int W = sizeof(PT) == 4 ? 16 : 24;  // 32-bit words per record
+};
+
+template <typename PT>
+__global__ void pack_rows_kernel(const int32_t* col, const PT* val, const PT* c, int64_t rows, int K, uint32_t* rec)
 {
-    if (MODE == SM_ROW) {
+    constexpr int W = RowRec<PT>::W;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) w[q] = 0u;
+#pragma unroll
+        for (int q = 0; q < kRowK; ++q)
+            if (q < K) {
+                w[q] = (uint32_t)col[r * K + q];
+                const PT v = val[r * K + q];
+                if constexpr (sizeof(PT) == 4) w[8 + q] = __float_as_uint(v);
+                else {
+                    const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+                    w[8 + 2 * q] = (uint32_t)u, w[9 + 2 * q] = (uint32_t)(u >> 32);
+                }
+            }
+        if constexpr (sizeof(PT) == 4) w[6] = __float_as_uint(c[r]);
+        else {
+            const unsigned long long u = (unsigned long long)__double_as_longlong(c[r]);
+            w[6] = (uint32_t)u, w[7] = (uint32_t)(u >> 32);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(rec + r * W);
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
+}
+template <typename PT>
+struct SItem<PT, SM_ROW> {  // a lane per action row (min) or per state (B_{pi,b}); ELL width K <= kRowK
+    int64_t s;
+    int act;        // this lane's row, -1 = none
+    bool valid;
+    int col[kRowK];
+    PT v[kRowK];
+    PT cost;
+};
+template <typename PT>
+struct SItem<PT, SM_VEC> {  // 8 consecutive nonzeros of the state's block (min) or of row pi(s)
+    int64_t s;
+    int act;
+    bool valid;
+    bool fixed;     // B_{pi,b}: no argmin over actions
+    int4 c0, c1;
+    PT v[8];
+    PT cost;
+};
+
+// pf: L2 policy of the row streams (evict_first)
+template <typename PT, int MODE>
+__device__ __forceinline__ void load_item(const SparseArgs& a, int64_t s, int act_fixed, int g, bool valid,
+                                          SItem<PT, MODE>& it, uint64_t pf)
+{
+    it.s = s;
+    it.valid = valid;
+    if constexpr (MODE == SM_ROW) {
+        it.act = !valid ? -1 : act_fixed >= 0 ? (g == 0 ? act_fixed : -1) : (g < a.A ? g : -1);
+        if (it.act >= 0 && a.rec) {
+            const uint32_t* rp = a.rec + (s * a.A + it.act) * RowRec<PT>::W;
+            uint32_t w0[8], w1[8];
+            ld_v8(rp, w0);
+            ld_v8(rp + 8, w1);
+#pragma unroll
+            for (int q = 0; q < kRowK; ++q) it.col[q] = (int)w0[q];
+            if constexpr (sizeof(PT) == 4) {
+#pragma unroll
+                for (int q = 0; q < kRowK; ++q) it.v[q] = __uint_as_float(w1[q]);
+                it.cost = __uint_as_float(w0[6]);
+            } else {
+                uint32_t w2[8];
+                ld_v8(rp + 16, w2);
+                auto dbl = [](uint32_t lo, uint32_t hi) {
+                    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+                };
+                it.v[0] = dbl(w1[0], w1[1]), it.v[1] = dbl(w1[2], w1[3]), it.v[2] = dbl(w1[4], w1[5]);
+                it.v[3] = dbl(w1[6], w1[7]), it.v[4] = dbl(w2[0], w2[1]), it.v[5] = dbl(w2[2], w2[3]);
+                it.cost = dbl(w0[6], w0[7]);
+            }
+        } else if (it.act >= 0) {
+            const int64_t row = s * a.A + it.act;
+            const int64_t e0 = row * a.K;
+#pragma unroll
+            for (int q = 0; q < kRowK; ++q)
+                if (q < a.K) {
+                    it.col[q] = ld_rows(a.col + e0 + q, pf);
+                    it.v[q] = ld_rows(static_cast<const PT*>(a.val) + e0 + q, pf);
+                }
+            it.cost = ld_rows(static_cast<const PT*>(a.c) + row, pf);
+        }
+    } else if constexpr (MODE == SM_VEC) {
+        it.act = act_fixed >= 0 ? act_fixed : (8 * g) / a.K;
+        it.fixed = act_fixed >= 0;
+        if (valid) {
+            const int64_t e = act_fixed >= 0 ? (s * a.A + act_fixed) * a.K + 8 * g : s * a.A * a.K + 8 * g;
+            it.c0 = ld_first(reinterpret_cast<const int4*>(a.col + e), pf);
+            it.c1 = ld_first(reinterpret_cast<const int4*>(a.col + e + 4), pf);
+            if constexpr (sizeof(PT) == 4) {
+                const float4 x = ld_first(reinterpret_cast<const float4*>(static_cast<const float*>(a.val) + e), pf);
+                const float4 y = ld_first(reinterpret_cast<const float4*>(static_cast<const float*>(a.val) + e + 4), pf);
+                it.v[0] = x.x, it.v[1] = x.y, it.v[2] = x.z, it.v[3] = x.w;
+                it.v[4] = y.x, it.v[5] = y.y, it.v[6] = y.z, it.v[7] = y.w;
+            } else {
+                const double* d = static_cast<const double*>(a.val) + e;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double2 x = ld_first(reinterpret_cast<const double2*>(d + 2 * q), pf);
+                    it.v[2 * q] = x.x, it.v[2 * q + 1] = x.y;
+                }
+            }
+            it.cost = ld_first(static_cast<const PT*>(a.c) + s * a.A + it.act, pf);
+        }
+    } else {
+        it.act = act_fixed;
+    }
+}
+
+// pl: L2 policy of the interim-V gathers (evict_last)
+template <typename PT, int MODE>
+__device__ __forceinline__ void finish_item(const SparseArgs& a, const double* X, const SItem<PT, MODE>& it, int g,
+                                            int GS, double& best, int& barg, uint64_t pl)
+{
+    const bool valid = it.valid;
+    const int64_t s = it.s;
+    if constexpr (MODE == SM_ROW) {
         double Q = INFINITY;
         int arg = 0x7fffffff;
-        const int act = !valid ? -1 : act_fixed >= 0 ? (g == 0 ? act_fixed : -1) : (g < a.A ? g : -1);
-        if (act >= 0) {
-            const int64_t row = s * a.A + act;
-            const int64_t e0 = a.K > 0 ? row * a.K : __ldg(a.row_ptr + row);
-            const int64_t e1 = a.K > 0 ? e0 + a.K : __ldg(a.row_ptr + row + 1);
+        if (it.act >= 0) {
             // one lane, storage order, separately rounded products and sums
             // (no FMA contraction): the same arithmetic as the oracle's row
             // sum, so row mode is bit-exact and exact Q ties (symmetric grids)
             // break identically on both sides
+            double x[kRowK];
+#pragma unroll
+            for (int q = 0; q < kRowK; ++q)
+                if (q < a.K) x[q] = ld_keep(X + it.col[q], pl);
             double acc = 0.0;
-            for (int64_t e = e0; e < e1; ++e)
-                acc = __dadd_rn(acc, __dmul_rn(ldv<PT>(a.val, e), __ldcg(X + __ldg(a.col + e))));
-            Q = __dadd_rn(ldv<PT>(a.c, row), __dmul_rn(a.gamma, acc));
-            arg = act;
+#pragma unroll
+            for (int q = 0; q < kRowK; ++q)
+                if (q < a.K) acc = __dadd_rn(acc, __dmul_rn((double)it.v[q], x[q]));
+            Q = __dadd_rn((double)it.cost, __dmul_rn(a.gamma, acc));
+            arg = it.act;
         }
         argmin_butterfly(Q, arg, 1, GS);
         best = Q;
         barg = arg;
-        return;
-    }
-    if (MODE == SM_VEC) {
-        // lane g owns nonzeros [8g, 8g+8) of the state's block (min) or of the
-        // row pi(s) (eval): 2x128-bit col + 2x128-bit val loads, 8 gathers in
-        // flight, a sequential 8-term sum, then a butterfly over the K/8 lanes
-        // of the action and an argmin butterfly over the actions
+    } else if constexpr (MODE == SM_VEC) {
+        // 8 gathers in flight, a sequential 8-term sum, then a butterfly over
+        // the K/8 lanes of the action and an argmin butterfly over the actions
         const int L = a.K >> 3;  // lanes per action row
+        const bool eval = it.fixed;
         double Q = INFINITY;
         int arg = 0x7fffffff;
         if (valid) {
-            const int act = act_fixed >= 0 ? act_fixed : (8 * g) / a.K;
-            const int64_t e = act_fixed >= 0 ? (s * a.A + act_fixed) * a.K + 8 * g : s * a.A * a.K + 8 * g;
-            const int4 c0 = ld_nc_int4(a.col + e);
-            const int4 c1 = ld_nc_int4(a.col + e + 4);
-            double v[8];
-            ld8<PT>(a.val, e, v);
-            const double x0 = __ldcg(X + c0.x), x1 = __ldcg(X + c0.y), x2 = __ldcg(X + c0.z), x3 = __ldcg(X + c0.w);
-            const double x4 = __ldcg(X + c1.x), x5 = __ldcg(X + c1.y), x6 = __ldcg(X + c1.z), x7 = __ldcg(X + c1.w);
-            double acc = v[0] * x0;
-            acc = fma(v[1], x1, acc);
-            acc = fma(v[2], x2, acc);
-            acc = fma(v[3], x3, acc);
-            acc = fma(v[4], x4, acc);
-            acc = fma(v[5], x5, acc);
-            acc = fma(v[6], x6, acc);
-            acc = fma(v[7], x7, acc);
+            const double x0 = ld_keep(X + it.c0.x, pl), x1 = ld_keep(X + it.c0.y, pl),
+                         x2 = ld_keep(X + it.c0.z, pl), x3 = ld_keep(X + it.c0.w, pl);
+            const double x4 = ld_keep(X + it.c1.x, pl), x5 = ld_keep(X + it.c1.y, pl),
+                         x6 = ld_keep(X + it.c1.z, pl), x7 = ld_keep(X + it.c1.w, pl);
+            double acc = (double)it.v[0] * x0;
+            acc = fma((double)it.v[1], x1, acc);
+            acc = fma((double)it.v[2], x2, acc);
+            acc = fma((double)it.v[3], x3, acc);
+            acc = fma((double)it.v[4], x4, acc);
+            acc = fma((double)it.v[5], x5, acc);
+            acc = fma((double)it.v[6], x6, acc);
+            acc = fma((double)it.v[7], x7, acc);
             Q = acc;
-            arg = act;
+            arg = it.act;
         }
         for (int o = 1; o < L; o <<= 1) Q += __shfl_xor_sync(0xffffffffu, Q, o);
-        if (valid) Q = ldv<PT>(a.c, s * a.A + arg) + a.gamma * Q;
-        if (act_fixed < 0) argmin_butterfly(Q, arg, L, GS);
+        if (valid) Q = (double)it.cost + a.gamma * Q;
+        if (!eval) argmin_butterfly(Q, arg, L, GS);
         best = Q;
         barg = arg;
-        return;
+    } else {
+        const int act_fixed = it.act;
+        const int a_lo = act_fixed >= 0 ? act_fixed : 0;
+        const int a_hi = act_fixed >= 0 ? act_fixed + 1 : a.A;
+        best = 0.0;
+        barg = a_lo;
+        for (int act = a_lo; act < a_hi; ++act) {
+            const int64_t row = s * a.A + act;
+            const int64_t e0 = !valid ? 0 : a.K > 0 ? row * a.K : __ldg(a.row_ptr + row);
+            const int64_t e1 = !valid ? 0 : a.K > 0 ? e0 + a.K : __ldg(a.row_ptr + row + 1);
+            double acc = 0.0;
+            for (int64_t e = e0 + g; e < e1; e += GS)
+                acc = fma(ldv<PT>(a.val, e), ld_keep(X + __ldg(a.col + e), pl), acc);
+            for (int o = GS >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const double Q = valid ? ldv<PT>(a.c, row) + a.gamma * acc : 0.0;
+            if (act == a_lo || Q < best) best = Q, barg = act;
+        }
     }
-    const int a_lo = act_fixed >= 0 ? act_fixed : 0;
-    const int a_hi = act_fixed >= 0 ? act_fixed + 1 : a.A;
-    best = 0.0;
-    barg = a_lo;
-    for (int act = a_lo; act < a_hi; ++act) {
-        const int64_t row = s * a.A + act;
-        const int64_t e0 = !valid ? 0 : a.K > 0 ? row * a.K : __ldg(a.row_ptr + row);
-        const int64_t e1 = !valid ? 0 : a.K > 0 ? e0 + a.K : __ldg(a.row_ptr + row + 1);
-        double acc = 0.0;
-        for (int64_t e = e0 + g; e < e1; e += GS) acc = fma(ldv<PT>(a.val, e), __ldcg(X + __ldg(a.col + e)), acc);
-        for (int o = GS >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        const double Q = valid ? ldv<PT>(a.c, row) + a.gamma * acc : 0.0;
-        if (act == a_lo || Q < best) best = Q, barg = act;
-    }
+}
+
+template <typename PT, int MODE>
+__device__ __forceinline__ void backup_state(const SparseArgs& a, const double* X, int64_t s, int act_fixed, int g,
+                                             int GS, bool valid, double& best, int& barg)
+{
+    SItem<PT, MODE> it;
+    load_item<PT, MODE>(a, s, act_fixed, g, valid, it, l2_evict_first());
+    finish_item<PT, MODE>(a, X, it, g, GS, best, barg, l2_evict_last());
 }
 
 struct SCtx {
     GridBarrier g;
     int64_t gb;  // global batch counter (X parity)
     int64_t batches;
-    // previous batch (for the X_cur -> X_next re-copy)
+    // previous batch (for the X_cur -> X_next re-copy); n < 2^31
     const uint32_t* prev_perm;
-    int64_t prev_lo, prev_cnt;
+    int prev_lo, prev_cnt;
     bool prev_valid;
-    unsigned long long t_mark;
-    long long t_comp, t_bar, n_bar;
+    // carry mode (at most one state per lane group and batch): the state this
+    // group backed up in the previous batch and its new value, stored into
+    // X_next during the next batch instead of the generic re-copy
+    int cs;
+    double cv;
 };
 
-__device__ __forceinline__ void s_prof(SCtx& x, long long* slot)
+// Phase profile of CTA 0 (rmb_last_phase_times): kept in shared memory so the
+// other 2^17 threads carry no registers for it.  [0] mark, [1] compute ns,
+// [2] barrier ns, [3] barriers.
+__shared__ unsigned long long s_prof_acc[4];
+enum { SP_MARK = 0, SP_COMP = 1, SP_BAR = 2, SP_NBAR = 3 };
+
+__device__ __forceinline__ void s_prof(int slot)
 {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const unsigned long long t = globaltimer_ns();
-        *slot += (long long)(t - x.t_mark);
-        x.t_mark = t;
+        s_prof_acc[slot] += t - s_prof_acc[SP_MARK];
+        s_prof_acc[SP_MARK] = t;
+        if (slot == SP_BAR) s_prof_acc[SP_NBAR] += 1;
     }
 }
 
@@ -291,17 +444,46 @@ __device__ __forceinline__ SweepResult read_slot(const SparseArgs& a, int slot)
     return s;
 }
 
+// Position of a lane group's item in the batch stream: batch start lo, the
+// warp's position w0 in the batch, and the sweep offset (0 = this sweep,
+// 1 = the next one).
+struct SPos {
+    int lo, w0, koff;
+};
+
+// The item pipeline of a lane group (software pipelining across items,
+// batches and sweeps).  Each state's V-independent data arrives through a
+// chain of dependent loads: perm[p] -> s, pol[s] -> action (B_{pi,b} only),
+// then the row's columns / probabilities / cost.  Item j+2 has its state id,
+// item j+1 its action and rows in flight, while item j gathers V -- so a
+// batch costs one V-gather round trip after its barrier, not four.
+template <typename PT, int MODE>
+struct SPipe {
+    SPos pA, pB, pC;  // items j+2, j+1, j
+    int sA, sB, aB;
+    bool vA, vB;
+    SItem<PT, MODE> C;
+};
+
 // One application of B_b (EVAL false) or B_{pi,b} (EVAL true), sweep k.
+// Lane group gid handles batch positions i = gid, gid + ngroups, ... of each
+// batch.  None of the pipeline's loads reads V, so they may cross the batch
+// barriers (Eq. 12 constrains only the V reads).  On entry `have` says whether
+// P already holds this sweep's first items (prefetched by the previous sweep
+// of the same kind); on exit whether it holds the next sweep's.
 template <typename PT, int MODE, bool EVAL>
-__device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const int32_t* pol)
+__device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const int32_t* pol,
+                                                 SPipe<PT, MODE>& P, bool& have, bool chain_next)
 {
-    const uint32_t* perm = a.identity ? nullptr : a.perm + (k % 3) * a.n;
     const int GS = EVAL ? a.GSE : a.GS;
     const int g = threadIdx.x & (GS - 1);
-    // warp-uniform trip counts: all 32 lanes stay in the loop for the shuffles
-    const int64_t ngroups = (int64_t)gridDim.x * ((int)blockDim.x / GS);
-    const int64_t gid = (int64_t)blockIdx.x * ((int)blockDim.x / GS) + threadIdx.x / GS;
-    const int64_t wfirst = gid - (threadIdx.x & 31) / GS;  // first group of this warp
+    // warp-uniform trip counts: all 32 lanes stay in the loop for the shuffles;
+    // state-space indices are 32-bit (n < 2^31)
+    const int n = (int)a.n, b = (int)min(a.b, a.n);
+    const int ngroups = (int)gridDim.x * ((int)blockDim.x / GS);
+    const int gid = (int)blockIdx.x * ((int)blockDim.x / GS) + (int)threadIdx.x / GS;
+    const int goff = (int)(threadIdx.x & 31) / GS;  // this group's offset from the warp's first group
+    const int wfirst = gid - goff;
     const int slot = (int)(k & 3);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // rearm the ring slot used two sweeps ahead
         const int z = (int)((k + 2) & 3);
@@ -309,66 +491,140 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
         atomicExch(a.red + 4 + z, 0ull);
         atomicExch(a.red + 8 + z, 0ull);
     }
-    const bool single = a.b >= a.n;  // one batch per sweep: every state rewritten each batch
+    const bool single = b >= n;  // one batch per sweep: every state rewritten each batch
     // chunked T (VI*): every chunk reads X_cur = the sweep-start
     // values and writes X_next; no re-copies, X flips once per sweep
     const bool chunked = !EVAL && a.chunked && !single;
+    // a single batch is order-free: walk it in state order (coalesced rows)
+    const uint32_t* perm0 = single || a.identity ? nullptr : a.perm + (k % 3) * a.n;
+    const uint32_t* perm1 = single || a.identity ? nullptr : a.perm + ((k + 1) % 3) * a.n;
+    // the next sweep's order is drawn during batch 0 of this one: its items
+    // may be looked up from batch 1 on, i.e. when the sweep has >= 4 batches
+    // (the pipeline runs at most 3 items ahead)
+    const int nbatch = (n + b - 1) / b;
+    const int maxoff = chain_next && nbatch >= 4 ? 1 : 0;
+    const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
+    auto cnt_of = [&](int lo) { return min(b, n - lo); };
+    auto advance = [&](SPos& p) {  // the warp's next position that holds an item
+        p.w0 += ngroups;
+        while (p.koff <= maxoff && p.w0 >= cnt_of(p.lo)) {
+            p.w0 = wfirst;
+            p.lo += b;
+            if (p.lo >= n) p.lo = 0, p.koff += 1;
+        }
+    };
+    auto state_at = [&](const SPos& p, int& s) -> bool {
+        const int i = p.w0 + goff;
+        const bool valid = p.koff <= maxoff && i < cnt_of(p.lo);
+        const uint32_t* pm = p.koff ? perm1 : perm0;
+        s = !valid ? 0 : pm ? ld_keep(reinterpret_cast<const int*>(pm) + p.lo + i, pf) : p.lo + i;
+        return valid;
+    };
+    auto action = [&](bool v, int s) -> int { return EVAL ? (v ? ld_keep(pol + s, pl) : 0) : -1; };
+    if (have) {  // items of this sweep, prefetched by the previous one
+        P.pA.koff -= 1;
+        P.pB.koff -= 1;
+        P.pC.koff -= 1;
+    } else {     // prologue: fill the pipeline
+        P.pC = SPos{0, wfirst - ngroups, 0};
+        advance(P.pC);
+        int s;
+        const bool v = state_at(P.pC, s);
+        load_item<PT, MODE>(a, s, action(v, s), g, v, P.C, pf);
+        P.pB = P.pC;
+        advance(P.pB);
+        P.vB = state_at(P.pB, P.sB);
+        P.aB = action(P.vB, P.sB);
+        P.pA = P.pB;
+        advance(P.pA);
+        P.vA = state_at(P.pA, P.sA);
+    }
     double rmax = 0.0;
     int bad = 0;
-    for (int64_t lo = 0; lo < a.n; lo += a.b) {
-        const int64_t cnt = min(a.b, a.n - lo);
+    // carry mode: every lane group holds at most one state of a batch
+    const bool carry = !single && !chunked && b <= ngroups;
+    for (int lo = 0; lo < n; lo += b) {
+        const int cnt = cnt_of(lo);
         const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
         double* Xn = (x.gb & 1) ? a.X0 : a.X1;
-        // states in processing order; a single batch is order-free, so walk it
-        // in state order (coalesced rows)
-        const uint32_t* bperm = single ? nullptr : perm;
-        for (int64_t w0 = wfirst; w0 < cnt; w0 += ngroups) {
-            const int64_t i = w0 + (gid - wfirst);
-            const bool valid = i < cnt;
-            const int64_t s = !valid ? 0 : bperm ? (int64_t)__ldg(bperm + lo + i) : lo + i;
+        if (carry && x.cs >= 0) {
+            // the previous batch's new value of this group's state, into X_next
+            // (its reads of that buffer ended at the barrier).  In the first
+            // batch of a sweep the state may belong to this batch too: then it
+            // gets this batch's new value and the old one is not stored.
+            bool skip = false;
+            if (lo == 0) {
+                if (a.identity) {
+                    skip = x.cs < cnt;
+                } else {
+                    Permutation pk;
+                    pk.init(a.n, a.seed, k);
+                    skip = (int64_t)pk.position((uint64_t)x.cs) < cnt;
+                }
+            }
+            if (!skip) st_keep(Xn + x.cs, x.cv, pl);
+            x.cs = -1;
+        }
+        while (P.pC.koff == 0 && P.pC.lo == lo) {
+            // stage A: state id of item j+3; stage B: action of item j+2;
+            // stage C: rows of item j+1 -- all issued before item j gathers V
+            SPos pN = P.pA;
+            advance(pN);
+            int sN;
+            const bool vN = state_at(pN, sN);
+            const int aA = action(P.vA, P.sA);
+            SItem<PT, MODE> next;
+            load_item<PT, MODE>(a, P.sB, P.aB, g, P.vB, next, pf);
+            // the state's own old value, in flight together with the gathers
+            const double old = P.C.valid && g == 0 ? ld_keep(Xc + P.C.s, pl) : 0.0;
             double v;
             int arg;
-            backup_state<PT, MODE>(a, Xc, s, EVAL && valid ? pol[s] : (EVAL ? 0 : -1), g, GS, valid, v, arg);
-            if (valid && g == 0) {
-                const double old = __ldcg(Xc + s);
+            finish_item<PT, MODE>(a, Xc, P.C, g, GS, v, arg, pl);
+            if (P.C.valid && g == 0) {
+                const int s = (int)P.C.s;
                 rmax = fmax(rmax, fabs(v - old));
                 bad |= !isfinite(v);
-                Xn[s] = v;
+                st_keep(Xn + s, v, pl);
                 if (!EVAL && a.pi) a.pi[s] = arg;
+                if (carry) x.cs = s, x.cv = v;
             }
+            P.C = next;
+            P.pC = P.pB;
+            P.sB = P.sA, P.aB = aA, P.vB = P.vA, P.pB = P.pA;
+            P.sA = sN, P.vA = vN, P.pA = pN;
         }
         // carry the previous batch's new values into X_next.  In the first
         // batch of a sweep the previous batch belongs to the previous sweep and
         // may share states with this batch: those get this batch's new value,
         // so their copy is skipped (membership through the inverse permutation).
-        if (x.prev_valid && !single) {
+        if (x.prev_valid && !single && !carry) {
             Permutation pk;
             if (lo == 0 && !a.identity) pk.init(a.n, a.seed, k);
-            const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-            for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.prev_cnt; i += stride) {
-                const int64_t s = x.prev_perm ? (int64_t)x.prev_perm[x.prev_lo + i] : x.prev_lo + i;
+            const int stride = (int)(gridDim.x * blockDim.x);
+            for (int i = (int)(blockIdx.x * blockDim.x + threadIdx.x); i < x.prev_cnt; i += stride) {
+                const int s = x.prev_perm ? ld_keep(reinterpret_cast<const int*>(x.prev_perm) + x.prev_lo + i, pf)
+                                          : x.prev_lo + i;
                 if (lo == 0) {
                     const int64_t pos = a.identity ? s : (int64_t)pk.position((uint64_t)s);
                     if (pos < cnt) continue;
                 }
-                Xn[s] = __ldcg(Xc + s);
+                st_keep(Xn + s, ld_keep(Xc + s, pl), pl);
             }
         }
         if (lo == 0 && !a.identity) {  // next sweep's order, off the critical path
             Permutation pm;
             pm.init(a.n, a.seed, k + 1);
             uint32_t* dst = a.perm + ((k + 1) % 3) * a.n;
-            const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-            for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < a.n; p += stride)
+            const int stride = (int)(gridDim.x * blockDim.x);
+            for (int p = (int)(blockIdx.x * blockDim.x + threadIdx.x); p < n; p += stride)
                 dst[p] = (uint32_t)pm((uint64_t)p);
         }
-        const bool last = lo + a.b >= a.n;
+        const bool last = lo + b >= n;
         if (last) cta_publish(a, slot, rmax, bad, 0);
-        s_prof(x, &x.t_comp);
+        s_prof(SP_COMP);
         grid_sync(x.g);
-        s_prof(x, &x.t_bar);
-        x.n_bar++;
-        x.prev_perm = single ? nullptr : perm;
+        s_prof(SP_BAR);
+        x.prev_perm = single || a.identity ? nullptr : a.perm + (k % 3) * a.n;
         x.prev_lo = lo;
         x.prev_cnt = cnt;
         x.prev_valid = !single && !chunked;
@@ -376,39 +632,48 @@ __device__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, int64_t k, const 
         ++x.batches;
     }
     if (chunked) ++x.gb;
+    have = maxoff == 1;
     return read_slot(a, slot);
 }
 
 // Policy improvement over all states against X_cur (no X write):
-// pw_next = greedy, changed vs pw_cur, ||TV - V||_inf.
+// pw_next = greedy, changed vs pw_cur, ||TV - V||_inf.  Software-pipelined
+// like run_sweep (the next state's rows load while this one gathers V).
 template <typename PT, int MODE>
-__device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx, const int32_t* pcur, int32_t* pnext,
+__device__ __forceinline__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx, const int32_t* pcur, int32_t* pnext,
                                    bool count_changed)
 {
     const int GS = a.GS;
     const int g = threadIdx.x & (GS - 1);
-    const int64_t ngroups = (int64_t)gridDim.x * ((int)blockDim.x / GS);
-    const int64_t gid = (int64_t)blockIdx.x * ((int)blockDim.x / GS) + threadIdx.x / GS;
-    const int64_t wfirst = gid - (threadIdx.x & 31) / GS;
-    // improvement steps use their own ring (slots 2,3 parity of imp_idx) via the
-    // same red[] words offset by 16
-    const SparseArgs* ap = &a;
+    const int n = (int)a.n;
+    const int ngroups = (int)gridDim.x * ((int)blockDim.x / GS);
+    const int gid = (int)blockIdx.x * ((int)blockDim.x / GS) + (int)threadIdx.x / GS;
+    const int goff = (int)(threadIdx.x & 31) / GS;
+    const int wfirst = gid - goff;
     const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
     double rmax = 0.0;
     int bad = 0;
     long long changed = 0;
-    for (int64_t w0 = wfirst; w0 < a.n; w0 += ngroups) {
-        const int64_t s = w0 + (gid - wfirst);
-        const bool valid = s < a.n;
+    const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
+    SItem<PT, MODE> cur;
+    load_item<PT, MODE>(a, gid < n ? gid : 0, -1, g, gid < n, cur, pf);
+    for (int w0 = wfirst; w0 < n; w0 += ngroups) {
+        SItem<PT, MODE> nxt;
+        {
+            const int s1 = w0 + ngroups + goff;
+            load_item<PT, MODE>(a, s1 < n ? s1 : 0, -1, g, s1 < n, nxt, pf);
+        }
         double v;
         int arg;
-        backup_state<PT, MODE>(a, Xc, valid ? s : 0, -1, g, GS, valid, v, arg);
-        if (valid && g == 0) {
-            rmax = fmax(rmax, fabs(v - __ldcg(Xc + s)));
+        finish_item<PT, MODE>(a, Xc, cur, g, GS, v, arg, pl);
+        if (cur.valid && g == 0) {
+            const int s = (int)cur.s;
+            rmax = fmax(rmax, fabs(v - ld_keep(Xc + s, pl)));
             bad |= !isfinite(v);
-            if (count_changed) changed += (arg != pcur[s]);
+            if (count_changed) changed += (arg != __ldcg(pcur + s));
             pnext[s] = arg;
         }
+        cur = nxt;
     }
     // improvement ring: red[16 + 4*q .. ] with q = imp_idx & 1 (rearmed for q^1)
     unsigned long long* base = a.red + 16 + 4 * (imp_idx & 1);
@@ -441,11 +706,9 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
             if (cc) atomicAdd(base + 2, (unsigned long long)cc);
         }
     }
-    (void)ap;
-    s_prof(x, &x.t_comp);
+    s_prof(SP_COMP);
     grid_sync(x.g);
-    s_prof(x, &x.t_bar);
-    x.n_bar++;
+    s_prof(SP_BAR);
     SweepResult r;
     r.r = __longlong_as_double((long long)ld_acquire_gpu(base));
     r.bad = ld_acquire_gpu(base + 1) != 0;
@@ -453,26 +716,39 @@ __device__ SweepResult run_improve(const SparseArgs& a, SCtx& x, int64_t imp_idx
     return r;
 }
 
-template <typename PT, int MODE, int MINB>
-__global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(const SparseArgs a)
+// Solve kinds: one kernel instantiation each, so that every kernel holds only
+// the state its own loop needs (register allocation is per kernel).
+enum SKind : int {
+    SK_MIN = 0,      // B_b sweeps: MB-VI, one B_b application
+    SK_EVAL = 1,     // B_{pi,b} sweeps: policy evaluation, one B_{pi,b} application
+    SK_MPI = 2,      // MB-MPI: evaluation sweeps + improvements
+    SK_IMPROVE = 3,  // one policy improvement
+};
+
+template <typename PT, int MODE, int KIND>
+__global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(const SparseArgs a)
 {
     SCtx x{};
     x.g = GridBarrier{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err};
-    if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t s = tid; s < a.n; s += stride) {
+    x.cs = -1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s_prof_acc[SP_MARK] = globaltimer_ns();
+        s_prof_acc[SP_COMP] = s_prof_acc[SP_BAR] = s_prof_acc[SP_NBAR] = 0;
+    }
+    const int stride = (int)(gridDim.x * blockDim.x);
+    const int tid = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    const int n = (int)a.n;
+    for (int s = tid; s < n; s += stride) {
         const double v = a.V[s];
         a.X0[s] = v;
         a.X1[s] = v;
-        if (a.mode == MODE_MPI || a.mode == MODE_APPLY_PI || a.mode == MODE_IMPROVE || a.mode == MODE_POLICY_VALUE)
-            a.pw0[s] = a.pi[s];
+        if (KIND != SK_MIN) a.pw0[s] = a.pi[s];
     }
-    if (!a.identity && a.mode != MODE_IMPROVE) {
+    if (!a.identity && KIND != SK_IMPROVE) {
         Permutation pm;
         pm.init(a.n, a.seed, a.k0);
         uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
-        for (int64_t p = tid; p < a.n; p += stride) dst[p] = (uint32_t)pm((uint64_t)p);
+        for (int p = tid; p < n; p += stride) dst[p] = (uint32_t)pm((uint64_t)p);
     }
     grid_sync(x.g);
 
@@ -482,13 +758,14 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(
     long long changed = 0;
     double last = 0.0;
     int pcur = 0;  // which pw buffer holds the current policy
-    if (a.mode == MODE_VI || a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI ||
-               a.mode == MODE_POLICY_VALUE) {
-        const bool eval = a.mode == MODE_APPLY_PI || a.mode == MODE_POLICY_VALUE;
-        const int64_t iters = (a.mode == MODE_VI || a.mode == MODE_POLICY_VALUE) ? a.max_iter : 1;
+    if constexpr (KIND == SK_MIN || KIND == SK_EVAL) {
+        const int64_t iters = a.max_iter;  // 1 for a single application
+        SPipe<PT, MODE> pre;
+        bool have = false;
         while (it < iters) {
-            SweepResult r = eval ? run_sweep<PT, MODE, true>(a, x, k, a.pw0)
-                                                    : run_sweep<PT, MODE, false>(a, x, k, nullptr);
+            const bool chain = it + 1 < iters;  // the next sweep (if any) is the same kind with k + 1
+            SweepResult r = run_sweep<PT, MODE, KIND == SK_EVAL>(a, x, k, KIND == SK_EVAL ? a.pw0 : nullptr, pre,
+                                                                  have, chain);
             if (lead && it < a.trace_len) a.trace[it] = r.r;
             ++it;
             ++k;
@@ -496,14 +773,14 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(
             if (r.bad) { status = RMB_ERR_NONFINITE; break; }
             if (a.eps >= 0.0 && r.r <= a.eps) { status = RMB_OK; break; }
         }
-        if ((a.mode == MODE_APPLY || a.mode == MODE_APPLY_PI) && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
-    } else if (a.mode == MODE_IMPROVE) {
+        if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;  // single application
+    } else if constexpr (KIND == SK_IMPROVE) {
         SweepResult r = run_improve<PT, MODE>(a, x, imp++, a.pw0, a.pw1, true);
         pcur = 1;
         last = r.r;
         changed = r.changed;
         status = r.bad ? RMB_ERR_NONFINITE : RMB_OK;
-    } else {  // MODE_MPI
+    } else {  // SK_MPI
         bool bad = false;
         if (!a.pi_given) {
             SweepResult r = run_improve<PT, MODE>(a, x, imp++, a.pw0, a.pw1, false);
@@ -513,8 +790,10 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(
         while (!bad && outer < a.max_iter) {
             const int64_t row = outer * (a.msweeps + 1);
             const int32_t* pol = pcur ? a.pw1 : a.pw0;
+            SPipe<PT, MODE> pre;
+            bool have = false;  // the policy just changed: nothing prefetched across the improvement
             for (int e = 0; e < a.msweeps && !bad; ++e) {
-                SweepResult r = run_sweep<PT, MODE, true>(a, x, k, pol);
+                SweepResult r = run_sweep<PT, MODE, true>(a, x, k, pol, pre, have, e + 1 < a.msweeps);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.r;
                 ++k;
                 ++it;
@@ -536,10 +815,9 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(
     // outputs: the interim vector after the last batch, and the policy
     const double* Xf = (x.gb & 1) ? a.X1 : a.X0;
     const int32_t* pf = pcur ? a.pw1 : a.pw0;
-    const bool write_pi_buf = a.mode == MODE_MPI || a.mode == MODE_IMPROVE;
-    for (int64_t s = tid; s < a.n; s += stride) {
-        if (a.mode != MODE_IMPROVE) a.V[s] = Xf[s];
-        if (write_pi_buf) a.pi[s] = pf[s];
+    for (int s = tid; s < n; s += stride) {
+        if (KIND != SK_IMPROVE) a.V[s] = Xf[s];
+        if (KIND == SK_MPI || KIND == SK_IMPROVE) a.pi[s] = pf[s];
     }
     if (lead) {
         a.out[OUT_SWEEPS] = it;
@@ -548,30 +826,34 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, MINB) sparse_solver_kernel(
         a.out[OUT_RESID_BITS] = __double_as_longlong(last);
         a.out[OUT_BATCHES] = x.batches;
         a.out[OUT_CHANGED] = changed;
-        a.prof[0] = x.t_comp;
-        a.prof[1] = x.t_bar;
+        a.prof[0] = (long long)s_prof_acc[SP_COMP];
+        a.prof[1] = (long long)s_prof_acc[SP_BAR];
         a.prof[2] = 0;
-        a.prof[3] = x.n_bar;
+        a.prof[3] = (long long)s_prof_acc[SP_NBAR];
     }
 }
 
-template <typename PT, int MODE, int MINB>
-static cudaError_t launch_sparse_minb(const SparseArgs& a, int grid, cudaStream_t st)
+template <typename PT, int MODE, int KIND>
+static cudaError_t launch_sparse_kind(const SparseArgs& a, int grid, cudaStream_t st)
 {
-    auto kern = sparse_solver_kernel<PT, MODE, MINB>;
+    auto kern = sparse_solver_kernel<PT, MODE, KIND>;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SThreads<MODE>::v, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-    if (grid > 1) grid *= std::min(per_sm, MINB);
     void* args[] = {const_cast<SparseArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(SThreads<MODE>::v), args, 0, st);
 }
 
 template <typename PT, int MODE>
-static cudaError_t launch_sparse(const SparseArgs& a, int grid, bool wide, cudaStream_t st)
+static cudaError_t launch_sparse(const SparseArgs& a, int grid, cudaStream_t st)
 {
-    return wide ? launch_sparse_minb<PT, MODE, 2>(a, grid, st) : launch_sparse_minb<PT, MODE, 1>(a, grid, st);
+    switch (a.mode) {
+    case MODE_VI: case MODE_APPLY: return launch_sparse_kind<PT, MODE, SK_MIN>(a, grid, st);
+    case MODE_APPLY_PI: case MODE_POLICY_VALUE: return launch_sparse_kind<PT, MODE, SK_EVAL>(a, grid, st);
+    case MODE_MPI: return launch_sparse_kind<PT, MODE, SK_MPI>(a, grid, st);
+    default: return launch_sparse_kind<PT, MODE, SK_IMPROVE>(a, grid, st);
+    }
 }
 
 // Layout of the sparse backup (mode, lanes per state) chosen from the CSR
@@ -594,7 +876,7 @@ static void sparse_layout(const Problem& pr, int& mode, int& GS, int& GSE)
         mode = SM_VEC;
         GS = (int)(AK / 8);
         GSE = ellK / 8;
-    } else if (ellK > 0 && ellK <= 8 && pr.A <= 32) {
+    } else if (ellK > 0 && ellK <= kRowK && pr.A <= 32) {
         mode = SM_ROW;
         while (GS < pr.A) GS <<= 1;
         GSE = 1;  // B_{pi,b}: one row per state -> a lane per state
@@ -661,24 +943,43 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     cudaEventCreate(&e1);
     cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    // row mode: repack the rows into records (inside the timed region: part of the solve)
+    a.rec = nullptr;
+    int launches = 1;
+    if (ce == cudaSuccess && mode == SM_ROW) {
+        const int64_t rows = n * pr.A;
+        const size_t W = pr.pdt == RMB_F32 ? RowRec<float>::W : RowRec<double>::W;
+        if (pr.rowrec.ensure((size_t)rows * W * 4) != cudaSuccess) {
+            set_error("sparse solver: row-record workspace allocation failed");
+            return RMB_ERR_OOM;
+        }
+        uint32_t* rec = static_cast<uint32_t*>(pr.rowrec.p);
+        const int blocks = (int)std::min<int64_t>((rows + 255) / 256, (int64_t)pr.num_sms * 16);
+        if (pr.pdt == RMB_F32)
+            pack_rows_kernel<float><<<blocks, 256, 0, st>>>(pr.col, (const float*)pr.val, (const float*)pr.c, rows,
+                                                            pr.ell_K, rec);
+        else
+            pack_rows_kernel<double><<<blocks, 256, 0, st>>>(pr.col, (const double*)pr.val, (const double*)pr.c, rows,
+                                                             pr.ell_K, rec);
+        ce = cudaGetLastError();
+        a.rec = rec;
+        ++launches;
+    }
     // tiny batches (<= 2048 nonzeros, e.g. GS-VI on the paper's environments)
     // are latency-bound: one CTA with CTA barriers beats a 148-CTA grid
     // barrier per batch (measured: FrozenLake b=1 96 vs 125 ms, maze80 b=1
     // 5.96 vs 7.35 s; from ~10^4 nonzeros per batch the full grid wins)
     const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(rq.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
-    int grid = nnz_batch <= kSparseSmallBatchNnz && !pr.sparse_full_grid ? 1 : pr.num_sms;
-    // two CTAs per SM for B_b sweeps over large batches (see kSparseWideNnz)
-    bool wide = grid > 1 && (rq.mode == MODE_VI || rq.mode == MODE_APPLY) && nnz_batch >= kSparseWideNnz;
-    if (pr.sparse_wide >= 0) wide = grid > 1 && pr.sparse_wide == 1;
+    const int grid = nnz_batch <= kSparseSmallBatchNnz && !pr.sparse_full_grid ? 1 : pr.num_sms;
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
-            ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, wide, st)
-                 : mode == SM_ROW ? launch_sparse<float, SM_ROW>(a, grid, wide, st)
-                                  : launch_sparse<float, SM_STRIDED>(a, grid, wide, st);
+            ce = mode == SM_VEC   ? launch_sparse<float, SM_VEC>(a, grid, st)
+                 : mode == SM_ROW ? launch_sparse<float, SM_ROW>(a, grid, st)
+                                  : launch_sparse<float, SM_STRIDED>(a, grid, st);
         else
-            ce = mode == SM_VEC   ? launch_sparse<double, SM_VEC>(a, grid, wide, st)
-                 : mode == SM_ROW ? launch_sparse<double, SM_ROW>(a, grid, wide, st)
-                                  : launch_sparse<double, SM_STRIDED>(a, grid, wide, st);
+            ce = mode == SM_VEC   ? launch_sparse<double, SM_VEC>(a, grid, st)
+                 : mode == SM_ROW ? launch_sparse<double, SM_ROW>(a, grid, st)
+                                  : launch_sparse<double, SM_STRIDED>(a, grid, st);
     }
     if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
     long long out[OUT_N + 4] = {0};
@@ -702,9 +1003,9 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     res->batches = out[OUT_BATCHES];
     res->changed = out[OUT_CHANGED];
     res->ms = ms;
-    res->launches = 1;
+    res->launches = launches;
     for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
-    pr.last_launches = 1;
+    pr.last_launches = launches;
     return RMB_OK;
 }
 

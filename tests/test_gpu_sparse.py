@@ -210,21 +210,22 @@ def _instance_with_flags(name, flags):
 
 @pytest.mark.parametrize("name", ["ell32", "grid", "ragged"])
 @pytest.mark.parametrize("b", [1, 37, None])
-def test_two_ctas_per_sm_variant_is_bitwise_default(name, b):
-    """The MINB = 2 build of the persistent solver (2 CTAs/SM, chosen for large
-    batches) forced at small sizes: V, pi and trace bitwise = the MINB = 1 build
-    (grid-free per-state arithmetic), and the oracle within the solve bar."""
-    m, p1 = _instance_with_flags(name, rmb.SPARSE_FULL_GRID | rmb.SPARSE_WIDE_OFF)
-    _, p2 = _instance_with_flags(name, rmb.SPARSE_FULL_GRID | rmb.SPARSE_WIDE_ON)
+def test_full_grid_is_bitwise_single_cta(name, b):
+    """Tiny batches run on one CTA by default; forced onto the full 148-CTA grid
+    (RMB_SPARSE_FULL_GRID) every result is bitwise the same (per-state
+    arithmetic is grid-free), for VI and MPI, and within the bar of the oracle."""
+    m, p1 = _instance_with_flags(name, 0)
+    _, p2 = _instance_with_flags(name, rmb.SPARSE_FULL_GRID)
     b = m.n if b is None else b
-    one = p1.vi(b, seed=5, eps=1e-8, max_sweeps=40)
-    two = p2.vi(b, seed=5, eps=1e-8, max_sweeps=40)
-    assert one.stats.sweeps == two.stats.sweeps
-    assert np.array_equal(one.trace, two.trace)
-    assert np.array_equal(one.V.cpu().numpy(), two.V.cpu().numpy())
-    assert np.array_equal(one.pi.cpu().numpy(), two.pi.cpu().numpy())
+    for solve in (lambda p: p.vi(b, seed=5, eps=1e-8, max_sweeps=40),
+                  lambda p: p.mpi(b, 3, seed=5, eps=1e-8, max_outer=6)):
+        one, two = solve(p1), solve(p2)
+        assert one.stats.sweeps == two.stats.sweeps
+        assert np.array_equal(one.trace, two.trace)
+        assert np.array_equal(one.V.cpu().numpy(), two.V.cpu().numpy())
+        assert np.array_equal(one.pi.cpu().numpy(), two.pi.cpu().numpy())
     ref = oracle.vi(m, b, seed=5, eps=1e-8, max_sweeps=40)
-    assert_close(two.V.cpu().numpy(), ref.V, 1e-9)
+    assert_close(p2.vi(b, seed=5, eps=1e-8, max_sweeps=40).V.cpu().numpy(), ref.V, 1e-9)
 
 
 # ------------------------------------------------------------ VI* (P:L577)

@@ -20,11 +20,11 @@ n, A = 10_000, 16
 P, c = rmb.generate_dense(n, A, 1)
 out = {}
 for b in (1000, 64):
+    she = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm, flags=rmb.SHARD_NO_GRAPH)
+    she.vi(b, seed=0, eps=1e-300, max_sweeps=2)
+    se = she.vi(b, seed=1, eps=1e-300, max_sweeps=20)
+    she.close()
     sh = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm)
-    os.environ["RMB_SHARD_NO_GRAPH"] = "1"
-    sh.vi(b, seed=0, eps=1e-300, max_sweeps=2)
-    se = sh.vi(b, seed=1, eps=1e-300, max_sweeps=20)
-    os.environ["RMB_SHARD_NO_GRAPH"] = "0"
     sh.vi(b, seed=0, eps=1e-300, max_sweeps=2)
     s = sh.vi(b, seed=1, eps=1e-300, max_sweeps=20)
     one = rmb.Problem.dense(P, c, 0.99)
