@@ -102,11 +102,20 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- CPU oracle
-def oracle_sample(seconds_target=12.0, n_rows=200):
-    """The oracle as it stands (single-threaded C, fp64, sequential sums) on a
-    bounded sample of the config-2 workload: full Bellman backups
-    (16 actions x 10^4 successors) of `n_rows` states of the instance, repeated
-    until ~seconds_target of CPU time.  Returns (backups/s, cores, sample)."""
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(seconds_target=8.0, n_rows=200):
+    """The oracle as it stands, ONE thread, on a bounded sample of the config-2
+    workload: full Bellman backups (16 actions x 10^4 successors) of `n_rows`
+    states, repeated until ~seconds_target.  Returns (backups/s, sample)."""
     import numpy as np
 
     import gen
@@ -121,46 +130,177 @@ def oracle_sample(seconds_target=12.0, n_rows=200):
         el = time.perf_counter() - t0
         if el >= seconds_target:
             break
-    rate = done * N_ACTIONS / el
-    return rate, 1, (f"oracle.backup_dense_row (single thread) over states 0..{n_rows - 1} of the config-2 "
-                     f"instance, {done} state backups x 16 actions x 10^4 successors in {el:.1f} s")
+    return done * N_ACTIONS / el, (f"oracle.backup_dense_row, 1 thread, states 0..{n_rows - 1} of the config-2 "
+                                   f"instance: {done} state backups x 16 actions x 10^4 successors in {el:.1f} s")
+
+
+class OracleSweeps:
+    """The oracle's B_b sweep over the WHOLE config-2 instance (host-generated,
+    6.4 GB fp32) with W worker threads over each batch's states -- one sweep is
+    one unit of the GPU arm's solve."""
+
+    def __init__(self, threads):
+        import numpy as np
+
+        import gen
+        import oracle
+        self.oracle, self.np = oracle, np
+        P, c = gen.dense(N_STATES, N_ACTIONS, INST_SEED)
+        self.m = oracle.MDP(N_STATES, N_ACTIONS, GAMMA, c, P=P)
+        self.V = np.zeros(N_STATES)
+        self.threads = threads
+        self.k = 1
+
+    def sweep(self, b):
+        self.oracle.set_threads(self.threads)
+        try:
+            self.V, _, r = self.oracle.sweep(self.m, self.V, b, self.oracle.partition(N_STATES, 0, self.k))
+        finally:
+            self.oracle.set_threads(1)
+        self.k += 1
+        return r
+
+
+def arm_config(b, parallelism, extra=None):
+    cfg = {"workload": WORKLOAD, "b": b,
+           "l2": "inputs larger than L2 (P 6.4 GB) + 256 MB flush between GPU solves",
+           "parallelism": parallelism}
+    cfg.update(extra or {})
+    return cfg
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle as it stands (oracle/, plain C + OpenMP
+    workers over a batch's states) on the same workload and metric.  One step =
+    one B_b sweep (b = args.b) of the full config-2 instance on all host cores;
+    value = state-action backups / s."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np
-
-    import gen
-    import oracle
-    n_rows = 64
-    Ph, ch = gen.dense(N_STATES, N_ACTIONS, INST_SEED, rows=(0, n_rows))
-    V = np.random.default_rng(0).random(N_STATES) * 50
-
-    def step():
-        for s in range(n_rows):
-            oracle.backup_dense_row(Ph[s], ch[s], GAMMA, V)
-
+    W = os.cpu_count() or 1
+    ora = OracleSweeps(W)
     for _ in range(args.warmup):
-        step()
+        ora.sweep(args.b)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        ora.sweep(args.b)
     el = time.perf_counter() - t0
-    value = args.steps * n_rows * N_ACTIONS / el
-    sample = (f"each step = oracle Bellman backups of {n_rows} states (x16 actions x 10^4 successors) of the "
-              f"config-2 instance, single thread")
+    value = args.steps * N_STATES * N_ACTIONS / el
+    sample = (f"each step = one oracle B_b sweep (b={args.b}) over all 10^4 states x 16 actions x 10^4 successors "
+              f"of the config-2 instance, {W} OpenMP threads over each batch's states ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "b": args.b, "parallelism": "cpu1"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": arm_config(args.b, f"cpu{W}"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": W, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baselines(b):
+    """cpu_baseline of the GPU arm: the oracle at W = 1 (a row sample) and at
+    W = nproc (whole B_b sweeps of the config-2 instance)."""
+    r1, s1 = oracle_sample()
+    W = os.cpu_count() or 1
+    ora = OracleSweeps(W)
+    ora.sweep(b)
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 8.0 or k < 2:
+        ora.sweep(b)
+        k += 1
+    el = time.perf_counter() - t0
+    rW = k * N_STATES * N_ACTIONS / el
+    del ora
+    return {"value": rW, "unit": UNIT, "cores": W, "kind": "oracle", "cpu": cpu_model(),
+            "sample": f"{k} oracle B_b sweeps (b={b}) of the whole config-2 instance with {W} OpenMP threads "
+                      f"over each batch's states, {el:.1f} s",
+            "w1": {"value": r1, "cores": 1, "sample": s1}}
+
+
+def vi_star_rows(rmb, torch, prob_c2, V, pi):
+    """SURVEY 8(f) row 3 / PAPER.md L577: VI* (the Bellman operator computed in
+    chunks of c states against the old values, RMB_CHUNKED_T) against MB-VI with
+    batches of the same size -- the same barriers and bytes per sweep, so the
+    time-to-eps ratio is the paper's equal-parallelism comparison."""
+    out = []
+    for b in (1000, 5000):
+        row = {"instance": "config 2 (dense 10^4 x 16, gamma 0.99, eps 1e-6)", "chunk_or_batch": b}
+        for name, ch in (("mb_vi", False), ("vi_star", True)):
+            sol = prob_c2.vi(b, seed=3, eps=EPS, max_sweeps=200_000, V=V, pi=pi, v0_zero=True, chunked=ch)
+            row[name] = {"sweeps": sol.stats.sweeps, "barriers_per_sweep": -(-N_STATES // b),
+                         "time_to_eps_ms": sol.stats.seconds * 1e3}
+        row["speedup_mb_vi_over_vi_star"] = row["vi_star"]["time_to_eps_ms"] / row["mb_vi"]["time_to_eps_ms"]
+        out.append(row)
+    from gen import envs
+    n, A, rp, col, val, c, _ = envs.maze(100)
+    dev = lambda x: torch.from_numpy(x).cuda()  # noqa: E731
+    prob = rmb.Problem.csr(n, A, dev(rp), dev(col), dev(val), dev(c), 0.95)
+    for b in (-(-n // 2), 512):  # the paper's 2 chunks of 4853 (N=100 maze) and its MB-VI m=512
+        row = {"instance": f"2D-Maze N=100 (n={n}, gamma 0.95, eps 1e-6)", "chunk_or_batch": b}
+        for name, ch in (("mb_vi", False), ("vi_star", True)):
+            sol = prob.vi(b, seed=3, eps=1e-6, max_sweeps=100_000, chunked=ch)
+            row[name] = {"sweeps": sol.stats.sweeps, "barriers_per_sweep": -(-n // b),
+                         "time_to_eps_ms": sol.stats.seconds * 1e3}
+        row["speedup_mb_vi_over_vi_star"] = row["vi_star"]["time_to_eps_ms"] / row["mb_vi"]["time_to_eps_ms"]
+        row["paper"] = "x2.57 (m=4853) / x3.04 (m=512) on a GTX 1650 Ti, P:L577"
+        out.append(row)
+    prob.close()
+    return out
+
+
+def config5_line(rmb, torch, dist, comm, world, rank, dev):
+    """BASELINE config 5 (dense |S|=50 000, |A|=32, fp32, MB-MPI m=10, b=n/8,
+    gamma 0.99): P is 320 GB, sharded 8 ways = 40 GB per GPU.  On N GPUs the
+    instance has n_N = 50 000 sqrt(N/8) states (the same 40 GB per GPU; n_8 is
+    config 5 itself), each rank generating its rows on the device.  N = 1 adds
+    the certificate ||TV - V||_inf with every row regenerated on the host."""
+    A, gamma = 32, 0.99
+    n = int(round(50_000 * (world / 8) ** 0.5 / 8)) * 8
+    b = n // 8
+    rows = rmb.shard_range(n, world, rank) if world > 1 else (0, n)
+    P, c = rmb.generate_dense(n, A, 5, rows=rows)
+    if world > 1:
+        prob = rmb.Problem.dense(P, c, gamma, n=n, row_range=rows, nccl_comm=comm)
+    else:
+        prob = rmb.Problem.dense(P, c, gamma)
+    prob.mpi(b, 10, seed=0, eps=1e-6, max_outer=1)
+    sol = prob.mpi(b, 10, seed=1, eps=1e-6, max_outer=1000)
+    t = sol.stats.seconds
+    if dist:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    st = sol.stats
+    share = (rows[1] - rows[0]) * A * n * 4
+    # bytes per rank: eval sweeps read one row per owned state, improvements all owned rows
+    rank_bytes = st.sweeps * share / A + (st.outer_iters + 1) * share
+    line = {"workload": f"config 5 on {world} GPU(s): dense |S|={n} |A|={A} fp32 ({share / 1e9:.1f} GB of P per GPU), "
+                        f"gamma={gamma}, MB-MPI m=10 b=n/8={b} to eps=1e-6",
+            "status": int(sol.status), "outer_iterations": st.outer_iters, "eval_sweeps": st.sweeps,
+            "time_to_eps_ms": t * 1e3, "backups_per_s": (st.sweeps * n + (st.outer_iters + 1) * n * A) / t,
+            "per_gpu_GB_per_s": rank_bytes / t / 1e9}
+    if world == 1:
+        import oracle
+        Vh = sol.V.cpu().numpy()
+        oracle.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        try:
+            rT, arg = oracle.bellman_residual_dense_gen(5, n, A, gamma, Vh)
+        finally:
+            oracle.set_threads(1)
+        line["certificate"] = {"bellman_residual_host": rT, "bound_V_minus_Vstar": rT / (1 - gamma),
+                               "gpu_final_residual": st.final_residual, "host_seconds": time.perf_counter() - t0,
+                               "policy_agrees_frac": float((arg == sol.pi.cpu().numpy()).mean()),
+                               "how": "oracle.bellman_residual_dense_gen: every row regenerated on the host "
+                                      "from gen/rmb_gen.h (fp32 storage), fp64 sequential sums, all cores"}
+    del prob, P, c
+    torch.cuda.empty_cache()
+    return line
 
 
 def other_configs(rmb, torch, dev):
@@ -174,11 +314,14 @@ def other_configs(rmb, torch, dev):
     sol = prob.vi(n // 8, seed=0, eps=1e-6, max_sweeps=100_000)
     st = sol.stats
     bps = n * A * K * 8 + n * A * 4 + 16 * n
+    peak, _ = peaks()
     out.append({"workload": "config 3: sparse random |S|=1e6 |A|=8 K=32 (ELL fp32), gamma=0.99, MB-VI b=n/8 to eps=1e-6",
                 "status": int(sol.status), "sweeps": st.sweeps, "time_to_eps_ms": st.seconds * 1e3,
                 "backups_per_s": st.sweeps * n * A / st.seconds,
                 "hbm_algorithmic_GB_per_s": st.sweeps * bps / st.seconds / 1e9,
-                "note": "L2-gather bound: one random 8-byte V gather (a 32-byte L2 sector) per nonzero"})
+                "frac": st.sweeps * bps / st.seconds / 1e9 / peak,
+                "note": "bound by L1TEX wavefronts of the random 8-byte V gathers (one sector each, 2.56e8 per "
+                        "sweep), not HBM: profiles/r02"})
     del prob, rp, col, val, c
     torch.cuda.empty_cache()
     N = 2048
@@ -189,29 +332,15 @@ def other_configs(rmb, torch, dev):
     sol = prob.mpi(65536, 10, seed=0, eps=1e-6, max_outer=100_000)
     st = sol.stats
     backups = st.sweeps * n + (st.outer_iters + 1) * n * 4
+    # algorithmic bytes: eval n(40 + 4 + 4) + 2 V; improvement the whole ELL + c + V
+    algo = st.sweeps * (n * 48 + 16 * n) + (st.outer_iters + 1) * (n * 4 * 40 + n * 4 * 4 + 8 * n)
     out.append({"workload": "config 4: 2048x2048 slip gridworld, gamma=0.95, MB-MPI m=10 b=65536 to eps=1e-6",
                 "status": int(sol.status), "outer_iterations": st.outer_iters, "eval_sweeps": st.sweeps,
-                "time_to_eps_ms": st.seconds * 1e3, "backups_per_s": backups / st.seconds})
+                "time_to_eps_ms": st.seconds * 1e3, "backups_per_s": backups / st.seconds,
+                "hbm_algorithmic_GB_per_s": algo / st.seconds / 1e9, "frac": algo / st.seconds / 1e9 / peak,
+                "note": "64 batches per evaluation sweep: per-batch latency (grid barrier ~2.5 us + one V-gather "
+                        "round trip) and L2 capacity (two 33.5 MB copies of V) bound it: profiles/r02"})
     del prob, rp, col, val, c
-    torch.cuda.empty_cache()
-    # config 5's per-GPU working set on one GPU: dense n = 50 000 (V > shared
-    # memory -> the TMA path's global-V mode), |A| = 4 fp32 = 40 GB = one rank's
-    # 6250 x 32 x 50 000 share; MB-MPI m = 10, b = n/8 (config 5's batch)
-    n, A = 50_000, 4
-    P, c = rmb.generate_dense(n, A, 5)
-    prob = rmb.Problem.dense(P, c, 0.99)
-    prob.vi(n // 8, seed=0, eps=1e-6, max_sweeps=2)
-    sol = prob.vi(n // 8, seed=1, eps=1e-6, max_sweeps=10)
-    st = sol.stats
-    bps = n * A * n * 4 + n * A * 4 + 16 * n + 4 * n
-    mp = prob.mpi(n // 8, 10, seed=1, eps=1e-6, max_outer=3)
-    out.append({"workload": "config 5 per-GPU share on 1 GPU: dense |S|=50000 |A|=4 fp32 (40 GB), gamma=0.99, "
-                            "global-V TMA mode; MB-VI b=n/8 10 sweeps, MB-MPI m=10 b=n/8 3 outer iterations",
-                "vi_ms_per_sweep": st.seconds / st.sweeps * 1e3, "vi_GB_per_s": st.sweeps * bps / st.seconds / 1e9,
-                "vi_backups_per_s": st.sweeps * n * A / st.seconds,
-                "mpi_ms_per_outer": mp.stats.seconds / max(1, mp.stats.outer_iters) * 1e3,
-                "mpi_eval_sweeps": mp.stats.sweeps})
-    del prob, P, c
     torch.cuda.empty_cache()
     return out
 
@@ -381,10 +510,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "b": args.b, "sweeps_per_solve": sweeps / args.steps,
-                   "l2": "inputs larger than L2 (P 6.4 GB) + 256 MB flush between solves",
-                   "parallelism": f"shard{world} (rows by state, V replicated, NCCL all-gather per batch)"
-                   if world > 1 else "dp1"},
+        "config": arm_config(args.b, f"shard{world} (rows by state, V replicated, NCCL all-gather per batch)"
+                             if world > 1 else "dp1", {"sweeps_per_solve": sweeps / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_note": "dram read+write bytes per launch = per-sweep DRAM bytes of the committed "
@@ -412,6 +539,8 @@ def main():
                           "backups_per_s": st.sweeps * N_STATES * N_ACTIONS / st.seconds,
                           "GB_per_s": st.sweeps * bb / st.seconds / 1e9})
         result["time_to_eps_vs_b"] = table
+    if rank == 0 and world == 1 and not args.no_other:
+        result["vi_star_vs_mb_vi"] = vi_star_rows(rmb, torch, prob, V, pi)
 
     if rank == 0 and world == 1 and not args.no_e2e:
         # e2e through the C ABI with HOST buffers: H2D of P, c inside the timed region
@@ -451,13 +580,16 @@ def main():
         line = sharded_config3(rmb, torch, dist, comm, world, rank, dev)
         if rank == 0:
             result["other_configs"] = [line]
+    if not args.no_other:
+        line = config5_line(rmb, torch, dist, comm, world, rank, dev)
+        if rank == 0:
+            result.setdefault("other_configs", []).append(line)
 
     if rank == 0 and world == 1 and not args.no_other:
         result["paper_envs"] = paper_envs(rmb, torch)
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, cores, sample = oracle_sample()
-        result["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        result["cpu_baseline"] = cpu_baselines(args.b)
 
     if rank == 0:
         print(json.dumps(result), flush=True)

@@ -40,7 +40,8 @@ def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
     if os.environ.get("RMB_ORACLE_SO"):
         return _SO
-    if force or not os.path.exists(_SO) or os.path.getmtime(src) > os.path.getmtime(_SO):
+    hdr = os.path.join(os.path.dirname(_HERE), "gen", "rmb_gen.h")
+    if force or not os.path.exists(_SO) or max(os.path.getmtime(src), os.path.getmtime(hdr)) > os.path.getmtime(_SO):
         # -ffp-contract=off: no FMA contraction — every product and sum is
         # rounded exactly as written in oracle.c
         # -fopenmp: optional worker threads across the states of one batch
@@ -80,6 +81,8 @@ def _load():
         lib.orc_backup_dense_row.restype = dbl
         lib.orc_backup_csr_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, vp, vp, i32, vp]
         lib.orc_backup_csr_row.restype = dbl
+        lib.orc_bellman_residual_dense_gen.argtypes = [u64, i64, i32, ctypes.c_int, dbl, vp, i64, i64, vp]
+        lib.orc_bellman_residual_dense_gen.restype = dbl
         for f in (lib.orc_partition, lib.orc_partition_inverse, lib.orc_sweep, lib.orc_sweep_chunked, lib.orc_improve,
                   lib.orc_vi, lib.orc_mpi):
             f.restype = ctypes.c_int
@@ -279,6 +282,18 @@ def backup_csr_row(n: int, row_ptr: np.ndarray, col: np.ndarray, val: np.ndarray
     q = _load().orc_backup_csr_row(n, len(row_ptr) - 1, gamma, int(val.dtype == np.float32), _p(row_ptr), _p(col),
                                    _p(val), _p(c_row), _p(Vint), pi_a, ctypes.byref(arg))
     return q, arg.value
+
+
+def bellman_residual_dense_gen(seed: int, n: int, A: int, gamma: float, V: np.ndarray, rows=None,
+                               f32: bool = True):
+    """||T V - V||_inf over rows (s0, s1) of the dense random instance (seed, n, A),
+    its rows regenerated on the host (certificate ||V - V*|| <= r / (1 - gamma),
+    Prop. 3).  Returns (r, argmin over the rows)."""
+    s0, s1 = rows if rows is not None else (0, n)
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    arg = np.zeros(s1 - s0, dtype=np.int32)
+    r = _load().orc_bellman_residual_dense_gen(seed, n, A, int(f32), gamma, _p(V), s0, s1, _p(arg))
+    return r, arg
 
 
 # ------------------------------------------------- plain definitions (numpy)

@@ -30,6 +30,9 @@
  */
 #include <math.h>
 #include <omp.h>
+/* the shared instance definition (no method arithmetic): rows of the dense
+   random instance are regenerated on the fly by orc_bellman_residual_dense_gen */
+#include "../gen/rmb_gen.h"
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -461,4 +464,44 @@ double orc_backup_csr_row(int64_t n, int32_t A, double gamma, int p_f32, const i
     double q = q_min(&m, 0, Vint, &a);
     if (arg) *arg = a;
     return q;
+}
+
+
+/* ------------------------------------------------------------------ */
+/* Certificate for instances too large to hold on the host (config 5:  */
+/* 320 GB of P): r_T = ||T V - V||_inf (Eq. 5 / Prop. 3: then           */
+/* ||V - V*||_inf <= r_T / (1 - gamma)) over the states [s0, s1) of the */
+/* dense random instance (seed, n, A), every row REGENERATED from the   */
+/* shared instance definition gen/rmb_gen.h, stored as float (f32) or   */
+/* double exactly as the instance is, and summed as q_value does        */
+/* (sequentially in j, fp64).  Threads split the states; the max is     */
+/* order-free.  arg_out (may be NULL): argmin_a Q(s,a), [s1 - s0].      */
+/* ------------------------------------------------------------------ */
+double orc_bellman_residual_dense_gen(uint64_t seed, int64_t n, int32_t A, int f32, double gamma, const double* V,
+                                      int64_t s0, int64_t s1, int32_t* arg_out)
+{
+    double r = 0.0;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(orc_nthreads) reduction(max : r)
+    for (int64_t s = s0; s < s1; ++s) {
+        double best = 0.0;
+        int32_t ba = 0;
+        for (int32_t a = 0; a < A; ++a) {
+            uint64_t W = 0;
+            for (int64_t j = 0; j < n; ++j) W += rmbgen_dense_w(seed, s, a, j);
+            double acc = 0.0;
+            for (int64_t j = 0; j < n; ++j) {
+                double p = rmbgen_dense_p(seed, s, a, j, W);
+                if (f32) p = (double)(float)p;
+                acc += p * V[j];
+            }
+            double c = rmbgen_cost_u01(seed, s, a);
+            if (f32) c = (double)(float)c;
+            const double q = c + gamma * acc;
+            if (a == 0 || q < best) { best = q; ba = a; }
+        }
+        if (arg_out) arg_out[s - s0] = ba;
+        const double d = fabs(best - V[s]);
+        if (d > r || d != d) r = d;
+    }
+    return r;
 }

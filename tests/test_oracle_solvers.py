@@ -348,3 +348,21 @@ def test_vi_driver_is_composition():
     res = oracle.vi(m, b, seed=9, eps=eps)
     assert res.sweeps == len(tr) and np.array_equal(res.V, V) and np.array_equal(res.pi, pi)
     assert np.array_equal(res.trace, np.array(tr))
+
+
+def test_bellman_residual_by_row_regeneration():
+    """The config-5 certificate routine (rows regenerated on the host) equals
+    ||T V - V|| computed from the stored instance with the numpy textbook
+    Bellman operator, for f32 and f64 storage."""
+    n, A, gamma = 90, 5, 0.97
+    V = np.random.default_rng(0).random(n) * 30
+    for f32 in (True, False):
+        P, c = gen.dense(n, A, 3, dtype=np.float32 if f32 else np.float64)
+        Q = c.astype(np.float64) + gamma * np.einsum("saj,j->sa", P.astype(np.float64), V)
+        r, arg = oracle.bellman_residual_dense_gen(3, n, A, gamma, V, f32=f32)
+        assert abs(r - np.abs(Q.min(1) - V).max()) <= 1e-12 * 30
+        m = oracle.MDP(n, A, gamma, c, P=P)
+        mask = gap_mask(m, V, 1e-9)
+        assert np.array_equal(arg[mask], Q.argmin(1)[mask])
+        r2, _ = oracle.bellman_residual_dense_gen(3, n, A, gamma, V, rows=(10, 40), f32=f32)
+        assert abs(r2 - np.abs(Q.min(1) - V)[10:40].max()) <= 1e-12 * 30
