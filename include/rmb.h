@@ -90,6 +90,14 @@ typedef struct {
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly
                                        instead of replaying it from a captured CUDA graph          */
+#define RMB_FUSED 0x800u  /* rmb_vi / rmb_mpi (+ _group) on DENSE shard handles: the fused multi-GPU
+                             path -- one persistent kernel per rank for the whole solve; each rank
+                             stores its batch results straight into every rank's exchange arrays
+                             (NVLink peer memory, CUDA IPC handles exchanged over the handle's NCCL
+                             communicator) and the ranks meet at an in-kernel cross-rank barrier:
+                             no host round trip or NCCL launch per batch.  Needs the TMA path
+                             (16-byte aligned rows), <= 8 ranks; results bitwise those of one GPU.
+                             With rmb_*_group the G logical ranks share one launch on one device. */
 
 /* Create a handle over a DENSE MDP.
  *   P: [n][A][n] row-major, P[(s*A + a)*n + j] = p(j | s, a), dtype desc->p_dtype.

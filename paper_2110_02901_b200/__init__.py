@@ -28,7 +28,7 @@ OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM,
 F32, F64 = 0, 1
 ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 CHUNKED_T = 0x40
-SPARSE_FULL_GRID, SHARD_NO_GRAPH = 0x80, 0x400
+SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED = 0x80, 0x400, 0x800
 
 _lib = None
 
@@ -267,26 +267,28 @@ class Problem:
         return _vec(V, self.n, "f64", "V"), _vec(pi, self.n, "i32", "pi")
 
     def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-           device="cuda", chunked=False):
+           device="cuda", chunked=False, fused=False):
         """MB-VI: V, pi updated in place (torch cuda/cpu or numpy).
         chunked=True: VI* -- every sweep is T computed in chunks of b
         states against the sweep-start values (RMB_CHUNKED_T)."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_sweeps)
         st = Stats()
-        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
+        flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
+                 | (FUSED if fused else 0))
         s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         return Solution(V, pi, tr[: st.sweeps], s, st)
 
     def mpi(self, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
-            v0_zero=False, device="cuda"):
+            v0_zero=False, device="cuda", fused=False):
         """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_outer * (m + 1))
         ch = np.zeros(max_outer, dtype=np.int64)
         st = Stats()
-        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+        flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+                 | (FUSED if fused else 0))
         s = lib().rmb_mpi(self._h, b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi), _ptr(tr), _ptr(ch),
                           ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
@@ -382,7 +384,7 @@ def _handles(problems):
 
 
 def vi_group(problems, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-             device="cuda"):
+             device="cuda", fused=False):
     """MB-VI over G logical shard handles on one GPU (device-copy exchange)."""
     import torch
     n = problems[0].n
@@ -392,7 +394,7 @@ def vi_group(problems, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None,
     _vec(pi, n, "i32", "pi")
     tr = np.zeros(max_sweeps)
     st = Stats()
-    flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+    flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (FUSED if fused else 0)
     s = lib().rmb_vi_group(_handles(problems), len(problems), b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi),
                            _ptr(tr), ctypes.byref(st))
     _check(s, (OK, NOT_CONVERGED, NONFINITE))
@@ -400,7 +402,7 @@ def vi_group(problems, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None,
 
 
 def mpi_group(problems, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
-              v0_zero=False, device="cuda"):
+              v0_zero=False, device="cuda", fused=False):
     """MB-MPI over G logical shard handles on one GPU."""
     import torch
     n = problems[0].n
@@ -411,7 +413,8 @@ def mpi_group(problems, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=Non
     tr = np.zeros(max_outer * (m + 1))
     ch = np.zeros(max_outer, dtype=np.int64)
     st = Stats()
-    flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+    flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
+             | (FUSED if fused else 0))
     s = lib().rmb_mpi_group(_handles(problems), len(problems), b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi),
                             _ptr(tr), _ptr(ch), ctypes.byref(st))
     _check(s, (OK, NOT_CONVERGED, NONFINITE))

@@ -105,6 +105,9 @@ static void free_problem(Problem* pr)
     pr->pistage.release();
     pr->aux.release();
     pr->rowrec.release();
+    for (int q = 0; q < 8; ++q)
+        if (pr->xpeer_open[q]) cudaIpcCloseMemHandle(pr->xpeer[q]);
+    pr->xbuf.release();
     delete pr;
 }
 
@@ -377,6 +380,7 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     rq.seed = seed;
     rq.k0 = 1;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.fused = flags & RMB_FUSED;
     rq.chunked = flags & RMB_CHUNKED_T;
     rq.eps = eps;
     rq.max_iter = max_sweeps;
@@ -440,6 +444,7 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     rq.seed = seed;
     rq.k0 = 1;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.fused = flags & RMB_FUSED;
     rq.eps = eps;
     rq.max_iter = max_outer;
     rq.pi_given = pi_given;
@@ -552,6 +557,7 @@ rmb_status rmb_vi_group(rmb_problem* hs, int32_t G, int64_t b, uint64_t seed, do
     rq.seed = seed;
     rq.k0 = 1;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.fused = flags & RMB_FUSED;
     rq.eps = eps;
     rq.max_iter = max_sweeps;
     return group_solve(hs, G, rq, flags, V, pi, trace, trace ? max_sweeps : 0, nullptr, 0, stats);
@@ -571,6 +577,7 @@ rmb_status rmb_mpi_group(rmb_problem* hs, int32_t G, int64_t b, int32_t m, uint6
     rq.seed = seed;
     rq.k0 = 1;
     rq.identity = flags & RMB_ORDER_IDENTITY;
+    rq.fused = flags & RMB_FUSED;
     rq.eps = eps;
     rq.max_iter = max_outer;
     rq.pi_given = flags & RMB_PI_GIVEN;

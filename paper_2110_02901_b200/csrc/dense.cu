@@ -49,8 +49,14 @@ constexpr int kPathWarp = 0, kPathTma = 3;  // compute path of a kernel instanti
 // TMA path with V (and pi) in GLOBAL memory (L2-resident) instead of shared
 // memory: dense n too large for a shared-memory copy of V (n > ~27k)
 constexpr int kPathTmaG = 4;
-__host__ __device__ constexpr bool is_tma(int c) { return c == kPathTma || c == kPathTmaG; }
+// kernel instantiations of the fused multi-rank path (K8f): the same two TMA
+// variants with the exchange compiled in (the single-GPU kernels carry none of it)
+constexpr int kPathTmaF = 5, kPathTmaGF = 6;
+__host__ __device__ constexpr bool is_tma(int c) { return c >= kPathTma && c <= kPathTmaGF; }
+__host__ __device__ constexpr bool is_vgl(int c) { return c == kPathTmaG || c == kPathTmaGF; }
+__host__ __device__ constexpr bool is_fused(int c) { return c == kPathTmaF || c == kPathTmaGF; }
 constexpr int64_t kRedundantMax = 8192;    // doubles of batch partials reduced by every CTA
+constexpr int kMaxRanks = 8;               // ranks of a fused multi-GPU group (one NVSwitch box)
 
 // CTA barrier of the 512 compute threads (named barrier 1).  Identical to
 // __syncthreads() for the 512-thread paths; the TMA path adds a producer warp
@@ -118,7 +124,33 @@ struct DenseArgs {
     int tma_piece;       //           columns per stage and row slot
     int tma_static;      //           batches with <= tma_static * grid items are dealt statically
     int tma_slot;        //           bytes per ring slot (piece bytes rounded up to 128)
+    // this rank's CTAs: [cta0, cta0 + nctas) of the launch (several ranks share
+    // one launch when a multi-GPU group is emulated on one device)
+    int cta0, nctas;
+    // fused multi-rank exchange (K8f; xG == 0: off).  Rank xrank of xG owns
+    // states [row0, row1); per batch it backs up its states of the batch and
+    // stores (value, argmin) at the batch position into EVERY rank's xval/xarg
+    // (peer memory), then a cross-rank barrier; every rank then patches its
+    // replica of V from its own xval/xarg.
+    int xG, xrank;
+    double* xval[kMaxRanks];              // per rank: [2][lcap] by batch position (batch parity)
+    int32_t* xarg[kMaxRanks];             // per rank: [2][lcap]
+    unsigned long long* xbar[kMaxRanks];  // per rank: cross-rank arrival counter (monotonic)
+    unsigned long long* ximp[kMaxRanks];  // per rank: [2][kMaxRanks][4] improvement records
+    unsigned long long xbase;             // cross-rank epochs completed before this launch
+    double* xval_own;                     // this rank's entries of the arrays above (no dynamic
+    int32_t* xarg_own;                    //   indexing of parameter arrays in the kernel)
+    unsigned long long* xbar_own;
+    unsigned long long* ximp_own;
+    uint32_t* xlist;                      // this rank: [3][2 xlcap] (position, state) of its batch states
+    unsigned int* xcnt;                   // this rank: [3] list lengths
+    int64_t xlcap;                        // batch positions per xval / xarg parity
+    unsigned long long* xloc;             // this rank: local arrival counter of the cross-rank barrier
+    unsigned long long* xrel;             // this rank: release epoch of the cross-rank barrier
 };
+
+// this CTA's index among its rank's CTAs
+__device__ __forceinline__ int cta_rank(const DenseArgs& a) { return (int)blockIdx.x - a.cta0; }
 
 // ---------------------------------------------------------------- loads
 template <typename PT, int VE>
@@ -398,9 +430,9 @@ __device__ void compute_phase(const DenseArgs& a, const double* Vs, const int32_
     // batches with at most one item per warp: a static deal (CTA-major, so
     // the items spread over all SMs) — 2368 warps grabbing from ONE counter at
     // the same instant serialise on that L2 address for several microseconds
-    const int64_t W = (int64_t)gridDim.x * kWarps;
+    const int64_t W = (int64_t)a.nctas * kWarps;
     const bool stat = items <= W;
-    int64_t static_it = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    int64_t static_it = (int64_t)(threadIdx.x >> 5) * a.nctas + cta_rank(a);
     auto grab = [&]() -> int64_t {
         if (stat) {
             const int64_t r = static_it;
@@ -577,6 +609,8 @@ struct TmaBatch {
     int kind;
     const uint32_t* perm;
     int64_t lo, cnt;
+    const uint32_t* list;  // fused multi-rank sweep batches: this rank's (position, state) pairs
+    const unsigned* lcnt;  //   and their number (final once the compute threads enter the batch)
 };
 
 __device__ __forceinline__ bool tma_segment(const DenseArgs& a, int64_t sg, int& kind, int64_t& k)
@@ -612,6 +646,7 @@ __device__ __forceinline__ bool tma_segment(const DenseArgs& a, int64_t sg, int&
 
 struct TmaSched {
     int64_t sg = 0, lo = -1, k = 0;
+    int64_t sb = 0;  // sweep batches so far (list slot sb % 3)
     int kind = -1;
     __device__ bool next(const DenseArgs& a, TmaBatch& bt)
     {
@@ -625,6 +660,8 @@ struct TmaSched {
             lo = kind == 2 ? a.row0 : 0;
         }
         bt.kind = kind;
+        bt.list = nullptr;
+        bt.lcnt = nullptr;
         if (kind >= 3) {
             bt.perm = a.olist;
             bt.lo = 0;
@@ -640,6 +677,11 @@ struct TmaSched {
             bt.lo = lo;
             bt.cnt = min(a.b, a.n - lo);
             lo += a.b;
+            if (a.xG > 0) {
+                bt.list = a.xlist + (sb % 3) * 2 * a.xlcap;
+                bt.lcnt = a.xcnt + (sb % 3);
+            }
+            ++sb;
         }
         return true;
     }
@@ -679,13 +721,14 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
     TmaSched sc;
     TmaBatch bt;
     int prev_kind = -1;
-    const unsigned G = gridDim.x;
+    const unsigned G = (unsigned)a.nctas;
     for (long long q = 0; !stop && sc.next(a, bt); ++q) {
         // run-ahead bound: one batch past the compute threads; fenced batches
         // (the first, and B_{pi,b} batches right after an improvement) wait
         // until the compute threads are in them
         const bool fence = q == 0 || ((bt.kind == 1 || bt.kind == 4) && prev_kind == 2) ||
-                           (bt.perm != nullptr && bt.kind <= 1 && bt.lo == 0 && a.b >= a.n);
+                           (bt.perm != nullptr && bt.kind <= 1 && bt.lo == 0 && a.b >= a.n) ||
+                           bt.list != nullptr;  // fused: the batch's list is built during the previous batch
         {
             SpinGuard sg;
             while (true) {
@@ -698,6 +741,7 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
         }
         if (stop) break;
         prev_kind = bt.kind;
+        if (bt.list) bt.cnt = (int64_t)__ldcg(bt.lcnt);
         const bool eval = bt.kind == 1 || bt.kind == 4;
         const Plan& pl = a.plan[eval ? 1 : (bt.kind == 2 ? 2 : 0)];
         const int NG = eval ? 1 : pl.ng;
@@ -717,7 +761,7 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
         // failing grabs return multiples of g from fail0 on; each producer does
         // exactly one, and the last of them re-arms the counter
         const unsigned fail0 = (items + g - 1) / g * g;
-        unsigned r = stat ? blockIdx.x : atomicAdd(ctr, g);
+        unsigned r = stat ? (unsigned)cta_rank(a) : atomicAdd(ctr, g);
         unsigned r_end = stat ? r + 1 : r + g;
         const unsigned nvecs = (unsigned)(n / VB);
         while (true) {
@@ -728,11 +772,19 @@ __device__ void tma_producer(const DenseArgs& a, const int32_t* pis, const TmaSm
             // next grab, in flight while this one streams
             const bool local = !stat && r + 1 < r_end && r + 1 < items;
             const unsigned rn = stat ? r + G : (local ? r + 1 : atomicAdd(ctr, g));
-            const unsigned i = r / per_state;
-            const unsigned rr = r - i * per_state;
+            const unsigned j = r / per_state;
+            const unsigned rr = r - j * per_state;
             const unsigned ag = rr / C;
             const unsigned ch = rr - ag * C;
-            const int64_t s = bt.perm ? (int64_t)__ldcg(bt.perm + bt.lo + i) : bt.lo + i;
+            // batch position i and state s of list entry j
+            unsigned i = j;
+            int64_t s;
+            if (bt.list) {
+                i = __ldcg(bt.list + 2 * j);
+                s = (int64_t)__ldcg(bt.list + 2 * j + 1);
+            } else {
+                s = bt.perm ? (int64_t)__ldcg(bt.perm + bt.lo + j) : bt.lo + j;
+            }
             const int a0 = eval ? ld_pi(pis, s) : (int)ag * NG;
             const int na = eval ? 1 : min(NG, a.A - a0);
             // columns [c0, c1) (vector aligned) of the group's rows
@@ -916,11 +968,24 @@ __device__ __forceinline__ void reduce_state_F(const DenseArgs& a, const double*
 // butterfly), Q = c + gamma*sum goes to smem Qs, then a thread per state takes
 // the argmin over actions in index order (lowest index on ties).  sink(i, s,
 // v, arg) is called by exactly one thread per state.
+// olist != null (fused multi-rank batches): the entries are this rank's
+// states of the batch, olist[2j] = batch position, olist[2j+1] = state, and
+// cnt is their number.
 template <typename PT, bool EVAL, typename Sink>
 __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double* part, int C, const uint32_t* perm,
                                                 int64_t lo, int64_t cnt, int64_t first, int64_t step,
-                                                const int32_t* pis, double* Qs, Sink&& sink, bool raw = false)
+                                                const int32_t* pis, double* Qs, Sink&& sink, bool raw = false,
+                                                const uint32_t* olist = nullptr)
 {
+    auto pos_state = [&](int64_t j, int64_t& i, int64_t& s) {
+        if (olist) {
+            i = (int64_t)__ldcg(olist + 2 * j);
+            s = (int64_t)__ldcg(olist + 2 * j + 1);
+        } else {
+            i = j;
+            s = perm ? (int64_t)__ldcg(perm + lo + j) : lo + j;
+        }
+    };
     // partial layout: (i, a, ch) -> (i*A + a)*C + ch, stride 1 over ch; raw
     // (TMA path, min modes): ((i*NAG + a/kAG)*C + ch)*kAG + a%kAG, stride kAG
     const int NAGr = (a.A + kAG - 1) / kAG;
@@ -941,8 +1006,8 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
             for (int64_t q = threadIdx.x; q < m * Ae; q += kThreads) {
                 const int64_t kk = q / Ae;
                 const int ai = (int)(q - kk * Ae);
-                const int64_t i = first + (k0 + kk) * step;
-                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                int64_t i, s;
+                pos_state(first + (k0 + kk) * step, i, s);
                 const int act = EVAL ? ld_pi(pis, s) : ai;
                 const double* pp = part + pbase(i, act);
                 double sum = 0.0;
@@ -953,8 +1018,8 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
             for (int64_t q = warp; q < m * Ae; q += kWarps) {
                 const int64_t kk = q / Ae;
                 const int ai = (int)(q - kk * Ae);
-                const int64_t i = first + (k0 + kk) * step;
-                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                int64_t i, s;
+                pos_state(first + (k0 + kk) * step, i, s);
                 const int act = EVAL ? ld_pi(pis, s) : ai;
                 const double* pp = part + pbase(i, act);
                 double sum = 0.0;
@@ -965,8 +1030,8 @@ __device__ __forceinline__ void reduce_states_S(const DenseArgs& a, const double
         }
         csync();
         for (int64_t kk = threadIdx.x; kk < m; kk += kThreads) {
-            const int64_t i = first + (k0 + kk) * step;
-            const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+            int64_t i, s;
+            pos_state(first + (k0 + kk) * step, i, s);
             double best = Qs[kk * Ae];
             int barg = EVAL ? ld_pi(pis, s) : 0;
             if (!EVAL)
@@ -1015,7 +1080,7 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
     }
     if (KIND >= 3) {
         acc.bad |= !isfinite(v);
-        if (blockIdx.x == 0) {
+        if (cta_rank(a) == 0) {
             a.send_val[i] = v;
             a.send_idx[i] = (uint32_t)s;
             a.send_arg[i] = arg;
@@ -1026,7 +1091,7 @@ __device__ __forceinline__ void patch_state(const DenseArgs& a, double* Vs, int3
     const double old = Vs[vi];
     acc.rmax = fmax(acc.rmax, fabs(v - old));
     acc.bad |= !isfinite(v);
-    const bool writer = blockIdx.x == 0;
+    const bool writer = cta_rank(a) == 0;
     if (KIND == 0 && a.vnext) {  // chunked T (VI*): the smem V keeps the sweep-start values
         if (writer) {
             a.vnext[s] = v;
@@ -1055,11 +1120,14 @@ struct Ctx {
     int tst;
     unsigned tph;
     long long gred_seq;  // global-V path: grid reductions so far (ring slot)
+    unsigned long long xepoch;  // fused multi-rank: cross-rank barriers so far in this launch
+    long long nimp;             //                   improvements so far (record parity)
+    bool cta0;                  // this is CTA 0 of its rank (phase profile)
 };
 
 __device__ __forceinline__ void prof_mark(Ctx& x, long long* slot)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (x.cta0 && threadIdx.x == 0) {
         const unsigned long long t = globaltimer_ns();
         *slot += (long long)(t - x.t_mark);
         x.t_mark = t;
@@ -1072,6 +1140,122 @@ __device__ __forceinline__ void timed_sync(Ctx& x)
     grid_sync<kThreads>(x.g);
     prof_mark(x, &x.t_bar);
     x.n_bar++;
+}
+
+// ------------------------------------------- fused multi-rank exchange (K8f)
+__device__ __forceinline__ void red_release_add_sys(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+template <typename F>
+__device__ __forceinline__ void spin_until(F&& done, const DenseArgs& a)
+{
+    unsigned spins = 0;
+    unsigned long long t0 = 0;
+    while (!done()) {
+        if (++spins == 4096u) {
+            spins = 0;
+            const unsigned long long t = globaltimer_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 30ull * 1000000000ull) {  // a rank is gone: fail loudly, do not wedge the GPU
+                atomicExch(a.err, 2);
+                __trap();
+            }
+        }
+    }
+}
+
+// Cross-rank barrier: every CTA of every rank.  The CTAs of a rank arrive on a
+// local counter (after a system-scope fence: their peer stores are visible to
+// every rank first); the rank's leader (CTA 0) signals every rank's arrival
+// counter, waits for all G signals of this epoch on its own, and releases its
+// CTAs.  Counters are monotonic across launches (a.xbase), so no rank ever
+// needs to reset a counter another rank may already be signalling.
+__device__ void xrank_sync(const DenseArgs& a, Ctx& x)
+{
+    prof_mark(x, &x.t_comp);
+    csync();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned long long e = ++x.xepoch;
+        red_release_add(a.xloc, 1ull);
+        if (cta_rank(a) == 0) {
+            const unsigned long long local = e * (unsigned long long)a.nctas;
+            spin_until([&] { return ld_acquire_gpu(a.xloc) >= local; }, a);
+            __threadfence_system();
+#pragma unroll
+            for (int r = 0; r < kMaxRanks; ++r)
+                if (r < a.xG) red_release_add_sys(a.xbar[r], 1ull);
+            const unsigned long long all = (a.xbase + e) * (unsigned long long)a.xG;
+            spin_until([&] { return ld_acquire_sys(a.xbar_own) >= all; }, a);
+            st_release_gpu(a.xrel, e);
+        } else {
+            spin_until([&] { return ld_acquire_gpu(a.xrel) >= e; }, a);
+        }
+    }
+    csync();
+    prof_mark(x, &x.t_bar);
+    x.n_bar++;
+}
+
+// This rank's states of the sweep batch with sequence number sb (positions
+// [lo, lo + cnt) of perm, or lo + i for the identity order) into list slot
+// sb % 3 as (position, state) pairs.  Order-free (no state's arithmetic
+// depends on the list order).  Run by all compute threads of the rank.
+__device__ void build_own_list(const DenseArgs& a, const uint32_t* perm, int64_t lo, int64_t cnt, int64_t sb)
+{
+    uint32_t* list = a.xlist + (sb % 3) * 2 * a.xlcap;
+    unsigned int* count = a.xcnt + (sb % 3);
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)a.nctas * kThreads;
+    for (int64_t i0 = (int64_t)cta_rank(a) * kThreads; i0 < cnt; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        int64_t s = -1;
+        if (i < cnt) s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+        const bool own = i < cnt && s >= a.row0 && s < a.row1;
+        const unsigned m = __ballot_sync(0xffffffffu, own);
+        unsigned base = 0;
+        if (lane == 0 && m) base = atomicAdd(count, (unsigned)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (own) {
+            const unsigned k = base + __popc(m & ((1u << lane) - 1u));
+            list[2 * k] = (uint32_t)i;
+            list[2 * k + 1] = (uint32_t)s;
+        }
+    }
+}
+
+// Fused improvement: this rank's (residual, changed, bad) to every rank, then
+// every rank reduces all G records (the improvement covers owned states only).
+__device__ PhaseAcc xrank_reduce(const DenseArgs& a, Ctx& x, PhaseAcc r)
+{
+    const int par = (int)(x.nimp++ & 1);
+    if (cta_rank(a) == 0 && threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < kMaxRanks; ++q) {
+            if (q < a.xG) {
+                unsigned long long* rec = a.ximp[q] + ((size_t)par * kMaxRanks + a.xrank) * 4;
+                rec[0] = (unsigned long long)__double_as_longlong(r.rmax);
+                rec[1] = (unsigned long long)r.changed;
+                rec[2] = (unsigned long long)r.bad;
+            }
+        }
+    }
+    xrank_sync(a, x);
+    PhaseAcc g{0.0, 0, 0};
+    const unsigned long long* mine = a.ximp_own + (size_t)par * kMaxRanks * 4;
+    for (int q = 0; q < a.xG; ++q) {
+        g.rmax = fmax(g.rmax, __longlong_as_double((long long)__ldcg(mine + 4 * q)));
+        g.changed += (long long)__ldcg(mine + 4 * q + 1);
+        g.bad |= (int)__ldcg(mine + 4 * q + 2);
+    }
+    return g;
 }
 
 
@@ -1162,9 +1346,12 @@ __device__ __forceinline__ void fast_finish(const DenseArgs& a, double* Vs, int3
 }
 
 // One batch (or improvement sub-batch): compute -> barrier -> combine/patch.
+// Fused multi-rank sweeps (a.xG > 0): (perm_next, lo_next, cnt_next) is the
+// next sweep batch, whose list of this rank's states is built now.
 template <typename PT, int VE, int KIND, int CTA>
 __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, const uint32_t* perm, int64_t lo,
-                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k)
+                          int64_t cnt, const Plan& pl, PhaseAcc& acc, double* Qs, int64_t fill_next_k,
+                          const uint32_t* perm_next = nullptr, int64_t lo_next = 0, int64_t cnt_next = 0)
 {
     constexpr bool EVAL = KIND == 1 || KIND == 4;
     double* part = a.part + (x.phase & 1) * a.part_stride;
@@ -1172,7 +1359,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
         // the producer may now run one batch ahead of this one (counters are
         // re-armed by the producers themselves)
         if (threadIdx.x == 0) st_release_cta(x.tm.ctl, x.phase);
-    } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+    } else if (cta_rank(a) == 0 && threadIdx.x == 0) {
         // the other parity's work counter was last used before the previous
         // barrier: CTA 0 rearms it for the next phase (ordered by this phase's barrier)
         atomicExch(a.wctr + ((x.phase + 1) & 1), 0u);
@@ -1180,16 +1367,21 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     // one compute path per kernel instantiation (register allocation is per
     // kernel: mixing paths made every path spill)
     if constexpr (is_tma(CTA))
-        compute_phase_tma<PT, EVAL, CTA == kPathTmaG>(a, Vs, pl, part, x.tm, x.tst, x.tph);
+        compute_phase_tma<PT, EVAL, is_vgl(CTA)>(a, Vs, pl, part, x.tm, x.tst, x.tph);
     else
         compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
     if (fill_next_k > 0) {  // next sweep's order, off the critical path
         Permutation pm;
         pm.init(a.n, a.seed, fill_next_k);
         uint32_t* dst = a.perm + (fill_next_k % 3) * a.n;
-        const int64_t stride = (int64_t)gridDim.x * kThreads;
-        for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < a.n; p += stride)
+        const int64_t stride = (int64_t)a.nctas * kThreads;
+        for (int64_t p = (int64_t)cta_rank(a) * kThreads + threadIdx.x; p < a.n; p += stride)
             dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+    constexpr bool fused = is_fused(CTA) && KIND <= 1;
+    if constexpr (fused) {
+        if (cta_rank(a) == 0 && threadIdx.x == 0) a.xcnt[(x.batches + 2) % 3] = 0u;  // slot of batch sb - 1
+        if (cnt_next > 0) build_own_list(a, perm_next, lo_next, cnt_next, x.batches + 1);
     }
     constexpr int AeK = EVAL ? 1 : 0;
     const int Ae = AeK ? 1 : a.A;
@@ -1198,17 +1390,56 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     // share): the same states take the same summation order for any G
     const int64_t plan_cnt = KIND == 2 ? a.imp_sub : a.b;
     const bool fast = CTA == kPathTma && pl.raw && pl.redundant && pl.C <= 4 && L <= 32 &&
-                      plan_cnt * L <= (int64_t)kFastK * kThreads;
+                      plan_cnt * L <= (int64_t)kFastK * kThreads && !fused;
     FastPre fp;
     if (fast) fast_pre<PT, EVAL>(a, perm, lo, cnt, pis, L, fp);
     timed_sync(x);
     const bool F = pl.C == 1 && !pl.raw;
     auto patch = [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND>(a, Vs, pis, i, s, v, arg, acc); };
-    if constexpr (CTA == kPathTmaG) {
+    if constexpr (fused) {
+        // CTA x finishes this rank's states x, x + grid, ... of the batch and
+        // stores (value, argmin) at their batch positions into every rank's
+        // exchange arrays; after the cross-rank barrier every rank patches all
+        // of the batch from its own arrays (Eq. 12: no state of the batch is
+        // patched before every read of the batch is done, on every rank)
+        const int64_t sb = x.batches;
+        const uint32_t* ol = a.xlist + (sb % 3) * 2 * a.xlcap;
+        const int64_t own = (int64_t)__ldcg(a.xcnt + (sb % 3));
+        const size_t par = (size_t)(sb & 1) * (size_t)a.xlcap;
+        reduce_states_S<PT, EVAL>(
+            a, part, pl.C, nullptr, 0, own, cta_rank(a), a.nctas, pis, Qs,
+            [&](int64_t i, int64_t s, double v, int arg) {
+                (void)s;
+#pragma unroll
+                for (int r = 0; r < kMaxRanks; ++r) {
+                    if (r < a.xG) {
+                        a.xval[r][par + i] = v;
+                        a.xarg[r][par + i] = arg;
+                    }
+                }
+            },
+            true, ol);
+        xrank_sync(a, x);
+        const double* xv = a.xval_own + par;
+        const int32_t* xa = a.xarg_own + par;
+        if constexpr (is_vgl(CTA)) {
+            const int64_t stride = (int64_t)a.nctas * kThreads;
+            for (int64_t i = (int64_t)cta_rank(a) * kThreads + threadIdx.x; i < cnt; i += stride) {
+                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                patch_state<KIND, true>(a, Vs, pis, i, s, __ldcg(xv + i), __ldcg(xa + i), acc);
+            }
+            timed_sync(x);
+        } else {
+            for (int64_t i = threadIdx.x; i < cnt; i += kThreads) {
+                const int64_t s = perm ? (int64_t)__ldcg(perm + lo + i) : lo + i;
+                patch_state<KIND>(a, Vs, pis, i, s, __ldcg(xv + i), __ldcg(xa + i), acc);
+            }
+        }
+    } else if constexpr (is_vgl(CTA)) {
         // global V: CTA x finishes and writes the states x, x + grid, ...; a
         // second barrier makes the batch visible before the next batch reads
         reduce_states_S<PT, EVAL>(
-            a, part, pl.C, perm, lo, cnt, blockIdx.x, gridDim.x, pis, Qs,
+            a, part, pl.C, perm, lo, cnt, cta_rank(a), a.nctas, pis, Qs,
             [&](int64_t i, int64_t s, double v, int arg) { patch_state<KIND, true>(a, Vs, pis, i, s, v, arg, acc); },
             true);
         timed_sync(x);
@@ -1217,7 +1448,7 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
     } else if (pl.raw && !pl.redundant) {
         // distributed combine: CTA x finishes the states x, x + grid, ... into
         // the list, a second grid barrier, then every CTA patches from it
-        reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, blockIdx.x, gridDim.x, pis, Qs,
+        reduce_states_S<PT, EVAL>(a, part, pl.C, perm, lo, cnt, cta_rank(a), a.nctas, pis, Qs,
                                   [&](int64_t i, int64_t s, double v, int arg) {
                                       (void)s;
                                       a.lval[i] = v;
@@ -1281,7 +1512,7 @@ __device__ PhaseAcc grid_reduce(const DenseArgs& a, Ctx& x, PhaseAcc v)
 {
     PhaseAcc r = block_reduce(v);
     unsigned long long* slot = a.gred + 4 * (x.gred_seq & 3);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // re-arm the slot used two reductions ahead
+    if (cta_rank(a) == 0 && threadIdx.x == 0) {  // re-arm the slot used two reductions ahead
         unsigned long long* z = a.gred + 4 * ((x.gred_seq + 2) & 3);
         atomicExch(z, 0ull);
         atomicExch(z + 1, 0ull);
@@ -1304,7 +1535,7 @@ __device__ PhaseAcc grid_reduce(const DenseArgs& a, Ctx& x, PhaseAcc v)
 template <int CTA>
 __device__ __forceinline__ PhaseAcc phase_reduce(const DenseArgs& a, Ctx& x, PhaseAcc v)
 {
-    if constexpr (CTA == kPathTmaG) return grid_reduce(a, x, v);
+    if constexpr (is_vgl(CTA)) return grid_reduce(a, x, v);
     else return block_reduce(v);
 }
 
@@ -1317,24 +1548,29 @@ __device__ PhaseAcc run_sweep(const DenseArgs& a, Ctx& x, double* Vs, int32_t* p
     PhaseAcc acc{0.0, 0, 0};
     for (int64_t lo = 0; lo < a.n; lo += a.b) {
         const int64_t cnt = min(a.b, a.n - lo);
+        // the next sweep batch: later in this sweep, or the first of the next
+        // sweep (its order is drawn in this sweep's batch 0)
+        const bool more = lo + a.b < a.n;
+        const uint32_t* pn = more ? perm : (a.identity ? nullptr : a.perm + ((k + 1) % 3) * a.n);
         run_batch<PT, VE, EVAL ? 1 : 0, CTA>(a, x, Vs, pis, perm, lo, cnt, pl, acc, Qs,
-                                         (lo == 0 && !a.identity) ? k + 1 : 0);
+                                         (lo == 0 && !a.identity) ? k + 1 : 0, pn, more ? lo + a.b : 0,
+                                         more ? min(a.b, a.n - lo - a.b) : min(a.b, a.n));
         ++x.batches;
     }
     if (!EVAL && a.vnext) {
         // chunked T (VI*): every chunk read the sweep-start values; the
         // new values were parked in vnext and land now, for the next sweep
         timed_sync(x);
-        if constexpr (CTA == kPathTmaG) {
-            const int64_t stride = (int64_t)gridDim.x * kThreads;
-            for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < a.n; j += stride)
+        if constexpr (is_vgl(CTA)) {
+            const int64_t stride = (int64_t)a.nctas * kThreads;
+            for (int64_t j = (int64_t)cta_rank(a) * kThreads + threadIdx.x; j < a.n; j += stride)
                 a.V[j] = __ldcg(a.vnext + j);
             timed_sync(x);
         } else {
             for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
                 const double v = __ldcg(a.vnext + j);
                 Vs[vs_index(j, a.vs_half)] = v;
-                if (blockIdx.x == 0) a.V[j] = v;
+                if (cta_rank(a) == 0) a.V[j] = v;
             }
             csync();
         }
@@ -1350,7 +1586,9 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
         const int64_t cnt = min(a.imp_sub, a.row1 - lo);
         run_batch<PT, VE, 2, CTA>(a, x, Vs, pis, nullptr, lo, cnt, a.plan[2], acc, Qs, 0);
     }
-    return phase_reduce<CTA>(a, x, acc);
+    PhaseAcc r = phase_reduce<CTA>(a, x, acc);
+    if constexpr (is_fused(CTA)) r = xrank_reduce(a, x, r);  // each rank improved its own states
+    return r;
 }
 
 template <typename PT, int VE, int CTA>
@@ -1365,9 +1603,10 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
                          a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
     const bool shard = a.mode == MODE_SHARD_MIN || a.mode == MODE_SHARD_EVAL || a.mode == MODE_SHARD_IMPROVE;
 
-    Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err}, 0, 0, 0, 0, 0, 0, 0};
+    Ctx x{{a.bar, a.bar + 32, 0ull, (unsigned long long)a.nctas, a.err}, 0, 0, 0, 0, 0, 0, 0};
+    x.cta0 = cta_rank(a) == 0;
     x.gred_seq = 0;
-    if constexpr (CTA == kPathTmaG) {  // V and pi stay in global memory (L2)
+    if constexpr (is_vgl(CTA)) {  // V and pi stay in global memory (L2)
         Vs = a.V;
         pis = a.pi;
     }
@@ -1391,23 +1630,27 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
             return;
         }
     }
-    if constexpr (CTA != kPathTmaG) {
+    if constexpr (!is_vgl(CTA)) {
         for (int64_t j = threadIdx.x; j < a.n; j += kThreads) {
             Vs[vs_index(j, a.vs_half)] = a.V[j];
             if (need_pi) pis[j] = a.pi[j];
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
+    if (cta_rank(a) == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
     if (!a.identity && a.mode != MODE_IMPROVE && !shard) {
         Permutation pm;
         pm.init(a.n, a.seed, a.k0);
         uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
-        for (int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x; p < a.n; p += (int64_t)gridDim.x * kThreads)
+        for (int64_t p = (int64_t)cta_rank(a) * kThreads + threadIdx.x; p < a.n; p += (int64_t)a.nctas * kThreads)
             dst[p] = (uint32_t)pm((uint64_t)p);
     }
     timed_sync(x);  // perm of the first sweep visible; also orders the smem loads
+    if (is_fused(CTA) && a.mode != MODE_IMPROVE) {  // fused: this rank's states of the first sweep batch
+        build_own_list(a, a.identity ? nullptr : a.perm + (a.k0 % 3) * a.n, 0, min(a.b, a.n), 0);
+        timed_sync(x);
+    }
 
-    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool lead = cta_rank(a) == 0 && threadIdx.x == 0;
     long long status = RMB_ERR_NOT_CONVERGED;
     int64_t k = a.k0, it = 0, outer = 0;
     long long changed = 0;
@@ -1487,6 +1730,7 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
         a.prof[1] = x.t_bar;
         a.prof[2] = x.t_comb;
         a.prof[3] = x.n_bar;
+        a.out[OUT_XEPOCHS] = (long long)x.xepoch;
     }
     if constexpr (is_tma(CTA)) {
         csync();  // every compute thread is done with the ring
@@ -1508,6 +1752,13 @@ template <typename PT, int VE, bool VGL>
 __global__ void __launch_bounds__(kTmaThreads, 1) dense_tma_kernel(const DenseArgs a)
 {
     dense_solver_body<PT, VE, VGL ? kPathTmaG : kPathTma>(a);
+}
+
+// one rank of a fused multi-GPU group (K8f), one launch per device
+template <typename PT, int VE, bool VGL>
+__global__ void __launch_bounds__(kTmaThreads, 1) dense_tma_fused_kernel(const DenseArgs a)
+{
+    dense_solver_body<PT, VE, VGL ? kPathTmaGF : kPathTmaF>(a);
 }
 
 // ------------------------------------------------------------------ host
@@ -1748,8 +1999,10 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     return RMB_OK;
 }
 
-static cudaError_t dense_launch(Problem& pr, const DenseLaunch& L, cudaStream_t st)
+static cudaError_t dense_launch(Problem& pr, DenseLaunch& L, cudaStream_t st)
 {
+    L.a.cta0 = 0;
+    L.a.nctas = pr.num_sms;
     cudaError_t ce = cudaMemsetAsync(L.a.bar, 0, 4096, st);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(L.a.scnt, 0, (size_t)L.lcap * 4, st);
     if (ce != cudaSuccess) return ce;
@@ -1819,6 +2072,218 @@ rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, i
     res->launches = 1;
     for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
     pr.last_launches = 1;
+    return RMB_OK;
+}
+
+}  // namespace rmb
+
+namespace rmb {
+
+// ------------------------------------------------------------------ K8f
+// Multi-GPU solve with the exchange fused into the persistent kernel (SURVEY
+// 8(e) "B200-native fused path"): no host round trip, no NCCL launch per
+// batch -- each rank stores its batch results straight into every rank's
+// exchange arrays over NVLink (peer memory) and the ranks meet at an in-kernel
+// cross-rank barrier.  Each state's arithmetic is the single-GPU kernel's
+// (plan from (n, A, b) and the device's SM count), so V, pi and the trace are
+// bitwise those of one GPU.
+
+// Every rank of a group launches with one DenseArgs; with G logical ranks on
+// one device the launch holds all of them (CTA groups of `per` CTAs).
+template <typename PT, int VE, bool VGL>
+__global__ void __launch_bounds__(kTmaThreads, 1) dense_tma_group_kernel(const DenseArgs* __restrict__ set, int per)
+{
+    dense_solver_body<PT, VE, VGL ? kPathTmaGF : kPathTmaF>(set[blockIdx.x / per]);
+}
+
+// exchange buffer layout for batches of up to `cap` positions
+struct XLayout {
+    size_t val, arg, bar, imp, list, cnt, bytes;
+    explicit XLayout(int64_t cap)
+    {
+        auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+        val = 0;
+        arg = up(val + (size_t)2 * cap * 8);
+        bar = up(arg + (size_t)2 * cap * 4);
+        imp = up(bar + 8);
+        list = up(imp + (size_t)2 * kMaxRanks * 4 * 8);
+        cnt = up(list + (size_t)3 * 2 * cap * 4);
+        bytes = up(cnt + 3 * 4);
+    }
+};
+
+rmb_status fused_buffer(Problem& pr)
+{
+    const XLayout X(pr.n);
+    if (pr.xbuf.p && pr.xbuf.bytes >= X.bytes) return RMB_OK;
+    if (pr.xpeer_G > 0) {
+        set_error("fused solve: exchange buffer already shared with peers");
+        return RMB_ERR_INVALID_ARG;
+    }
+    if (pr.xbuf.ensure(X.bytes) != cudaSuccess) {
+        set_error("fused solve: exchange buffer allocation failed");
+        return RMB_ERR_OOM;
+    }
+    cudaError_t e = cudaMemsetAsync(pr.xbuf.p, 0, X.bytes, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) {
+        set_error(std::string("fused solve: ") + cudaGetErrorString(e));
+        return RMB_ERR_CUDA;
+    }
+    pr.xepochs = 0;
+    return RMB_OK;
+}
+
+rmb_status dense_fused_solve(Problem** ranks, int G, bool nccl, const SolveRequest& rq0, double* trace_host,
+                             int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res)
+{
+    Problem& p0 = *ranks[0];
+    const int L = nccl ? 1 : G;  // ranks in this launch
+    int world = G, me = 0;
+    if (nccl) {
+        rmb_status s = fused_peers(p0, &world, &me);  // shard.cu: IPC handles over NCCL
+        if (s != RMB_OK) return s;
+    }
+    if (world > kMaxRanks) {
+        set_error("fused solve: at most 8 ranks");
+        return RMB_ERR_UNSUPPORTED;
+    }
+    const XLayout X(p0.n);
+    std::vector<DenseLaunch> Ls((size_t)L);
+    for (int r = 0; r < L; ++r) {
+        Problem& pr = *ranks[r];
+        if (!nccl) {
+            rmb_status s = fused_buffer(pr);
+            if (s != RMB_OK) return s;
+        }
+        SolveRequest rq = rq0;
+        rq.V = pr.stage_V;
+        rq.pi = pr.stage_pi;
+        if (pr.trace.ensure((size_t)std::max<int64_t>(1, trace_len) * 8) != cudaSuccess ||
+            pr.chg.ensure((size_t)std::max<int64_t>(1, chg_len) * 8) != cudaSuccess) {
+            set_error("fused solve: trace allocation failed");
+            return RMB_ERR_OOM;
+        }
+        rmb_status s = dense_prepare(pr, rq, static_cast<double*>(pr.trace.p), trace_len,
+                                     static_cast<long long*>(pr.chg.p), chg_len, Ls[r]);
+        if (s != RMB_OK) return s;
+        DenseArgs& a = Ls[r].a;
+        if (!is_tma(a.path)) {
+            set_error("fused solve: needs the TMA path (16-byte aligned rows, RMB_DENSE_NO_TMA unset)");
+            return RMB_ERR_UNSUPPORTED;
+        }
+        if (Ls[r].smem != Ls[0].smem || Ls[r].lcap > p0.n) {
+            set_error("fused solve: ranks disagree on the launch shape");
+            return RMB_ERR_INVALID_ARG;
+        }
+        a.xG = world;
+        a.xrank = nccl ? me : r;
+        for (int q = 0; q < world; ++q) {
+            char* base = static_cast<char*>(nccl ? p0.xpeer[q] : ranks[q]->xbuf.p);
+            a.xval[q] = reinterpret_cast<double*>(base + X.val);
+            a.xarg[q] = reinterpret_cast<int32_t*>(base + X.arg);
+            a.xbar[q] = reinterpret_cast<unsigned long long*>(base + X.bar);
+            a.ximp[q] = reinterpret_cast<unsigned long long*>(base + X.imp);
+        }
+        a.xval_own = a.xval[a.xrank];
+        a.xarg_own = a.xarg[a.xrank];
+        a.xbar_own = a.xbar[a.xrank];
+        a.ximp_own = a.ximp[a.xrank];
+        char* own = static_cast<char*>(pr.xbuf.p);
+        a.xlist = reinterpret_cast<uint32_t*>(own + X.list);
+        a.xcnt = reinterpret_cast<unsigned int*>(own + X.cnt);
+        a.xlcap = p0.n;
+        a.xbase = (unsigned long long)pr.xepochs;
+        unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
+        a.xloc = ctrl + 352;
+        a.xrel = ctrl + 384;
+    }
+    const int per = nccl ? p0.num_sms : p0.num_sms / L;
+    if (per < 1) {
+        set_error("fused solve: more logical ranks than SMs");
+        return RMB_ERR_UNSUPPORTED;
+    }
+    cudaStream_t st = p0.stream;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaEventRecord(e0, st);
+    for (int r = 0; r < L && ce == cudaSuccess; ++r) {
+        DenseLaunch& D = Ls[r];
+        D.a.cta0 = r * per;
+        D.a.nctas = per;
+        ce = cudaMemsetAsync(D.a.bar, 0, 4096, st);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(D.a.scnt, 0, (size_t)D.lcap * 4, st);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(D.a.xcnt, 0, 3 * 4, st);
+    }
+    const DenseLaunch& D0 = Ls[0];
+    const bool f32 = ranks[0]->pdt == RMB_F32;
+    const bool vgl = D0.a.path == kPathTmaG;
+    if (ce == cudaSuccess) {
+        // same launch shape for every instantiation: 544 threads, D0.smem bytes
+        const void* kern = f32 ? (vgl ? (const void*)dense_tma_group_kernel<float, 4, true>
+                                      : (const void*)dense_tma_group_kernel<float, 4, false>)
+                               : (vgl ? (const void*)dense_tma_group_kernel<double, 2, true>
+                                      : (const void*)dense_tma_group_kernel<double, 2, false>);
+        ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D0.smem);
+        // the argument sets live in device memory (rank 0's aux buffer)
+        if (ce == cudaSuccess && p0.aux.ensure(sizeof(DenseArgs) * (size_t)L + 256) != cudaSuccess)
+            ce = cudaErrorMemoryAllocation;
+        std::vector<DenseArgs> host((size_t)L);
+        for (int r = 0; r < L; ++r) host[r] = Ls[r].a;
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(p0.aux.p, host.data(), sizeof(DenseArgs) * (size_t)L, cudaMemcpyHostToDevice, st);
+        if (ce == cudaSuccess && L == 1) {
+            // one rank per device: the regular entry (arguments in parameter space)
+            const void* k1 = f32 ? (vgl ? (const void*)dense_tma_fused_kernel<float, 4, true>
+                                        : (const void*)dense_tma_fused_kernel<float, 4, false>)
+                                 : (vgl ? (const void*)dense_tma_fused_kernel<double, 2, true>
+                                        : (const void*)dense_tma_fused_kernel<double, 2, false>);
+            ce = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D0.smem);
+            void* args[] = {&host[0]};
+            if (ce == cudaSuccess)
+                ce = cudaLaunchCooperativeKernel(k1, dim3(per), dim3(kTmaThreads), args, D0.smem, st);
+        } else if (ce == cudaSuccess) {
+            const DenseArgs* set = static_cast<const DenseArgs*>(p0.aux.p);
+            int per_arg = per;
+            void* args[] = {&set, &per_arg};
+            ce = cudaLaunchCooperativeKernel(kern, dim3(per * L), dim3(kTmaThreads), args, D0.smem, st);
+        }
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // the host copy of the args stays alive until here
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
+    long long out[OUT_N + 4] = {0};
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, D0.a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, D0.a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && trace_host && trace_len > 0)
+        ce = cudaMemcpyAsync(trace_host, D0.a.trace, (size_t)trace_len * 8, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && chg_host && chg_len > 0)
+        ce = cudaMemcpyAsync(chg_host, D0.a.chg, (size_t)chg_len * 8, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) {
+        set_error(std::string("fused solve: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    res->sweeps = out[OUT_SWEEPS];
+    res->outer = out[OUT_OUTER];
+    res->status = (int)out[OUT_STATUS];
+    double d;
+    memcpy(&d, &out[OUT_RESID_BITS], 8);
+    res->final_resid = d;
+    res->batches = out[OUT_BATCHES];
+    res->changed = out[OUT_CHANGED];
+    res->ms = ms;
+    res->launches = 1;
+    for (int r = 0; r < L; ++r) {
+        ranks[r]->xepochs += out[OUT_XEPOCHS];  // every rank ran the same epochs
+        ranks[r]->last_launches = 1;
+        ranks[r]->last_graph_launches = 0;
+        for (int i = 0; i < 4; ++i) ranks[r]->prof[i] = out[OUT_N + i];
+    }
     return RMB_OK;
 }
 

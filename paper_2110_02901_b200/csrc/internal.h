@@ -31,6 +31,7 @@ enum OutSlot : int {
     OUT_RESID_BITS = 3,
     OUT_BATCHES = 4,
     OUT_CHANGED = 5,
+    OUT_XEPOCHS = 6,  // fused multi-rank solves: cross-rank barrier epochs of the launch
     OUT_N = 8
 };
 
@@ -41,6 +42,7 @@ struct SolveRequest {
     int64_t k0 = 1;          // first sweep index
     bool identity = false;   // RMB_ORDER_IDENTITY
     bool chunked = false;    // RMB_CHUNKED_T: VI* (T in chunks of b against the sweep-start values)
+    bool fused = false;      // RMB_FUSED: multi-rank solve with the in-kernel peer-memory exchange
     double eps = -1.0;       // < 0: no convergence test
     int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
     int msweeps = 1;         // MPI evaluation sweeps per outer iteration
@@ -109,6 +111,13 @@ struct Problem {
     bool sparse_full_grid = false;  // RMB_SPARSE_FULL_GRID
     bool shard_no_graph = false;    // RMB_SHARD_NO_GRAPH
     int64_t last_graph_launches = 0;
+    // fused multi-rank solves (K8f): exchange buffer (xval | xarg | xbar | ximp |
+    // xlist | xcnt, sized for b <= n), its peers' mappings, epochs done so far
+    DevBuf xbuf;
+    void* xpeer[8] = {nullptr};    // per rank: the mapped exchange buffer (own: xbuf.p)
+    bool xpeer_open[8] = {false};  // opened through CUDA IPC (closed at destroy)
+    int xpeer_G = 0;
+    int64_t xepochs = 0;
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
     bool vglobal = false; // dense: RMB_DENSE_VGLOBAL (V and pi in global memory)
     cudaStream_t stream = nullptr;
@@ -125,10 +134,19 @@ struct Problem {
 // dense.cu
 rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                        long long* chg_dev, int64_t chg_len, SolveResult* res);
+// fused multi-rank dense solve (K8f): G logical ranks in one launch on one
+// device (nccl == false) or this process's rank of an NCCL group (peer memory
+// through CUDA IPC)
+rmb_status dense_fused_solve(Problem** ranks, int G, bool nccl, const SolveRequest& rq, double* trace_host,
+                             int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res);
 rmb_status dense_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t* olist, const int* ocount,
                             double* send_val, uint32_t* send_idx, int32_t* send_arg, cudaStream_t st,
                             long long** out_dev);
-// shard.cu: multi-GPU (NCCL) and logical-group (one GPU) sharded solves
+// shard.cu: multi-GPU (NCCL) and logical-group (one GPU) sharded solves;
+// fused_peers maps every rank's exchange buffer (CUDA IPC handles all-gathered
+// over the handle's NCCL communicator) into this process: pr.xpeer[0..G)
+rmb_status fused_peers(Problem& pr, int* G, int* rank);
+rmb_status fused_buffer(Problem& pr);  // dense.cu: allocate + zero the exchange buffer (once)
 rmb_status sharded_solve(Problem** ranks, int G, bool nccl, const SolveRequest& rq, double* trace_host,
                          int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res);
 // sparse.cu

@@ -223,6 +223,13 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
                          int64_t trace_len, int64_t* chg_host, int64_t chg_len, SolveResult* res)
 {
     Problem& p0 = *ranks[0];
+    if (rq0.fused) {
+        if (!p0.dense) {
+            set_error("RMB_FUSED: dense shard handles only (sparse shards use the per-batch all-gather)");
+            return RMB_ERR_UNSUPPORTED;
+        }
+        return dense_fused_solve(ranks, G_local, use_nccl, rq0, trace_host, trace_len, chg_host, chg_len, res);
+    }
     const int64_t n = p0.n;
     cudaStream_t st = p0.stream;
     int G = G_local;
@@ -601,6 +608,75 @@ rmb_status sharded_solve(Problem** ranks, int G_local, bool use_nccl, const Solv
         ranks[r]->last_launches = launches;
         ranks[r]->last_graph_launches = graph_launches;
     }
+    return RMB_OK;
+}
+
+// Map every rank's fused-exchange buffer into this process:
+// CUDA IPC handles all-gathered over the handle's NCCL communicator, opened
+// once and kept for the handle's lifetime (NVLink / NVSwitch peer memory).
+rmb_status fused_peers(Problem& pr, int* G, int* rank)
+{
+    if (!nccl().ok) {
+        set_error("NCCL unavailable: " + nccl().why);
+        return RMB_ERR_NCCL;
+    }
+    ncclComm_t comm = static_cast<ncclComm_t>(pr.nccl_comm);
+    ncclResult_t r = nccl().CommCount(comm, G);
+    if (r == ncclSuccess) r = nccl().CommUserRank(comm, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "fused peers");
+    if (*G > 8) {
+        set_error("fused solve: at most 8 ranks");
+        return RMB_ERR_UNSUPPORTED;
+    }
+    if (pr.xpeer_G == *G) return RMB_OK;
+    rmb_status s = fused_buffer(pr);
+    if (s != RMB_OK) return s;
+    cudaIpcMemHandle_t mine;
+    cudaError_t e = cudaIpcGetMemHandle(&mine, pr.xbuf.p);
+    if (e != cudaSuccess) {
+        set_error(std::string("fused peers: cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+        return RMB_ERR_CUDA;
+    }
+    const size_t H = sizeof(cudaIpcMemHandle_t);
+    DevBuf tmp;
+    if (tmp.ensure(H * (size_t)(*G + 1)) != cudaSuccess) {
+        set_error("fused peers: allocation failed");
+        return RMB_ERR_OOM;
+    }
+    char* d = static_cast<char*>(tmp.p);
+    std::vector<cudaIpcMemHandle_t> all((size_t)*G);
+    e = cudaMemcpyAsync(d, &mine, H, cudaMemcpyHostToDevice, pr.stream);
+    if (e == cudaSuccess) {
+        r = nccl().AllGather(d, d + H, H, ncclUint8, comm, pr.stream);
+        if (r != ncclSuccess) {
+            tmp.release();
+            return nccl_fail(r, "fused peers: ncclAllGather");
+        }
+        e = cudaMemcpyAsync(all.data(), d + H, H * (size_t)*G, cudaMemcpyDeviceToHost, pr.stream);
+    }
+    if (e != cudaSuccess) {
+        tmp.release();
+        set_error(std::string("fused peers: ") + cudaGetErrorString(e));
+        return RMB_ERR_CUDA;
+    }
+    s = wait_stream(pr.stream, comm, "fused peers");
+    tmp.release();
+    if (s != RMB_OK) return s;
+    for (int q = 0; q < *G; ++q) {
+        if (q == *rank) {
+            pr.xpeer[q] = pr.xbuf.p;
+            continue;
+        }
+        void* p = nullptr;
+        e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            set_error(std::string("fused peers: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+            return RMB_ERR_CUDA;
+        }
+        pr.xpeer[q] = p;
+        pr.xpeer_open[q] = true;
+    }
+    pr.xpeer_G = *G;
     return RMB_OK;
 }
 

@@ -234,3 +234,91 @@ def test_group_rejects_out_of_range_given_policy():
     with pytest.raises(rmb.RmbError) as e:
         rmb.mpi_group(shards(P, c, gamma, 2), 10, 2, pi=tdev(pi), pi_given=True)
     assert e.value.status == rmb.INVALID_ARG
+
+
+# --------------------------------------------- fused exchange (K8f, RMB_FUSED)
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("b", [1, 37, 300])
+def test_fused_group_vi_is_bitwise_single_gpu(G, b):
+    """The fused multi-rank kernel (G logical ranks in one launch: each rank
+    backs up its states of a batch, stores the results into every rank's
+    exchange arrays, in-kernel cross-rank barrier) = the single-GPU solve bit
+    for bit, and the oracle within the solve bar."""
+    n, A, gamma = 300, 8, 0.95
+    P, c = gen.dense(n, A, 3, dtype=np.float32)
+    ref = rmb.Problem.dense(tdev(P), tdev(c), gamma).vi(b, seed=2, eps=1e-8, max_sweeps=40)
+    sol = rmb.vi_group(shards(P, c, gamma, G), b, seed=2, eps=1e-8, max_sweeps=40, fused=True)
+    assert sol.stats.sweeps == ref.stats.sweeps and sol.status == ref.status
+    assert np.array_equal(sol.trace, ref.trace)
+    assert np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+    assert np.array_equal(sol.pi.cpu().numpy(), ref.pi.cpu().numpy())
+    orc = oracle.vi(oracle.MDP(n, A, gamma, c, P=P), b, seed=2, eps=1e-8, max_sweeps=40)
+    assert np.abs(sol.V.cpu().numpy() - orc.V).max() <= 1e-9 * max(1, np.abs(orc.V).max())
+
+
+@pytest.mark.parametrize("G", [2, 5, 8])
+@pytest.mark.parametrize("vglobal", [False, True])
+def test_fused_group_mpi_is_bitwise_single_gpu(G, vglobal):
+    """MB-MPI through the fused path (improvement on owned states, cross-rank
+    reduction of ||TV - V|| and the changed counts), smem-V and global-V modes."""
+    n, A, gamma, b, m = 240, 6, 0.95, 29, 4
+    P, c = gen.dense(n, A, 6, dtype=np.float32)
+    single = rmb.Problem.dense(tdev(P), tdev(c), gamma, vglobal=vglobal).mpi(b, m, seed=4, eps=1e-8)
+    hs = []
+    for g in range(G):
+        r0, r1 = rmb.shard_range(n, G, g)
+        hs.append(rmb.Problem.dense(tdev(P[r0:r1]), tdev(c[r0:r1]), gamma, n=n, row_range=(r0, r1),
+                                    vglobal=vglobal))
+    sol = rmb.mpi_group(hs, b, m, seed=4, eps=1e-8, fused=True)
+    assert sol.status == rmb.OK and sol.stats.outer_iters == single.stats.outer_iters
+    assert np.array_equal(sol.V.cpu().numpy(), single.V.cpu().numpy())
+    assert np.array_equal(sol.pi.cpu().numpy(), single.pi.cpu().numpy())
+    assert np.array_equal(sol.changed, single.changed)
+    assert np.array_equal(sol.trace, single.trace)
+
+
+def test_fused_repeated_solves_on_the_same_handles():
+    """The cross-rank counters are monotonic across launches: consecutive fused
+    solves (VI, MPI, VI) on the same handles agree with fresh single-GPU solves."""
+    n, A, gamma = 200, 4, 0.9
+    P, c = gen.dense(n, A, 9, dtype=np.float32)
+    hs = shards(P, c, gamma, 4)
+    one = rmb.Problem.dense(tdev(P), tdev(c), gamma)
+    for b, mode in ((17, "vi"), (50, "mpi"), (200, "vi"), (3, "mpi")):
+        if mode == "vi":
+            a, r = rmb.vi_group(hs, b, seed=b, eps=1e-7, fused=True), one.vi(b, seed=b, eps=1e-7)
+        else:
+            a, r = rmb.mpi_group(hs, b, 3, seed=b, eps=1e-7, fused=True), one.mpi(b, 3, seed=b, eps=1e-7)
+        assert a.stats.sweeps == r.stats.sweeps
+        assert np.array_equal(a.V.cpu().numpy(), r.V.cpu().numpy())
+
+
+def test_fused_nccl_single_rank_path():
+    """rmb_vi / rmb_mpi with RMB_FUSED on a shard handle with a real (1-rank)
+    NCCL communicator: the per-rank fused kernel, peers mapped through the
+    handle's communicator (here only the rank itself)."""
+    n, A, gamma = 400, 8, 0.95
+    P, c = gen.dense(n, A, 8, dtype=np.float32)
+    comm = rmb.nccl_comm_init(1, 0, rmb.nccl_unique_id())
+    try:
+        (h,) = shards(P, c, gamma, 1, comm=comm)
+        one = rmb.Problem.dense(tdev(P), tdev(c), gamma)
+        sol, ref = h.vi(23, seed=1, eps=1e-9, fused=True), one.vi(23, seed=1, eps=1e-9)
+        assert sol.status == rmb.OK and np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+        assert np.array_equal(sol.trace, ref.trace) and h.last_launch_count() == 1
+        solm, refm = h.mpi(23, 3, seed=1, eps=1e-9, fused=True), one.mpi(23, 3, seed=1, eps=1e-9)
+        assert np.array_equal(solm.V.cpu().numpy(), refm.V.cpu().numpy())
+        assert np.array_equal(solm.pi.cpu().numpy(), refm.pi.cpu().numpy())
+        h.close()
+    finally:
+        rmb.nccl_comm_destroy(comm)
+
+
+def test_fused_config2_shape_group_of_8():
+    """Config-2 shape (|A| = 16, gamma 0.99, fp32) at n = 2048, b = n/8, 8 fused logical ranks."""
+    n, A, gamma = 2048, 16, 0.99
+    P, c = gen.dense(n, A, 1, dtype=np.float32)
+    ref = rmb.Problem.dense(tdev(P), tdev(c), gamma).vi(n // 8, seed=0, eps=1e-6, max_sweeps=30)
+    sol = rmb.vi_group(shards(P, c, gamma, 8), n // 8, seed=0, eps=1e-6, max_sweeps=30, fused=True)
+    assert np.array_equal(sol.V.cpu().numpy(), ref.V.cpu().numpy())
+    assert np.array_equal(sol.trace, ref.trace)
