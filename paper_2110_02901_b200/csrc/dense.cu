@@ -2150,12 +2150,11 @@ rmb_status dense_fused_solve(Problem** ranks, int G, bool nccl, const SolveReque
     }
     const XLayout X(p0.n);
     std::vector<DenseLaunch> Ls((size_t)L);
+    if (!nccl)  // every rank's exchange buffer exists before any rank's arguments point at it
+        for (int r = 0; r < L; ++r)
+            if (rmb_status s = fused_buffer(*ranks[r]); s != RMB_OK) return s;
     for (int r = 0; r < L; ++r) {
         Problem& pr = *ranks[r];
-        if (!nccl) {
-            rmb_status s = fused_buffer(pr);
-            if (s != RMB_OK) return s;
-        }
         SolveRequest rq = rq0;
         rq.V = pr.stage_V;
         rq.pi = pr.stage_pi;

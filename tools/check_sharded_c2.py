@@ -1,6 +1,8 @@
-"""Sharded protocol overhead at 1 rank (real 1-rank NCCL communicator) on
-BASELINE config 2 (dense 10^4 x 16 fp32, b = 1000), next to the persistent
-single-GPU solver: ms per sweep of each."""
+"""Multi-GPU protocol overhead at 1 rank (real 1-rank NCCL communicator) on
+BASELINE config 2 (dense 10^4 x 16 fp32), next to the persistent single-GPU
+solver: ms per sweep of the fused path (RMB_FUSED: in-kernel exchange), the
+host-driven protocol (per-batch NCCL all-gather, graph replay and eager), and
+8 logical fused ranks sharing the one device."""
 import json
 import os
 import sys
@@ -19,23 +21,36 @@ comm = rmb.nccl_comm_init(1, 0, rmb.nccl_unique_id())
 n, A = 10_000, 16
 P, c = rmb.generate_dense(n, A, 1)
 out = {}
+
+
+def per_sweep(f):
+    f(seed=0, max_sweeps=2)
+    s = f(seed=1, max_sweeps=20)
+    return s.stats.seconds / s.stats.sweeps * 1e3, s
+
+
 for b in (1000, 64):
-    she = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm, flags=rmb.SHARD_NO_GRAPH)
-    she.vi(b, seed=0, eps=1e-300, max_sweeps=2)
-    se = she.vi(b, seed=1, eps=1e-300, max_sweeps=20)
-    she.close()
-    sh = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm)
-    sh.vi(b, seed=0, eps=1e-300, max_sweeps=2)
-    s = sh.vi(b, seed=1, eps=1e-300, max_sweeps=20)
+    row = {}
     one = rmb.Problem.dense(P, c, 0.99)
-    one.vi(b, seed=0, eps=1e-300, max_sweeps=2)
-    r = one.vi(b, seed=1, eps=1e-300, max_sweeps=20)
-    out[f"b={b}"] = {"sharded_1rank_ms_per_sweep": s.stats.seconds / s.stats.sweeps * 1e3,
-                     "sharded_1rank_eager_ms_per_sweep": se.stats.seconds / se.stats.sweeps * 1e3,
-                     "persistent_ms_per_sweep": r.stats.seconds / r.stats.sweeps * 1e3,
-                     "sharded_launches": sh.last_launch_count()}
+    row["persistent_ms_per_sweep"], ref = per_sweep(lambda **k: one.vi(b, eps=1e-300, **k))
+    sh = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm)
+    row["fused_1rank_ms_per_sweep"], fs = per_sweep(lambda **k: sh.vi(b, eps=1e-300, fused=True, **k))
+    row["fused_bitwise"] = bool(torch.equal(fs.V, ref.V))
+    row["host_protocol_1rank_graph_ms_per_sweep"], _ = per_sweep(lambda **k: sh.vi(b, eps=1e-300, **k))
     sh.close()
+    she = rmb.Problem.dense(P, c, 0.99, n=n, row_range=(0, n), nccl_comm=comm, flags=rmb.SHARD_NO_GRAPH)
+    row["host_protocol_1rank_eager_ms_per_sweep"], _ = per_sweep(lambda **k: she.vi(b, eps=1e-300, **k))
+    she.close()
+    hs = [rmb.Problem.dense(P[r0:r1], c[r0:r1], 0.99, n=n, row_range=(r0, r1))
+          for r0, r1 in (rmb.shard_range(n, 8, g) for g in range(8))]
+    row["fused_8_logical_ranks_one_gpu_ms_per_sweep"], g8 = per_sweep(
+        lambda **k: rmb.vi_group(hs, b, eps=1e-300, fused=True, **k))
+    row["fused_8_bitwise"] = bool(torch.equal(g8.V, ref.V))
+    row["phases_8_logical"] = hs[0].last_phase_times()
+    for h in hs:
+        h.close()
     one.close()
-print(json.dumps(out))
+    out[f"b={b}"] = row
+    print(json.dumps({f"b={b}": row}), flush=True)
 rmb.nccl_comm_destroy(comm)
 dist.destroy_process_group()
