@@ -268,8 +268,15 @@ def config5_line(rmb, torch, dist, comm, world, rank, dev):
         prob = rmb.Problem.dense(P, c, gamma, n=n, row_range=rows, nccl_comm=comm)
     else:
         prob = rmb.Problem.dense(P, c, gamma)
-    prob.mpi(b, 10, seed=0, eps=1e-6, max_outer=1)
-    sol = prob.mpi(b, 10, seed=1, eps=1e-6, max_outer=1000)
+    fused = world > 1
+    if fused:
+        try:
+            prob.mpi(b, 10, seed=0, eps=1e-6, max_outer=1, fused=True)
+        except rmb.RmbError as e:
+            print(f"bench.py: config 5 fused path unavailable ({e})", file=sys.stderr)
+            fused = False
+    prob.mpi(b, 10, seed=0, eps=1e-6, max_outer=1, fused=fused)
+    sol = prob.mpi(b, 10, seed=1, eps=1e-6, max_outer=1000, fused=fused)
     t = sol.stats.seconds
     if dist:
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
@@ -282,6 +289,7 @@ def config5_line(rmb, torch, dist, comm, world, rank, dev):
     line = {"workload": f"config 5 on {world} GPU(s): dense |S|={n} |A|={A} fp32 ({share / 1e9:.1f} GB of P per GPU), "
                         f"gamma={gamma}, MB-MPI m=10 b=n/8={b} to eps=1e-6",
             "status": int(sol.status), "outer_iterations": st.outer_iters, "eval_sweeps": st.sweeps,
+            "exchange": "fused in-kernel NVLink" if fused else ("none" if world == 1 else "NCCL all-gather per batch"),
             "time_to_eps_ms": t * 1e3, "backups_per_s": (st.sweeps * n + (st.outer_iters + 1) * n * A) / t,
             "per_gpu_GB_per_s": rank_bytes / t / 1e9}
     if world == 1:
@@ -455,7 +463,18 @@ def main():
     pi = torch.zeros(N_STATES, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
 
+    # N > 1: the fused path (RMB_FUSED: exchange inside the persistent kernel
+    # over NVLink peer memory); should it fail on this node, every rank falls
+    # back to the per-batch NCCL all-gather protocol (same results)
+    mode = {"fused": world > 1}
+
     def solve(b, seed=0):
+        if mode["fused"]:
+            try:
+                return prob.vi(b, seed=seed, eps=EPS, max_sweeps=200_000, V=V, pi=pi, v0_zero=True, fused=True)
+            except rmb.RmbError as e:
+                print(f"bench.py: fused path unavailable ({e}); per-batch all-gather instead", file=sys.stderr)
+                mode["fused"] = False
         return prob.vi(b, seed=seed, eps=EPS, max_sweeps=200_000, V=V, pi=pi, v0_zero=True)
 
     def barrier():
@@ -510,7 +529,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": arm_config(args.b, f"shard{world} (rows by state, V replicated, NCCL all-gather per batch)"
+        "config": arm_config(args.b, (f"shard{world} (rows by state, V replicated, " +
+                                      ("fused in-kernel NVLink exchange per batch)" if mode["fused"]
+                                       else "NCCL all-gather per batch)"))
                              if world > 1 else "dp1", {"sweeps_per_solve": sweeps / args.steps}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
