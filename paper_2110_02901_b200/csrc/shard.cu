@@ -629,23 +629,28 @@ rmb_status fused_peers(Problem& pr, int* G, int* rank)
         return RMB_ERR_UNSUPPORTED;
     }
     if (pr.xpeer_G == *G) return RMB_OK;
-    rmb_status s = fused_buffer(pr);
-    if (s != RMB_OK) return s;
+    // Every step below is collective: a rank that fails locally still takes
+    // part in both all-gathers, so all ranks reach the same verdict and either
+    // all launch the fused kernel or none does (no rank left waiting in it).
+    std::string why;
+    int ok = 1;
+    if (fused_buffer(pr) != RMB_OK) ok = 0, why = rmb_last_error();
     cudaIpcMemHandle_t mine;
-    cudaError_t e = cudaIpcGetMemHandle(&mine, pr.xbuf.p);
-    if (e != cudaSuccess) {
-        set_error(std::string("fused peers: cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
-        return RMB_ERR_CUDA;
+    memset(&mine, 0, sizeof mine);
+    if (ok) {
+        cudaError_t e = cudaIpcGetMemHandle(&mine, pr.xbuf.p);
+        if (e != cudaSuccess) ok = 0, why = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
     }
     const size_t H = sizeof(cudaIpcMemHandle_t);
     DevBuf tmp;
-    if (tmp.ensure(H * (size_t)(*G + 1)) != cudaSuccess) {
+    if (tmp.ensure(H * (size_t)(*G + 1) + 8 * (size_t)(*G + 1)) != cudaSuccess) {
         set_error("fused peers: allocation failed");
         return RMB_ERR_OOM;
     }
     char* d = static_cast<char*>(tmp.p);
+    int* flags = reinterpret_cast<int*>(d + H * (size_t)(*G + 1));
     std::vector<cudaIpcMemHandle_t> all((size_t)*G);
-    e = cudaMemcpyAsync(d, &mine, H, cudaMemcpyHostToDevice, pr.stream);
+    cudaError_t e = cudaMemcpyAsync(d, &mine, H, cudaMemcpyHostToDevice, pr.stream);
     if (e == cudaSuccess) {
         r = nccl().AllGather(d, d + H, H, ncclUint8, comm, pr.stream);
         if (r != ncclSuccess) {
@@ -654,27 +659,54 @@ rmb_status fused_peers(Problem& pr, int* G, int* rank)
         }
         e = cudaMemcpyAsync(all.data(), d + H, H * (size_t)*G, cudaMemcpyDeviceToHost, pr.stream);
     }
-    if (e != cudaSuccess) {
-        tmp.release();
-        set_error(std::string("fused peers: ") + cudaGetErrorString(e));
-        return RMB_ERR_CUDA;
+    if (e == cudaSuccess) {
+        rmb_status s = wait_stream(pr.stream, comm, "fused peers");
+        if (s != RMB_OK) {
+            tmp.release();
+            return s;
+        }
     }
-    s = wait_stream(pr.stream, comm, "fused peers");
+    void* opened[8] = {nullptr};
+    for (int q = 0; q < *G && ok && e == cudaSuccess; ++q) {
+        if (q == *rank) continue;
+        cudaError_t eo = cudaIpcOpenMemHandle(&opened[q], all[q], cudaIpcMemLazyEnablePeerAccess);
+        if (eo != cudaSuccess) {
+            ok = 0;
+            why = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(eo);
+            opened[q] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    // the verdict: every rank's ok flag
+    std::vector<int> oks((size_t)*G, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flags, &ok, 4, cudaMemcpyHostToDevice, pr.stream);
+    if (e == cudaSuccess) {
+        r = nccl().AllGather(flags, flags + 1, 4, ncclUint8, comm, pr.stream);
+        if (r != ncclSuccess) {
+            tmp.release();
+            return nccl_fail(r, "fused peers: ncclAllGather(verdict)");
+        }
+        e = cudaMemcpyAsync(oks.data(), flags + 1, 4 * (size_t)*G, cudaMemcpyDeviceToHost, pr.stream);
+    }
+    if (e == cudaSuccess) {
+        rmb_status s = wait_stream(pr.stream, comm, "fused peers");
+        if (s != RMB_OK) {
+            tmp.release();
+            return s;
+        }
+    }
     tmp.release();
-    if (s != RMB_OK) return s;
+    bool all_ok = e == cudaSuccess;
+    for (int q = 0; q < *G; ++q) all_ok = all_ok && oks[q] == 1;
+    if (!all_ok) {
+        for (int q = 0; q < *G; ++q)
+            if (opened[q]) cudaIpcCloseMemHandle(opened[q]);
+        set_error("fused solve: peer memory unavailable on some rank" + (why.empty() ? std::string() : " (" + why + ")"));
+        return RMB_ERR_UNSUPPORTED;
+    }
     for (int q = 0; q < *G; ++q) {
-        if (q == *rank) {
-            pr.xpeer[q] = pr.xbuf.p;
-            continue;
-        }
-        void* p = nullptr;
-        e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) {
-            set_error(std::string("fused peers: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
-            return RMB_ERR_CUDA;
-        }
-        pr.xpeer[q] = p;
-        pr.xpeer_open[q] = true;
+        pr.xpeer[q] = q == *rank ? pr.xbuf.p : opened[q];
+        pr.xpeer_open[q] = q != *rank;
     }
     pr.xpeer_G = *G;
     return RMB_OK;

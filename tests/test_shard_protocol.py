@@ -130,3 +130,92 @@ def test_shard_ranges_partition_the_states():
             for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
                 assert e0 == b1 and b0 <= e0
             assert max(e - b for b, e in spans) == -(-n // G)
+
+
+# ------------------------------------------------- fused exchange (K8f) model
+def fused_mpi(rank, world, b, msweeps, outer_iters):
+    """The fused multi-rank protocol of the dense kernel (RMB_FUSED) step by
+    step on CPU: per batch each rank builds the list of its states (order-free:
+    shuffled on purpose), backs them up against its replica, stores (value,
+    argmin) at their batch POSITIONS into every rank's exchange arrays (here: a
+    position-indexed array all-gathered, each position written by its owner
+    only), meets the others (the collective), then patches ALL of the batch from
+    its own arrays.  Improvements run on the owned states only, and (residual,
+    changed) records are exchanged and reduced.  MB-MPI from V0 = 0, pi_0 =
+    greedy(V0)."""
+    r0, r1 = rmb.shard_range(N, world, rank)
+    P, c = gen.dense(N, A, 11, dtype=np.float64)
+    m = oracle.MDP(N, A, GAMMA, c, P=P)
+    rng = np.random.default_rng(rank)
+    V = np.zeros(N)
+    pi = np.zeros(N, np.int32)
+
+    def improve_owned():
+        rT, ch = 0.0, 0
+        for s in range(r0, r1):
+            q, a = oracle.backup_dense_row(P[s], c[s], GAMMA, V)
+            rT = max(rT, abs(q - V[s]))
+            ch += int(a != pi[s])
+            pi[s] = a
+        rec = torch.tensor([rT, float(ch)], dtype=torch.float64)
+        recs = [torch.zeros_like(rec) for _ in range(world)]
+        dist.all_gather(recs, rec)
+        return max(float(x[0]) for x in recs), int(sum(float(x[1]) for x in recs))
+
+    improve_owned()  # pi_0 = greedy(V0)
+    k, trace, changed = 1, [], []
+    for o in range(outer_iters):
+        for e in range(msweeps):
+            perm = rmb.partition(N, SEED, k)
+            k += 1
+            r = 0.0
+            for lo in range(0, N, b):
+                cnt = min(b, N - lo)
+                own = [(i, int(perm[lo + i])) for i in range(cnt) if r0 <= perm[lo + i] < r1]
+                rng.shuffle(own)  # list order is irrelevant to every state's arithmetic
+                xval = torch.zeros(cnt, dtype=torch.float64)
+                for i, s in own:
+                    xval[i], _ = oracle.backup_dense_row(P[s], c[s], GAMMA, V, pi_a=int(pi[s]))
+                parts = [torch.zeros_like(xval) for _ in range(world)]
+                dist.all_gather(parts, xval)  # each rank's stores land in every rank's arrays
+                mine = parts[0].clone()
+                for g in range(1, world):
+                    mine += parts[g]  # positions are disjoint across ranks: exact
+                for i in range(cnt):
+                    s = int(perm[lo + i])
+                    r = max(r, abs(float(mine[i]) - V[s]))
+                    V[s] = float(mine[i])
+            trace.append(r)
+        rT, ch = improve_owned()
+        trace.append(rT)
+        changed.append(ch)
+    return V, pi[r0:r1], np.array(trace), np.array(changed), (r0, r1)
+
+
+def _fused_worker(rank, world, port, b, msweeps, outer, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        V, pil, tr, ch, (r0, r1) = fused_mpi(rank, world, b, msweeps, outer)
+        out[rank] = (V, pil, tr, ch, r0, r1)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("b", [1, 7, N])
+def test_two_rank_gloo_fused_protocol_mpi_equals_oracle(b):
+    world, msweeps, outer = 2, 3, 4
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_fused_worker, args=(world, _free_port(), b, msweeps, outer, out), nprocs=world, join=True)
+        res = dict(out)
+    P, c = gen.dense(N, A, 11, dtype=np.float64)
+    ref = oracle.mpi(oracle.MDP(N, A, GAMMA, c, P=P), b, msweeps, seed=SEED, eps=1e-300, max_outer=outer)
+    pi = np.zeros(N, np.int32)
+    for rank in range(world):
+        V, pil, tr, ch, r0, r1 = res[rank]
+        assert np.array_equal(V, ref.V) and np.array_equal(tr, ref.trace)
+        assert np.array_equal(ch, ref.changed)
+        pi[r0:r1] = pil
+    assert np.array_equal(pi, ref.pi)
