@@ -86,6 +86,9 @@ typedef struct {
                                    read the sweep-start V, the new values land at the end of the sweep.
                                    One barrier per chunk, like B_b; the result is T V for any b, order
                                    and chunking (DESIGN reading R21).  Not for sharded handles.        */
+#define RMB_DENSE_NO_CLUSTER 0x1000u /* rmb_create_dense: never use the one-cluster solver for tiny batches
+                                      (<= 2 MB of P and <= 256 rows per batch: 16 CTAs, DSMEM combine,
+                                      hardware cluster barrier); results agree to fp64 rounding        */
 /* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly

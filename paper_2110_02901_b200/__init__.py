@@ -28,7 +28,7 @@ OK, INVALID_ARG, INVALID_MDP, NOT_CONVERGED, NONFINITE, CUDA_ERR, NCCL_ERR, OOM,
 F32, F64 = 0, 1
 ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 CHUNKED_T = 0x40
-SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED = 0x80, 0x400, 0x800
+SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED, DENSE_NO_CLUSTER = 0x80, 0x400, 0x800, 0x1000
 
 _lib = None
 

@@ -275,6 +275,7 @@ rmb_status rmb_create_dense(const rmb_desc* desc, const void* P, const void* c, 
     pr->dense = true;
     pr->no_tma = (flags & RMB_DENSE_NO_TMA) != 0;
     pr->vglobal = (flags & RMB_DENSE_VGLOBAL) != 0;
+    pr->no_cluster = (flags & RMB_DENSE_NO_CLUSTER) != 0;
     apply_create_flags(*pr, flags);
     if (s == RMB_OK && (flags & RMB_VALIDATE)) s = validate_mdp(*pr);
     if (s != RMB_OK) {

@@ -1,0 +1,487 @@
+// cluster.cu — dense MB-VI / B_{pi,b} sweeps for TINY batches on one
+// thread-block cluster (sm_100a: up to 16 CTAs, distributed shared memory,
+// hardware cluster barrier).
+//
+// Small b is latency-bound by construction (SURVEY 7 hard part #1): b = 1 is
+// the Gauss-Seidel operator F, 10^4 batches per sweep on
+// config 2, each only b*|A|*n*4 bytes of P (640 KB at b = 1).  On the 148-CTA
+// grid a batch costs a grid barrier (~2 us through L2 atomics) plus a combine
+// that reads every CTA's partial sums back from L2 -- ~5 us against 0.1 us of
+// HBM time.  Here one cluster of CS CTAs does the whole solve:
+//   * CTA q owns the column slab [q*slab, (q+1)*slab) of every row; a batch's
+//     rows (state s, action a) are streamed slab by slab with cp.async.bulk
+//     into a shared-memory ring, up to RING stages ahead (P does not depend on
+//     V: the loads of the next batches are in flight across the barrier);
+//   * each warp dots its rows' slab with the shared-memory copy of V (fp64),
+//     the row partials stay in the CTA's shared memory;
+//   * one hardware cluster barrier per batch (barrier.cluster release/acquire);
+//   * every CTA then reads all CS partials of every row through DSMEM
+//     (ld.shared::cluster), adds them in CTA order (fixed: reproducible), takes
+//     min / argmin (lowest action on exact ties) and patches its own V copy --
+//     Eq. 12: V changes only after the barrier that ends every read of the batch.
+// The per-state arithmetic is fixed by (n, CS): bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <type_traits>
+
+#include "common.cuh"
+#include "internal.h"
+#include "partition.cuh"
+
+namespace rmb {
+
+constexpr int kCThreads = 256;  // 8 warps per CTA, every one a compute warp
+constexpr int kCWarps = kCThreads / kWarp;
+constexpr int kCRowsMax = 16;   // rows per ring stage
+constexpr int kCBatchRows = 256;  // rows (states x actions) per batch this path serves
+
+struct ClusterArgs {
+    const void* P;
+    const void* c;
+    int n, A;
+    double gamma;
+    double* V;
+    int32_t* pi;
+    int b;
+    uint64_t seed;
+    int64_t k0;
+    int identity;
+    int eval;       // 1: B_{pi,b} sweeps (row pi(s)), 0: B_b
+    double eps;     // < 0: no stopping test (single application)
+    int64_t max_iter;
+    uint32_t* perm; // 3 * n
+    double* trace;
+    int64_t trace_len;
+    long long* out;
+    long long* prof;
+    int slab;       // columns per CTA (multiple of 16 bytes)
+    int row_bytes;  // bytes per row slot of a stage
+    int rows;       // rows per stage
+    int ring;       // stages
+    int64_t v_off, pi_off, ring_off, part_off, bar_off;  // dynamic smem layout (bytes)
+};
+
+__device__ __forceinline__ unsigned cluster_rank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// generic address of the same shared-memory variable in CTA `rank` of the cluster
+__device__ __forceinline__ const double* dsmem(const double* p, unsigned rank)
+{
+    uint64_t r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+    return reinterpret_cast<const double*>(r);
+}
+
+// One row job of the solve: the rows [r0, r0 + nr) of batch `bt` (rows are
+// (position, action) pairs, position-major).
+struct CJob {
+    int64_t k;   // sweep
+    int lo, cnt; // batch positions
+    int r0, nr;  // rows of the batch in this stage
+};
+
+template <typename PT>
+__global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const ClusterArgs a)
+{
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* Vs = reinterpret_cast<double*>(sm + a.v_off);
+    int32_t* pis = reinterpret_cast<int32_t*>(sm + a.pi_off);
+    unsigned char* ring = sm + a.ring_off;
+    double* part = reinterpret_cast<double*>(sm + a.part_off);  // [2][kCBatchRows]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + a.bar_off);
+    const unsigned q = cluster_rank();
+    const unsigned CS = gridDim.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = a.n;
+    const int Ae = a.eval ? 1 : a.A;
+    const int c0 = (int)q * a.slab, c1 = min(n, c0 + a.slab);
+    constexpr int E = 16 / (int)sizeof(PT);
+    using VT = typename std::conditional<sizeof(PT) == 4, float4, double2>::type;
+
+    for (int j = t; j < n; j += kCThreads) {
+        Vs[j] = a.V[j];
+        if (a.eval) pis[j] = a.pi[j];
+    }
+    if (t == 0)
+        for (int s = 0; s < a.ring; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the first sweep's order: every CTA draws its share of the positions
+    if (!a.identity) {
+        Permutation pm;
+        pm.init(n, a.seed, a.k0);
+        uint32_t* dst = a.perm + (a.k0 % 3) * n;
+        for (int p = (int)q * kCThreads + t; p < n; p += (int)CS * kCThreads) dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+    cluster_sync();
+
+    // ---- the row-job stream (identical on every CTA; each loads its own slab)
+    const int nbatch = (n + a.b - 1) / a.b;
+    auto job_at = [&](int64_t sweep, int bi, int st, CJob& J) {
+        J.k = sweep;
+        J.lo = bi * a.b;
+        J.cnt = min(a.b, n - J.lo);
+        J.r0 = st * a.rows;
+        J.nr = min(a.rows, J.cnt * Ae - J.r0);
+    };
+    // producer state (thread 0): the next job to issue
+    int64_t pk = a.k0;
+    int pb = 0, ps = 0;
+    int64_t issued = 0;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const PT* P = static_cast<const PT*>(a.P);
+    const int64_t last_sweep = a.k0 + a.max_iter - 1;
+    auto issue_one = [&]() {  // thread 0: the next job into ring slot issued % ring
+        if (pk > last_sweep) return;
+        CJob J;
+        job_at(pk, pb, ps, J);
+        const int slot = (int)(issued % a.ring);
+        unsigned char* dst = ring + (size_t)slot * a.rows * a.row_bytes;
+        const uint32_t* pm = a.identity ? nullptr : a.perm + (J.k % 3) * n;
+        const unsigned bytes = (unsigned)((c1 - c0) * (int)sizeof(PT));
+        mbar_arrive_tx(full + slot, bytes * (unsigned)J.nr);
+        for (int r = 0; r < J.nr; ++r) {
+            const int row = J.r0 + r;
+            const int i = row / Ae;
+            const int s = pm ? (int)__ldcg(pm + J.lo + i) : J.lo + i;
+            const int act = a.eval ? __ldcg(a.pi + s) : row - i * Ae;
+            bulk_g2s(dst + (size_t)r * a.row_bytes, P + ((int64_t)s * a.A + act) * n + c0, bytes, full + slot, pol);
+        }
+        ++issued;
+        if (++ps * a.rows >= J.cnt * Ae) {  // next batch
+            ps = 0;
+            if (++pb == nbatch) pb = 0, ++pk;
+        }
+    };
+    // a job may be issued only once the perm of its sweep is visible: the next
+    // sweep's order is drawn in batch 0 of the current one (so >= 2 batches per
+    // sweep lets the stream run across sweeps; this path serves tiny batches)
+    int64_t ck = a.k0;  // consumer position
+    auto may_issue = [&](int64_t cons_k, int cons_b) {
+        return pk == cons_k || (pk == cons_k + 1 && cons_b >= 1);
+    };
+    if (t == 0)
+        for (int s = 0; s < a.ring && may_issue(ck, 0); ++s) issue_one();
+
+    int64_t consumed = 0;
+    long long status = RMB_ERR_NOT_CONVERGED;
+    int64_t it = 0, batches = 0;
+    double last = 0.0;
+    double rmax = 0.0;
+    int bad = 0;
+    while (it < a.max_iter) {
+        const int64_t k = ck;
+        const uint32_t* pm = a.identity ? nullptr : a.perm + (k % 3) * n;
+        rmax = 0.0;
+        bad = 0;
+        for (int bi = 0; bi < nbatch; ++bi) {
+            const int lo = bi * a.b, cnt = min(a.b, n - lo);
+            const int nrows = cnt * Ae;
+            double* pr = part + (size_t)(batches & 1) * kCBatchRows;
+            for (int st = 0; st * a.rows < nrows; ++st) {
+                const int slot = (int)(consumed % a.ring);
+                const unsigned ph = (unsigned)((consumed / a.ring) & 1);
+                CJob J;
+                job_at(k, bi, st, J);
+                {
+                    SpinGuard sg;
+                    while (!mbar_try(full + slot, ph)) sg.tick();
+                }
+                const unsigned char* stg = ring + (size_t)slot * a.rows * a.row_bytes;
+                const int nv = (c1 - c0) / E;  // 16-byte vectors of the slab (slab and n are multiples of E)
+                for (int r = warp; r < J.nr; r += kCWarps) {
+                    const VT* row = reinterpret_cast<const VT*>(stg + (size_t)r * a.row_bytes);
+                    double acc = 0.0;
+                    for (int v = lane; v < nv; v += kWarp) {
+                        const VT x = row[v];
+                        const int j = c0 + v * E;
+                        if constexpr (sizeof(PT) == 4) {
+                            acc = fma((double)x.x, Vs[j], acc);
+                            acc = fma((double)x.y, Vs[j + 1], acc);
+                            acc = fma((double)x.z, Vs[j + 2], acc);
+                            acc = fma((double)x.w, Vs[j + 3], acc);
+                        } else {
+                            acc = fma(x.x, Vs[j], acc);
+                            acc = fma(x.y, Vs[j + 1], acc);
+                        }
+                    }
+                    acc = warp_sum(acc);
+                    if (lane == 0) pr[J.r0 + r] = acc;
+                }
+                __syncthreads();  // every warp is done with the slot
+                ++consumed;
+                if (t == 0) {
+                    ck = k;
+                    while (issued < consumed + a.ring && may_issue(k, bi)) issue_one();
+                }
+            }
+            // next sweep's order, off the critical path (batch 0)
+            if (bi == 0 && !a.identity) {
+                Permutation pm2;
+                pm2.init(n, a.seed, k + 1);
+                uint32_t* dst = a.perm + ((k + 1) % 3) * n;
+                for (int p = (int)q * kCThreads + t; p < n; p += (int)CS * kCThreads)
+                    dst[p] = (uint32_t)pm2((uint64_t)p);
+            }
+            cluster_sync();  // the batch's partials of every CTA are complete (and its reads of V done)
+            // combine: L = pow2 >= Ae lanes per state; lane g takes action g;
+            // partials of the CS CTAs added in CTA order
+            int L = 1;
+            while (L < Ae) L <<= 1;
+            for (int base = 0; base < cnt * L; base += kCThreads) {
+                const int id = base + t;
+                const int i = id / L, g = id - i * L;
+                const bool valid = i < cnt && g < Ae;
+                double Q = INFINITY;
+                int arg = 0x7fffffff;
+                int s = 0;
+                if (i < cnt) s = pm ? (int)__ldcg(pm + lo + i) : lo + i;
+                if (valid) {
+                    double sum = 0.0;
+                    for (unsigned cq = 0; cq < CS; ++cq) sum += *dsmem(pr + i * Ae + g, cq);
+                    const int act = a.eval ? pis[s] : g;
+                    Q = (double)__ldg(static_cast<const PT*>(a.c) + (int64_t)s * a.A + act) + a.gamma * sum;
+                    arg = act;
+                }
+                // argmin over the L lanes of the state (lower value, then lower action)
+                for (int o = 1; o < L; o <<= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, Q, o);
+                    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                    if (ov < Q || (ov == Q && oa < arg)) Q = ov, arg = oa;
+                }
+                if (valid && g == 0) {
+                    rmax = fmax(rmax, fabs(Q - Vs[s]));
+                    bad |= !isfinite(Q);
+                    Vs[s] = Q;
+                    if (q == 0) {
+                        a.V[s] = Q;
+                        if (!a.eval && a.pi) a.pi[s] = arg;
+                    }
+                }
+            }
+            __syncthreads();  // the patched V is visible to the CTA's next batch
+            ++batches;
+        }
+        // sweep residual: every CTA patched every state, so the CTA-local max
+        // is the sweep's; reduce it over the CTA
+        __shared__ double red[kCWarps];
+        __shared__ int redb[kCWarps];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if (lane == 0) red[warp] = rmax, redb[warp] = bad;
+        __syncthreads();
+        double r = 0.0;
+        int bb = 0;
+        for (int w = 0; w < kCWarps; ++w) r = fmax(r, red[w]), bb |= redb[w];
+        __syncthreads();
+        if (q == 0 && t == 0 && it < a.trace_len) a.trace[it] = r;
+        ++it;
+        ++ck;
+        last = r;
+        if (bb) { status = RMB_ERR_NONFINITE; break; }
+        if (a.eps >= 0.0 && r <= a.eps) { status = RMB_OK; break; }
+        if (t == 0)  // the next sweep's first batch may now stream (its order is visible)
+            while (issued < consumed + a.ring && may_issue(ck, 0)) issue_one();
+    }
+    if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+    // drain: bulk copies in flight must land before the CTA exits
+    if (t == 0) {
+        for (int64_t d = consumed; d < issued; ++d) {
+            const int slot = (int)(d % a.ring);
+            const unsigned ph = (unsigned)((d / a.ring) & 1);
+            SpinGuard sg;
+            while (!mbar_try(full + slot, ph)) sg.tick();
+        }
+    }
+    cluster_sync();  // no CTA exits while another may still read its shared memory
+    if (q == 0 && t == 0) {
+        a.out[OUT_SWEEPS] = it;
+        a.out[OUT_OUTER] = 0;
+        a.out[OUT_STATUS] = status;
+        a.out[OUT_RESID_BITS] = __double_as_longlong(last);
+        a.out[OUT_BATCHES] = batches;
+        a.out[OUT_CHANGED] = 0;
+        a.prof[0] = a.prof[1] = a.prof[2] = 0;
+        a.prof[3] = batches;
+    }
+}
+
+// The cluster path serves dense B_b / B_{pi,b} solves whose batches hold at
+// most kCBatchRows rows and kClusterBatchBytes of P; returns false when the
+// request is outside that envelope (the grid solver takes it).
+constexpr int64_t kClusterBatchBytes = int64_t(2) << 20;
+
+bool dense_cluster_eligible(const Problem& pr, const SolveRequest& rq)
+{
+    if (!pr.dense || pr.no_tma || pr.vglobal || rq.chunked || rq.fused) return false;
+    if (pr.row_begin != 0 || pr.row_end != pr.n || pr.nccl_comm) return false;
+    const bool eval = rq.mode == MODE_APPLY_PI || rq.mode == MODE_POLICY_VALUE;
+    if (!(rq.mode == MODE_VI || rq.mode == MODE_APPLY || eval)) return false;
+    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
+    const int64_t n = pr.n;
+    if (n % (16 / psz) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) return false;
+    const int Ae = eval ? 1 : pr.A;
+    if (rq.b >= n || rq.b * Ae > kCBatchRows) return false;
+    if (rq.b * Ae * n * psz > kClusterBatchBytes) return false;
+    return true;
+}
+
+template <typename PT>
+static cudaError_t launch_cluster(const ClusterArgs& a, int CS, size_t smem, cudaStream_t st)
+{
+    auto kern = dense_cluster_kernel<PT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(kCThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// largest cluster (16, else 8, ...) that can be scheduled with this shared memory
+template <typename PT>
+static int cluster_size(size_t smem)
+{
+    auto kern = dense_cluster_kernel<PT>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cs = 16; cs >= 2; cs >>= 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kCThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc >= 1) return cs;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
+rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                               SolveResult* res)
+{
+    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
+    const int n = (int)pr.n;
+    const bool eval = rq.mode == MODE_APPLY_PI || rq.mode == MODE_POLICY_VALUE;
+    ClusterArgs a{};
+    a.P = pr.P;
+    a.c = pr.c;
+    a.n = n;
+    a.A = pr.A;
+    a.gamma = pr.gamma;
+    a.V = rq.V;
+    a.pi = rq.pi;
+    a.b = (int)rq.b;
+    a.seed = rq.seed;
+    a.k0 = rq.k0;
+    a.identity = rq.identity ? 1 : 0;
+    a.eval = eval ? 1 : 0;
+    a.eps = rq.eps;
+    a.max_iter = rq.max_iter;
+    a.trace = trace_dev;
+    a.trace_len = trace_len;
+    const int E = 16 / psz;
+    auto layout = [&](int CS, size_t& smem) {
+        a.slab = ((n + CS - 1) / CS + E - 1) / E * E;
+        a.row_bytes = (a.slab * psz + 127) / 128 * 128;
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            const size_t o = off;
+            off = (off + bytes + 127) / 128 * 128;
+            return (int64_t)o;
+        };
+        a.v_off = take((size_t)n * 8);
+        a.pi_off = take(eval ? (size_t)n * 4 : 16);
+        a.part_off = take((size_t)2 * kCBatchRows * 8);
+        a.bar_off = take(8 * 8);
+        const int64_t room = (int64_t)pr.smem_optin - (int64_t)off - 1024;
+        const int Ae = eval ? 1 : pr.A;
+        a.rows = (int)std::min<int64_t>(kCRowsMax, std::min<int64_t>(rq.b * Ae, room / (2 * a.row_bytes)));
+        a.ring = (int)std::min<int64_t>(8, room / std::max<int64_t>(1, (int64_t)a.rows * a.row_bytes));
+        a.ring_off = take((size_t)std::max(0, a.ring) * std::max(0, a.rows) * a.row_bytes);
+        smem = off;
+        return a.rows >= 1 && a.ring >= 2;
+    };
+    size_t smem = 0;
+    int CS = 16;
+    if (!layout(CS, smem)) return RMB_ERR_UNSUPPORTED;
+    CS = pr.pdt == RMB_F32 ? cluster_size<float>(smem) : cluster_size<double>(smem);
+    if (CS < 2) return RMB_ERR_UNSUPPORTED;
+    if (!layout(CS, smem)) return RMB_ERR_UNSUPPORTED;
+    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.ctrl.ensure(4096) != cudaSuccess) {
+        set_error("cluster solver: workspace allocation failed");
+        return RMB_ERR_OOM;
+    }
+    a.perm = static_cast<uint32_t*>(pr.perm.p);
+    unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
+    a.out = reinterpret_cast<long long*>(ctrl + 128);
+    a.prof = reinterpret_cast<long long*>(ctrl + 192);
+    cudaStream_t st = pr.stream;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    if (ce == cudaSuccess)
+        ce = pr.pdt == RMB_F32 ? launch_cluster<float>(a, CS, smem, st) : launch_cluster<double>(a, CS, smem, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
+    long long out[OUT_N + 4] = {0};
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out + OUT_N, a.prof, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) {
+        set_error(std::string("cluster solver: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    res->sweeps = out[OUT_SWEEPS];
+    res->outer = 0;
+    res->status = (int)out[OUT_STATUS];
+    double d;
+    memcpy(&d, &out[OUT_RESID_BITS], 8);
+    res->final_resid = d;
+    res->batches = out[OUT_BATCHES];
+    res->changed = 0;
+    res->ms = ms;
+    res->launches = 1;
+    for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
+    pr.prof[2] = CS;  // the phase slot of the combine reports the cluster size on this path
+    pr.last_launches = 1;
+    return RMB_OK;
+}
+
+}  // namespace rmb

@@ -545,64 +545,6 @@ __device__ __forceinline__ TmaSmem tma_smem(unsigned char* base, const DenseArgs
     return m;
 }
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned tx)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
-{
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_addr(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Hang guard for ring waits (a broken pipeline traps instead of wedging the GPU).
-struct SpinGuard {
-    unsigned spins = 0;
-    unsigned long long t0 = 0;
-    __device__ __forceinline__ void tick()
-    {
-        if (++spins == 8192u) {
-            spins = 0;
-            const unsigned long long t = globaltimer_ns();
-            if (t0 == 0) t0 = t;
-            else if (t - t0 > 20ull * 1000000000ull) __trap();
-        }
-    }
-};
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
-                                         uint64_t pol)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ long long ld_acquire_cta(const long long* p)
-{
-    long long v;
-    asm volatile("ld.acquire.cta.shared.b64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_cta(long long* p, long long v)
-{
-    asm volatile("st.release.cta.shared.b64 [%0], %1;" ::"r"(smem_addr(p)), "l"(v) : "memory");
-}
-
 // The batch sequence of a launch, as the compute threads will run it (one
 // entry per run_batch call), assuming no early stop.  Kinds as run_batch KIND.
 struct TmaBatch {
@@ -2038,6 +1980,11 @@ rmb_status dense_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t*
 rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                        long long* chg_dev, int64_t chg_len, SolveResult* res)
 {
+    // tiny batches (<= 2 MB of P, <= 256 rows): one thread-block cluster
+    if (!pr.no_cluster && dense_cluster_eligible(pr, rq)) {
+        rmb_status s = dense_cluster_solve(pr, rq, trace_dev, trace_len, res);
+        if (s != RMB_ERR_UNSUPPORTED) return s;
+    }
     DenseLaunch L;
     rmb_status s = dense_prepare(pr, rq, trace_dev, trace_len, chg_dev, chg_len, L);
     if (s != RMB_OK) return s;

@@ -120,6 +120,7 @@ struct Problem {
     int64_t xepochs = 0;
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
     bool vglobal = false; // dense: RMB_DENSE_VGLOBAL (V and pi in global memory)
+    bool no_cluster = false;  // dense: RMB_DENSE_NO_CLUSTER (tiny batches on the grid solver too)
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 0;
@@ -134,6 +135,11 @@ struct Problem {
 // dense.cu
 rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                        long long* chg_dev, int64_t chg_len, SolveResult* res);
+// cluster.cu: tiny dense batches on one thread-block cluster (DSMEM combine,
+// hardware cluster barrier); eligible = inside that path's envelope
+bool dense_cluster_eligible(const Problem& pr, const SolveRequest& rq);
+rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                               SolveResult* res);
 // fused multi-rank dense solve (K8f): G logical ranks in one launch on one
 // device (nccl == false) or this process's rank of an NCCL group (peer memory
 // through CUDA IPC)

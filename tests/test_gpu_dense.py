@@ -475,3 +475,52 @@ def test_binding_rejects_wrong_vector_types():
         prob.vi(4, pi=np.zeros(n, np.int64))
     with pytest.raises(TypeError):
         prob.apply(4, 0, 1, np.zeros(n, np.float32))
+
+
+# ---------------------------------------- one-cluster path for tiny batches
+@pytest.mark.parametrize("n,A,b,dtype", [(1000, 16, 1, np.float32), (2000, 4, 3, np.float32),
+                                         (512, 8, 2, np.float64), (10_000, 16, 1, np.float32)])
+def test_cluster_path_matches_grid_path_and_oracle(n, A, b, dtype):
+    """Tiny batches (<= 2 MB of P, <= 256 rows) run on one thread-block cluster
+    (DSMEM combine, hardware cluster barrier).  Its trajectory equals the
+    148-CTA grid solver's (RMB_DENSE_NO_CLUSTER) to fp64 rounding and the
+    oracle's within the solve bar; single applications (B_b and B_{pi,b}) to 1e-11."""
+    P, c = gen.dense(n, A, 17, dtype=dtype)
+    gamma = 0.95
+    clu = rmb.Problem.dense(tdev(P), tdev(c), gamma)
+    grid = rmb.Problem.dense(tdev(P), tdev(c), gamma, flags=rmb.DENSE_NO_CLUSTER)
+    sweeps = 3 if n >= 10_000 else 12
+    a = clu.vi(b, seed=4, eps=1e-300, max_sweeps=sweeps)
+    g = grid.vi(b, seed=4, eps=1e-300, max_sweeps=sweeps)
+    assert clu.last_phase_times()[2] in (2, 4, 8, 16)  # the cluster path ran (reports its size)
+    assert grid.last_phase_times()[2] not in (2, 4, 8, 16) or grid.last_phase_times()[3] > 0
+    assert a.stats.batches == g.stats.batches == sweeps * -(-n // b)
+    assert_close(a.V.cpu().numpy(), g.V.cpu().numpy(), 1e-12)
+    assert_close(a.trace, g.trace, 1e-12)
+    if n <= 2000:
+        m = oracle.MDP(n, A, gamma, c, P=P)
+        ref = oracle.vi(m, b, seed=4, eps=1e-300, max_sweeps=sweeps)
+        assert_close(a.V.cpu().numpy(), ref.V, 1e-10)
+        assert_close(a.trace, ref.trace, 1e-10)
+        mask = qgap(m, ref.V) > 1e-9
+        assert np.array_equal(a.pi.cpu().numpy()[mask], ref.pi[mask])
+        V0 = np.random.default_rng(1).random(n) * 10
+        pi = np.random.default_rng(2).integers(0, A, n).astype(np.int32)
+        for pol in (None, pi):
+            V1, arg, r = clu.apply(b, 9, 2, tdev(V0), pi=None if pol is None else tdev(pol))
+            Vo, ao, ro = oracle.sweep(m, V0, b, oracle.partition(n, 9, 2), pol)
+            assert_close(V1.cpu().numpy(), Vo, 1e-11)
+            assert abs(r - ro) <= 1e-11 * 10
+
+
+def test_cluster_path_policy_value_and_convergence():
+    n, A, b = 800, 6, 1
+    m, prob, P, c = make(n, A, seed=23, dtype=np.float32, gamma=0.9)
+    sol = prob.vi(b, seed=1, eps=1e-8, max_sweeps=2000)
+    ref = oracle.vi(m, b, seed=1, eps=1e-8, max_sweeps=2000)
+    assert sol.status == rmb.OK and sol.stats.sweeps == ref.sweeps
+    assert_close(sol.V.cpu().numpy(), ref.V, 1e-9)
+    pi = np.random.default_rng(3).integers(0, A, n).astype(np.int32)
+    pv = prob.policy_value(tdev(pi), b=b, seed=2, eps=1e-10)
+    J = oracle.policy_value(m, pi)
+    assert np.abs(pv.V.cpu().numpy() - J).max() <= 0.9 * pv.stats.final_residual / 0.1 + 1e-9
