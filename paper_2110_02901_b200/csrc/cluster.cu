@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -34,8 +36,9 @@
 
 namespace rmb {
 
-constexpr int kCThreads = 256;  // 8 warps per CTA, every one a compute warp
+constexpr int kCThreads = 288;  // 8 compute warps + the issuing warp (all take part in the combine)
 constexpr int kCWarps = kCThreads / kWarp;
+constexpr int kCDot = 8;        // warps that dot the stages; warp kCDot issues the bulk copies
 constexpr int kCRowsMax = 16;   // rows per ring stage
 constexpr int kCBatchRows = 256;  // rows (states x actions) per batch this path serves
 
@@ -109,8 +112,12 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
     constexpr int E = 16 / (int)sizeof(PT);
     using VT = typename std::conditional<sizeof(PT) == 4, float4, double2>::type;
 
+    // V in shared memory; fp32 P: split planes (lo: V[4q], V[4q+1]; hi:
+    // V[4q+2], V[4q+3]) so that a lane's two 16-byte reads are conflict-free
+    const int vhalf = sizeof(PT) == 4 ? ((n + 3) & ~3) / 2 : 0;
+    auto vidx = [&](int j) { return vhalf ? ((j & 2) ? vhalf : 0) + ((j >> 2) << 1) + (j & 1) : j; };
     for (int j = t; j < n; j += kCThreads) {
-        Vs[j] = a.V[j];
+        Vs[vidx(j)] = a.V[j];
         if (a.eval) pis[j] = a.pi[j];
     }
     if (t == 0)
@@ -142,38 +149,73 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     const PT* P = static_cast<const PT*>(a.P);
     const int64_t last_sweep = a.k0 + a.max_iter - 1;
-    auto issue_one = [&]() {  // thread 0: the next job into ring slot issued % ring
-        if (pk > last_sweep) return;
-        CJob J;
-        job_at(pk, pb, ps, J);
-        const int slot = (int)(issued % a.ring);
-        unsigned char* dst = ring + (size_t)slot * a.rows * a.row_bytes;
-        const uint32_t* pm = a.identity ? nullptr : a.perm + (J.k % 3) * n;
-        const unsigned bytes = (unsigned)((c1 - c0) * (int)sizeof(PT));
-        mbar_arrive_tx(full + slot, bytes * (unsigned)J.nr);
-        for (int r = 0; r < J.nr; ++r) {
-            const int row = J.r0 + r;
-            const int i = row / Ae;
-            const int s = pm ? (int)__ldcg(pm + J.lo + i) : J.lo + i;
-            const int act = a.eval ? __ldcg(a.pi + s) : row - i * Ae;
-            bulk_g2s(dst + (size_t)r * a.row_bytes, P + ((int64_t)s * a.A + act) * n + c0, bytes, full + slot, pol);
-        }
-        ++issued;
-        if (++ps * a.rows >= J.cnt * Ae) {  // next batch
-            ps = 0;
-            if (++pb == nbatch) pb = 0, ++pk;
-        }
-    };
     // a job may be issued only once the perm of its sweep is visible: the next
     // sweep's order is drawn in batch 0 of the current one (so >= 2 batches per
     // sweep lets the stream run across sweeps; this path serves tiny batches)
     int64_t ck = a.k0;  // consumer position
     auto may_issue = [&](int64_t cons_k, int cons_b) {
-        return pk == cons_k || (pk == cons_k + 1 && cons_b >= 1);
+        return pk <= last_sweep && (pk == cons_k || (pk == cons_k + 1 && cons_b >= 1));
     };
-    if (t == 0)
-        for (int s = 0; s < a.ring && may_issue(ck, 0); ++s) issue_one();
+    // lane r's state id of job J, a raw L2 load: nothing consumes it until
+    // the job is issued (no scoreboard stall here)
+    auto state_of = [&](const CJob& J) -> int {
+        if (lane >= J.nr) return 0;
+        const uint32_t* pm = a.identity ? nullptr : a.perm + (J.k % 3) * n;
+        const int i = (J.r0 + lane) / Ae;
+        return pm ? (int)__ldcg(pm + J.lo + i) : J.lo + i;
+    };
+    auto source = [&](const CJob& J, int s) -> const PT* {
+        if (lane >= J.nr) return nullptr;
+        const int row = J.r0 + lane;
+        const int act = a.eval ? __ldcg(a.pi + s) : row - (row / Ae) * Ae;
+        return P + ((int64_t)s * a.A + act) * n + c0;
+    };
+    // warp 0: the next job into ring slot issued % ring (lane r: row r); the
+    // state ids of the job after it are looked up right away, so that their
+    // round trip overlaps everything until the next call
+    int pre_s = 0;
+    bool pre_ok = false;
+    auto issue_one = [&](int64_t cons_k, int cons_b) {
+        if (pk > last_sweep) return;
+        CJob J;
+        job_at(pk, pb, ps, J);
+        const PT* src = source(J, pre_ok ? pre_s : state_of(J));
+        const int slot = (int)(issued % a.ring);
+        unsigned char* dst = ring + (size_t)slot * a.rows * a.row_bytes;
+        const unsigned bytes = (unsigned)((c1 - c0) * (int)sizeof(PT));
+        if (lane == 0) mbar_arrive_tx(full + slot, bytes * (unsigned)J.nr);
+        __syncwarp();
+        if (lane < J.nr) bulk_g2s(dst + (size_t)lane * a.row_bytes, src, bytes, full + slot, pol);
+        ++issued;
+        if (++ps * a.rows >= J.cnt * Ae) {  // next batch
+            ps = 0;
+            if (++pb == nbatch) pb = 0, ++pk;
+        }
+        pre_ok = may_issue(cons_k, cons_b);
+        if (pre_ok) {
+            CJob J2;
+            job_at(pk, pb, ps, J2);
+            pre_s = state_of(J2);
+        }
+    };
+    if (warp == kCDot)
+        for (int s = 0; s < a.ring && may_issue(ck, 0); ++s) issue_one(ck, 0);
 
+    // phase profile of CTA 0 (rmb_last_phase_times): stream + dot, cluster barrier, combine
+    const bool lead = q == 0 && t == 0;
+    unsigned long long tmark = lead ? globaltimer_ns() : 0, t_comp = 0, t_bar = 0, t_comb = 0, t_wait = 0;
+    auto mark = [&](unsigned long long& acc) {
+        if (lead) {
+            const unsigned long long now = globaltimer_ns();
+            acc += now - tmark;
+            tmark = now;
+        }
+    };
+    int L = 1;  // lanes per state in the combine (pow2 >= Ae)
+    while (L < Ae) L <<= 1;
+    int cs_s[2] = {0, 0};
+    double cs_c[2] = {0.0, 0.0};
+    bool pre_comb = false;
     int64_t consumed = 0;
     long long status = RMB_ERR_NOT_CONVERGED;
     int64_t it = 0, batches = 0;
@@ -189,42 +231,94 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
             const int lo = bi * a.b, cnt = min(a.b, n - lo);
             const int nrows = cnt * Ae;
             double* pr = part + (size_t)(batches & 1) * kCBatchRows;
+            // the combine's states and costs: looked up one batch ahead (the
+            // state ids at the start of the previous batch, the costs after its
+            // combine), here only when nothing was prefetched
+            if (!pre_comb) {
+#pragma unroll
+                for (int rd = 0; rd < 2; ++rd) {
+                    const int id = rd * kCThreads + t;
+                    const int i = id / L, g = id - i * L;
+                    cs_s[rd] = i < cnt ? (pm ? (int)__ldcg(pm + lo + i) : lo + i) : 0;
+                    cs_c[rd] = i < cnt && g < Ae
+                                   ? (double)__ldg(static_cast<const PT*>(a.c) + (int64_t)cs_s[rd] * a.A +
+                                                   (a.eval ? pis[cs_s[rd]] : g))
+                                   : 0.0;
+                }
+            }
+            // the next batch's state ids (later in this sweep, or the first of
+            // the next sweep once its order is visible, i.e. from batch 1 on)
+            const bool nx_same = bi + 1 < nbatch;
+            const bool nx_ok = nx_same || (it + 1 < a.max_iter && nbatch >= 2);
+            const int nx_lo = nx_same ? lo + a.b : 0;
+            const int nx_cnt = min(a.b, n - nx_lo);
+            const uint32_t* nx_pm = a.identity ? nullptr : a.perm + ((nx_same ? k : k + 1) % 3) * n;
+            int nx_s[2] = {0, 0};
+            if (nx_ok && (nx_same || bi >= 1)) {
+#pragma unroll
+                for (int rd = 0; rd < 2; ++rd) {
+                    const int i = (rd * kCThreads + t) / L;
+                    nx_s[rd] = i < nx_cnt ? (nx_pm ? (int)__ldcg(nx_pm + nx_lo + i) : nx_lo + i) : 0;
+                }
+            }
             for (int st = 0; st * a.rows < nrows; ++st) {
                 const int slot = (int)(consumed % a.ring);
                 const unsigned ph = (unsigned)((consumed / a.ring) & 1);
                 CJob J;
                 job_at(k, bi, st, J);
+                if (warp == kCDot) {  // refill the ring (the slot of the previous job is free) while the others dot
+                    ck = k;
+                    while (issued < consumed + a.ring && may_issue(k, bi)) issue_one(k, bi);
+                }
                 {
+                    mark(t_comp);
                     SpinGuard sg;
                     while (!mbar_try(full + slot, ph)) sg.tick();
+                    mark(t_wait);
                 }
                 const unsigned char* stg = ring + (size_t)slot * a.rows * a.row_bytes;
                 const int nv = (c1 - c0) / E;  // 16-byte vectors of the slab (slab and n are multiples of E)
-                for (int r = warp; r < J.nr; r += kCWarps) {
-                    const VT* row = reinterpret_cast<const VT*>(stg + (size_t)r * a.row_bytes);
-                    double acc = 0.0;
+                // warp w dots rows w and w + 8 of the stage; each V vector is
+                // read once (conflict-free split planes) for both rows
+                if (warp < kCDot && warp < J.nr) {
+                    const bool two = warp + kCDot < J.nr;
+                    const VT* row0 = reinterpret_cast<const VT*>(stg + (size_t)warp * a.row_bytes);
+                    const VT* row1 = reinterpret_cast<const VT*>(stg + (size_t)(warp + kCDot) * a.row_bytes);
+                    double acc0 = 0.0, acc1 = 0.0;
                     for (int v = lane; v < nv; v += kWarp) {
-                        const VT x = row[v];
                         const int j = c0 + v * E;
+                        double vs[E];
                         if constexpr (sizeof(PT) == 4) {
-                            acc = fma((double)x.x, Vs[j], acc);
-                            acc = fma((double)x.y, Vs[j + 1], acc);
-                            acc = fma((double)x.z, Vs[j + 2], acc);
-                            acc = fma((double)x.w, Vs[j + 3], acc);
+                            const double2 lo = *reinterpret_cast<const double2*>(Vs + (j >> 1));
+                            const double2 hi = *reinterpret_cast<const double2*>(Vs + vhalf + (j >> 1));
+                            vs[0] = lo.x, vs[1] = lo.y, vs[2] = hi.x, vs[3] = hi.y;
                         } else {
-                            acc = fma(x.x, Vs[j], acc);
-                            acc = fma(x.y, Vs[j + 1], acc);
+                            const double2 x = *reinterpret_cast<const double2*>(Vs + j);
+                            vs[0] = x.x, vs[1] = x.y;
+                        }
+                        const VT x0 = row0[v];
+                        const double p0[4] = {(double)x0.x, (double)x0.y, sizeof(PT) == 4 ? (double)((const float*)&x0)[2] : 0.0,
+                                              sizeof(PT) == 4 ? (double)((const float*)&x0)[3] : 0.0};
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc0 = fma(p0[e], vs[e], acc0);
+                        if (two) {
+                            const VT x1 = row1[v];
+                            const double p1[4] = {(double)x1.x, (double)x1.y,
+                                                  sizeof(PT) == 4 ? (double)((const float*)&x1)[2] : 0.0,
+                                                  sizeof(PT) == 4 ? (double)((const float*)&x1)[3] : 0.0};
+#pragma unroll
+                            for (int e = 0; e < E; ++e) acc1 = fma(p1[e], vs[e], acc1);
                         }
                     }
-                    acc = warp_sum(acc);
-                    if (lane == 0) pr[J.r0 + r] = acc;
+                    acc0 = warp_sum(acc0);
+                    acc1 = warp_sum(acc1);
+                    if (lane == 0) {
+                        pr[J.r0 + warp] = acc0;
+                        if (two) pr[J.r0 + warp + kCDot] = acc1;
+                    }
                 }
                 __syncthreads();  // every warp is done with the slot
                 ++consumed;
-                if (t == 0) {
-                    ck = k;
-                    while (issued < consumed + a.ring && may_issue(k, bi)) issue_one();
-                }
             }
             // next sweep's order, off the critical path (batch 0)
             if (bi == 0 && !a.identity) {
@@ -234,24 +328,29 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
                 for (int p = (int)q * kCThreads + t; p < n; p += (int)CS * kCThreads)
                     dst[p] = (uint32_t)pm2((uint64_t)p);
             }
+            mark(t_comp);
             cluster_sync();  // the batch's partials of every CTA are complete (and its reads of V done)
+            mark(t_bar);
             // combine: L = pow2 >= Ae lanes per state; lane g takes action g;
-            // partials of the CS CTAs added in CTA order
-            int L = 1;
-            while (L < Ae) L <<= 1;
-            for (int base = 0; base < cnt * L; base += kCThreads) {
-                const int id = base + t;
+            // partials of the CS CTAs added in CTA order (cnt * L <= 2 * 256 < 2 * kCThreads)
+            for (int rd = 0; rd * kCThreads < cnt * L; ++rd) {
+                const int id = rd * kCThreads + t;
                 const int i = id / L, g = id - i * L;
                 const bool valid = i < cnt && g < Ae;
                 double Q = INFINITY;
                 int arg = 0x7fffffff;
-                int s = 0;
-                if (i < cnt) s = pm ? (int)__ldcg(pm + lo + i) : lo + i;
+                const int s = rd ? cs_s[1] : cs_s[0];
                 if (valid) {
+                    // all CS remote loads in flight at once, then added in CTA order
+                    double pv[16];
+#pragma unroll
+                    for (unsigned cq = 0; cq < 16; ++cq) pv[cq] = cq < CS ? *dsmem(pr + i * Ae + g, cq) : 0.0;
                     double sum = 0.0;
-                    for (unsigned cq = 0; cq < CS; ++cq) sum += *dsmem(pr + i * Ae + g, cq);
+#pragma unroll
+                    for (unsigned cq = 0; cq < 16; ++cq)
+                        if (cq < CS) sum += pv[cq];
                     const int act = a.eval ? pis[s] : g;
-                    Q = (double)__ldg(static_cast<const PT*>(a.c) + (int64_t)s * a.A + act) + a.gamma * sum;
+                    Q = (rd ? cs_c[1] : cs_c[0]) + a.gamma * sum;
                     arg = act;
                 }
                 // argmin over the L lanes of the state (lower value, then lower action)
@@ -261,9 +360,9 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
                     if (ov < Q || (ov == Q && oa < arg)) Q = ov, arg = oa;
                 }
                 if (valid && g == 0) {
-                    rmax = fmax(rmax, fabs(Q - Vs[s]));
+                    rmax = fmax(rmax, fabs(Q - Vs[vidx(s)]));
                     bad |= !isfinite(Q);
-                    Vs[s] = Q;
+                    Vs[vidx(s)] = Q;
                     if (q == 0) {
                         a.V[s] = Q;
                         if (!a.eval && a.pi) a.pi[s] = arg;
@@ -271,6 +370,20 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
                 }
             }
             __syncthreads();  // the patched V is visible to the CTA's next batch
+            pre_comb = nx_ok && (nx_same || bi >= 1);
+            if (pre_comb) {  // the next batch's costs (its state ids arrived during this batch)
+#pragma unroll
+                for (int rd = 0; rd < 2; ++rd) {
+                    const int id = rd * kCThreads + t;
+                    const int i = id / L, g = id - i * L;
+                    cs_s[rd] = nx_s[rd];
+                    cs_c[rd] = i < nx_cnt && g < Ae
+                                   ? (double)__ldg(static_cast<const PT*>(a.c) + (int64_t)nx_s[rd] * a.A +
+                                                   (a.eval ? pis[nx_s[rd]] : g))
+                                   : 0.0;
+                }
+            }
+            mark(t_comb);
             ++batches;
         }
         // sweep residual: every CTA patched every state, so the CTA-local max
@@ -294,8 +407,8 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         last = r;
         if (bb) { status = RMB_ERR_NONFINITE; break; }
         if (a.eps >= 0.0 && r <= a.eps) { status = RMB_OK; break; }
-        if (t == 0)  // the next sweep's first batch may now stream (its order is visible)
-            while (issued < consumed + a.ring && may_issue(ck, 0)) issue_one();
+        if (warp == kCDot)  // the next sweep's first batch may now stream (its order is visible)
+            while (issued < consumed + a.ring && may_issue(ck, 0)) issue_one(ck, 0);
     }
     if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
     // drain: bulk copies in flight must land before the CTA exits
@@ -315,8 +428,11 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         a.out[OUT_RESID_BITS] = __double_as_longlong(last);
         a.out[OUT_BATCHES] = batches;
         a.out[OUT_CHANGED] = 0;
-        a.prof[0] = a.prof[1] = a.prof[2] = 0;
-        a.prof[3] = batches;
+        a.prof[0] = (long long)t_comp;
+        a.prof[1] = (long long)t_bar;
+        a.prof[2] = (long long)t_comb;
+        a.prof[3] = batches + 2;  // cluster barriers (one per batch, one at each end)
+        a.out[7] = (long long)t_wait;  // of prof[0]: waiting for the ring
     }
 }
 
@@ -479,8 +595,9 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     res->ms = ms;
     res->launches = 1;
     for (int i = 0; i < 4; ++i) pr.prof[i] = out[OUT_N + i];
-    pr.prof[2] = CS;  // the phase slot of the combine reports the cluster size on this path
+    pr.prof[0] += out[7];  // stream + dot = ring wait + the rest of the compute phase
     pr.last_launches = 1;
+    if (getenv("RMB_CLUSTER_DEBUG")) fprintf(stderr, "cluster CS=%d ring=%d rows=%d slab=%d ring_wait_ns=%lld\n", CS, a.ring, a.rows, a.slab, out[7]);
     return RMB_OK;
 }
 

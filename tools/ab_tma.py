@@ -6,7 +6,8 @@ import paper_2110_02901_b200 as rmb
 n, A = 10_000, 16
 BS = tuple(int(x) for x in sys.argv[1].split(',')) if len(sys.argv) > 1 else (10000, 2000, 1000, 250, 64, 1)
 P, c = rmb.generate_dense(n, A, 1)
-probs = {"tma": rmb.Problem.dense(P, c, 0.99), "warp": rmb.Problem.dense(P, c, 0.99, tma=False)}
+probs = {"tma": rmb.Problem.dense(P, c, 0.99, flags=rmb.DENSE_NO_CLUSTER), "warp": rmb.Problem.dense(P, c, 0.99, tma=False),
+         "cluster": rmb.Problem.dense(P, c, 0.99)}
 for name, prob in probs.items():
     prob.vi(1000, seed=0, eps=1e-6, max_sweeps=3)
 for b in BS:
