@@ -99,7 +99,8 @@ typedef struct {
                              (NVLink peer memory, CUDA IPC handles exchanged over the handle's NCCL
                              communicator) and the ranks meet at an in-kernel cross-rank barrier:
                              no host round trip or NCCL launch per batch.  Needs the TMA path
-                             (16-byte aligned rows), <= 8 ranks; results bitwise those of one GPU.
+                             (16-byte aligned rows), <= 8 ranks; results bitwise those of the
+                             single-GPU grid solver.
                              With rmb_*_group the G logical ranks share one launch on one device. */
 
 /* Create a handle over a DENSE MDP.
@@ -188,8 +189,10 @@ rmb_status rmb_improve(rmb_problem h, const void* V, int32_t* pi, double* bellma
  * V replicated, one exchange of the batch's updated (state, value, argmin)
  * entries per batch (an all-gather).  The partition of every sweep is global,
  * so each batch is the same set of states on every rank, and every state's
- * backup is computed with the single-GPU arithmetic: V, pi and the residual
- * trace are bitwise identical for any number of ranks.
+ * backup is computed with the single-GPU grid solver's arithmetic: V, pi and
+ * the residual trace are bitwise identical for any number of ranks (and to a
+ * single handle created with RMB_DENSE_NO_CLUSTER; tiny batches on one GPU
+ * otherwise run on the one-cluster path, equal to fp64 rounding).
  * A shard handle is created with desc.row_begin/row_end from rmb_shard_range
  * and P / c pointing at the owned rows only ([row_end-row_begin][A][n] and
  * [row_end-row_begin][A]) -- for rmb_create_csr: row_ptr [(row_end-row_begin)*A+1]

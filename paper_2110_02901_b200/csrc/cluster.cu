@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = a.n;
     const int Ae = a.eval ? 1 : a.A;
-    const int c0 = (int)q * a.slab, c1 = min(n, c0 + a.slab);
+    // this CTA's columns (possibly none when n is small)
+    const int c0 = min(n, (int)q * a.slab), c1 = min(n, c0 + a.slab);
     constexpr int E = 16 / (int)sizeof(PT);
     using VT = typename std::conditional<sizeof(PT) == 4, float4, double2>::type;
 
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         const unsigned bytes = (unsigned)((c1 - c0) * (int)sizeof(PT));
         if (lane == 0) mbar_arrive_tx(full + slot, bytes * (unsigned)J.nr);
         __syncwarp();
-        if (lane < J.nr) bulk_g2s(dst + (size_t)lane * a.row_bytes, src, bytes, full + slot, pol);
+        if (lane < J.nr && bytes > 0) bulk_g2s(dst + (size_t)lane * a.row_bytes, src, bytes, full + slot, pol);
         ++issued;
         if (++ps * a.rows >= J.cnt * Ae) {  // next batch
             ps = 0;
@@ -485,7 +486,7 @@ static int cluster_size(size_t smem)
     auto kern = dense_cluster_kernel<PT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs = 16; cs >= 2; cs >>= 1) {
+    for (int cs = 16; cs >= 1; cs >>= 1) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs);
         cfg.blockDim = dim3(kCThreads);
@@ -553,7 +554,9 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     int CS = 16;
     if (!layout(CS, smem)) return RMB_ERR_UNSUPPORTED;
     CS = pr.pdt == RMB_F32 ? cluster_size<float>(smem) : cluster_size<double>(smem);
-    if (CS < 2) return RMB_ERR_UNSUPPORTED;
+    // at least ~256 columns per CTA: fewer CTAs for small n (less to synchronise)
+    while (CS > 1 && (int64_t)CS * 256 > n) CS >>= 1;
+    if (CS < 1) return RMB_ERR_UNSUPPORTED;
     if (!layout(CS, smem)) return RMB_ERR_UNSUPPORTED;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("cluster solver: workspace allocation failed");
