@@ -74,9 +74,11 @@ def _load():
         lib.orc_set_threads.argtypes, lib.orc_set_threads.restype = [ctypes.c_int], None
         lib.orc_get_threads.argtypes, lib.orc_get_threads.restype = [], ctypes.c_int
         lib.orc_improve.argtypes = [pm, vp, vp, vp, vp]
-        lib.orc_vi.argtypes = [pm, i64, u64, ctypes.c_int, i64, dbl, i64, ctypes.c_int, vp, vp, vp, vp]
+        lib.orc_vi.argtypes = [pm, i64, u64, ctypes.c_int, i64, dbl, i64, ctypes.c_int, vp, vp, vp, vp,
+                               ctypes.c_int, vp]
         lib.orc_mpi.argtypes = [pm, i64, i32, u64, ctypes.c_int, i64, dbl, i64, ctypes.c_int,
-                                vp, vp, vp, vp, vp, vp]
+                                vp, vp, vp, vp, vp, vp, ctypes.c_int, vp]
+        lib.orc_select.argtypes, lib.orc_select.restype = [i64, u64, i64, vp, vp], ctypes.c_int
         lib.orc_backup_dense_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, i32, vp]
         lib.orc_backup_dense_row.restype = dbl
         lib.orc_backup_csr_row.argtypes = [i64, i32, dbl, ctypes.c_int, vp, vp, vp, vp, vp, i32, vp]
@@ -173,6 +175,28 @@ def partition_inverse(n: int, seed: int, k: int, identity: bool = False) -> np.n
     return out
 
 
+def select(n: int, seed: int, k: int, weights: np.ndarray | None = None) -> np.ndarray:
+    """The n states drawn WITH replacement for operator application k (DESIGN
+    R28-R29): uniform, or P(s) = w_s / sum(w) for
+    integer weights w_s >= 1."""
+    out = np.empty(n, dtype=np.uint32)
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.uint32)
+    if w is not None and w.shape != (n,):
+        raise ValueError("select: weights must have n entries")
+    rc = _load().orc_select(n, seed, k, _p(w), _p(out))
+    if rc:
+        raise ValueError("select: invalid argument (n out of range or a zero weight)")
+    return out
+
+
+def _sel_args(select, weights, n):
+    if weights is not None:
+        w = np.ascontiguousarray(weights, dtype=np.uint32)
+        assert w.shape == (n,)
+        return 1, w
+    return int(bool(select)), None
+
+
 # ------------------------------------------------------------ the operator
 def sweep(m: MDP, V: np.ndarray, b: int, perm: np.ndarray, pi: np.ndarray | None = None):
     """One application of B_b (pi None) or B_{pi,b}: returns (V', argmin, r)."""
@@ -225,15 +249,17 @@ class Result:
 
 def vi(m: MDP, b: int, seed: int = 0, eps: float = 1e-6, max_sweeps: int = 100000,
        V0: np.ndarray | None = None, identity: bool = False, first_sweep: int = 1,
-       chunked: bool = False) -> Result:
+       chunked: bool = False, replace: bool = False, weights: np.ndarray | None = None) -> Result:
     """MB-VI (P:L186) to ||V_k - V_{k-1}||_inf <= eps; chunked=True: VI* (P:L577),
-    T in chunks of b states against the old values."""
+    T in chunks of b states against the old values; replace=True / weights:
+    every sweep draws n states with replacement (uniform / P(s) ~ w_s, R28-R29)."""
     V = np.zeros(m.n) if V0 is None else np.array(V0, dtype=np.float64, copy=True)
     pi = np.zeros(m.n, dtype=np.int32)
     tr = np.zeros(max_sweeps)
     sw = ctypes.c_int64()
+    sel, w = _sel_args(replace, weights, m.n)
     st = _load().orc_vi(ctypes.byref(m._s), b, seed, int(identity), first_sweep, eps, max_sweeps,
-                        int(chunked), _p(V), _p(pi), _p(tr), ctypes.byref(sw))
+                        int(chunked), _p(V), _p(pi), _p(tr), ctypes.byref(sw), sel, _p(w))
     if st == INVALID_ARG:
         raise ValueError("vi: invalid argument")
     return Result(st, V, pi, tr[: sw.value], sw.value)
@@ -241,16 +267,18 @@ def vi(m: MDP, b: int, seed: int = 0, eps: float = 1e-6, max_sweeps: int = 10000
 
 def mpi(m: MDP, b: int, msweeps: int, seed: int = 0, eps: float = 1e-6, max_outer: int = 10000,
         V0: np.ndarray | None = None, pi0: np.ndarray | None = None, identity: bool = False,
-        first_sweep: int = 1) -> Result:
-    """MB-MPI: Algorithm 1 with B_{pi,b} evaluation and warm start."""
+        first_sweep: int = 1, replace: bool = False, weights: np.ndarray | None = None) -> Result:
+    """MB-MPI: Algorithm 1 with B_{pi,b} evaluation and warm start
+    (replace / weights: evaluation sweeps draw with replacement, R28-R29)."""
     V = np.zeros(m.n) if V0 is None else np.array(V0, dtype=np.float64, copy=True)
     pi = np.zeros(m.n, dtype=np.int32) if pi0 is None else np.array(pi0, dtype=np.int32, copy=True)
     tr = np.zeros(max_outer * (msweeps + 1))
     chg = np.zeros(max_outer, dtype=np.int64)
     sw, ou = ctypes.c_int64(), ctypes.c_int64()
+    sel, w = _sel_args(replace, weights, m.n)
     st = _load().orc_mpi(ctypes.byref(m._s), b, msweeps, seed, int(identity), first_sweep, eps, max_outer,
                          int(pi0 is not None), _p(V), _p(pi), _p(tr), _p(chg), ctypes.byref(sw),
-                         ctypes.byref(ou))
+                         ctypes.byref(ou), sel, _p(w))
     if st == INVALID_ARG:
         raise ValueError("mpi: invalid argument")
     o = ou.value

@@ -171,6 +171,75 @@ int orc_partition_inverse(int64_t n, uint64_t seed, int64_t k, int identity, uin
 }
 
 /* ------------------------------------------------------------------ */
+/* State selection WITH replacement ("there  */
+/* could be advantages in sampling the states with replacement and/or   */
+/* according to a non-uniform distribution ... importance-sampling ...  */
+/* epsilon-greedy").  The paper defines no law; DESIGN readings R28-R29: */
+/*   key_k  = mix64(mix64(seed) ^ k)           (as the partition, R2)    */
+/*   skey_k = mix64(key_k ^ 0x5E1EC7105E1EC710)                          */
+/*   u_i    = mix64(skey_k + i),  i = 0 .. n-1  (n draws per sweep)      */
+/*   uniform:  s_i = floor(u_i * n / 2^64)                               */
+/*   weighted (integer w_s >= 1, W = sum w_s < 2^63):                    */
+/*             t_i = floor(u_i * W / 2^64),                              */
+/*             s_i = min { s : w_0 + ... + w_s > t_i }                   */
+/* i.e. P(s_i = s) = w_s / W up to 2^-64.  Batch t = draws [t*b, ...)   */
+/* as R4; a state drawn twice in one batch is backed up once (both      */
+/* copies read the same interim V, Eq. 12 is a statement about the set  */
+/* of the batch's states).                                              */
+/* ------------------------------------------------------------------ */
+#define ORC_SEL_C 0x5E1EC7105E1EC710ULL
+
+static uint64_t mulhi64(uint64_t a, uint64_t b)
+{
+    return (uint64_t)(((unsigned __int128)a * (unsigned __int128)b) >> 64);
+}
+
+int orc_select(int64_t n, uint64_t seed, int64_t k, const uint32_t* w, uint32_t* sel)
+{
+    if (n < 1 || n > 0x7FFFFFFFLL || !sel) return ORC_INVALID_ARG;
+    uint64_t* cum = NULL;
+    uint64_t W = 0;
+    if (w) {
+        /* inclusive prefix sums C_s = w_0 + ... + w_s, sequential */
+        cum = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+        if (!cum) return ORC_OOM;
+        for (int64_t s = 0; s < n; ++s) {
+            if (w[s] == 0) { free(cum); return ORC_INVALID_ARG; }
+            W += w[s];
+            cum[s] = W;
+        }
+    }
+    const uint64_t key = orc_mix64(orc_mix64(seed) ^ (uint64_t)k);
+    const uint64_t skey = orc_mix64(key ^ ORC_SEL_C);
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t u = orc_mix64(skey + (uint64_t)i);
+        if (!w) {
+            sel[i] = (uint32_t)mulhi64(u, (uint64_t)n);
+        } else {
+            const uint64_t t = mulhi64(u, W);
+            /* smallest s with cum[s] > t (plain binary search) */
+            int64_t lo = 0, hi = n - 1;
+            while (lo < hi) {
+                int64_t mid = lo + (hi - lo) / 2;
+                if (cum[mid] > t) hi = mid;
+                else lo = mid + 1;
+            }
+            sel[i] = (uint32_t)lo;
+        }
+    }
+    free(cum);
+    return ORC_OK;
+}
+
+/* the order of operator application k: the partition (R2) or, with
+   select != 0, the n draws with replacement (R28-R29) */
+static int draw_order(int64_t n, uint64_t seed, int64_t k, int identity, int select, const uint32_t* w,
+                      uint32_t* perm)
+{
+    return select ? orc_select(n, seed, k, w, perm) : orc_partition(n, seed, k, identity, perm);
+}
+
+/* ------------------------------------------------------------------ */
 /* Q-value: g(i,u) + alpha * sum_j p_ij(u) J(j)   (Eq. 7)        */
 /* ------------------------------------------------------------------ */
 static double q_value(const orc_mdp* m, int64_t s, int32_t a, const double* J)
@@ -337,25 +406,41 @@ int orc_improve(const orc_mdp* m, const double* V, int32_t* pi, double* bellman_
 /* sweep (reading R9).  trace[i] = r_{first_sweep+i}.                   */
 /* chunked != 0: VI* of P:L577 instead -- every application is T in     */
 /* chunks of b states against the old values (orc_sweep_chunked).       */
+/* select != 0: every application draws n states WITH replacement      */
+/* (orc_select; w = integer weights or NULL for uniform, R28-R29).  r_k */
+/* is then the max change over the DRAWN states only, so r_k <= eps     */
+/* only triggers the stopping test of R30: rT = ||TV - V||_inf (the     */
+/* improvement pass, orc_improve, pi <- greedy(V)); stop iff rT <= eps. */
+/* On OK, pi = greedy(V) and ||V - V*|| <= rT / (1 - gamma).            */
 /* ------------------------------------------------------------------ */
 int orc_vi(const orc_mdp* m, int64_t b, uint64_t seed, int identity, int64_t first_sweep,
            double eps, int64_t max_sweeps, int chunked, double* V, int32_t* pi, double* trace,
-           int64_t* sweeps_out)
+           int64_t* sweeps_out, int select, const uint32_t* w)
 {
     if (!m || !V || !pi || b < 1 || b > m->n || max_sweeps < 1 || !(eps > 0.0)) return ORC_INVALID_ARG;
+    if (select && (chunked || identity)) return ORC_INVALID_ARG;
     uint32_t* perm = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m->n);
     if (!perm) return ORC_OOM;
     int st = ORC_NOT_CONVERGED;
     int64_t it = 0;
     while (it < max_sweeps) {
         double r;
-        orc_partition(m->n, seed, first_sweep + it, identity, perm);
+        if (draw_order(m->n, seed, first_sweep + it, identity, select, w, perm)) { st = ORC_INVALID_ARG; break; }
         int rc = chunked ? orc_sweep_chunked(m, b, perm, NULL, V, pi, &r)
                          : orc_sweep(m, b, perm, NULL, V, pi, &r);
         if (trace) trace[it] = r;
         ++it;
         if (rc == ORC_NONFINITE) { st = ORC_NONFINITE; break; }
-        if (r <= eps) { st = ORC_OK; break; }
+        if (r <= eps) {
+            if (select) {  /* R30: confirm on all states */
+                double rT;
+                int64_t ch;
+                if (orc_improve(m, V, pi, &rT, &ch) == ORC_NONFINITE) { st = ORC_NONFINITE; break; }
+                if (rT > eps) continue;
+            }
+            st = ORC_OK;
+            break;
+        }
     }
     free(perm);
     if (sweeps_out) *sweeps_out = it;
@@ -372,13 +457,15 @@ int orc_vi(const orc_mdp* m, int64_t b, uint64_t seed, int identity, int64_t fir
 /*   stop when changed == 0 and r_T <= eps (reading R11).               */
 /* trace layout: trace[o*(m+1) + e], e < m eval residuals, e = m: r_T.  */
 /* changed_trace[o] = changed count of outer iteration o.               */
+/* select != 0: evaluation sweeps draw with replacement (as orc_vi).    */
 /* ------------------------------------------------------------------ */
 int orc_mpi(const orc_mdp* m, int64_t b, int32_t msweeps, uint64_t seed, int identity, int64_t first_sweep,
             double eps, int64_t max_outer, int pi_given, double* V, int32_t* pi, double* trace,
-            int64_t* changed_trace, int64_t* sweeps_out, int64_t* outer_out)
+            int64_t* changed_trace, int64_t* sweeps_out, int64_t* outer_out, int select, const uint32_t* w)
 {
     if (!m || !V || !pi || b < 1 || b > m->n || msweeps < 1 || max_outer < 1 || !(eps > 0.0))
         return ORC_INVALID_ARG;
+    if (select && identity) return ORC_INVALID_ARG;
     uint32_t* perm = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m->n);
     if (!perm) return ORC_OOM;
     int st = ORC_NOT_CONVERGED;
@@ -392,12 +479,13 @@ int orc_mpi(const orc_mdp* m, int64_t b, int32_t msweeps, uint64_t seed, int ide
         int bad = 0;
         for (int32_t e = 0; e < msweeps; ++e) {
             double r;
-            orc_partition(m->n, seed, k, identity, perm);
+            if (draw_order(m->n, seed, k, identity, select, w, perm)) { bad = 2; break; }
             int rc = orc_sweep(m, b, perm, pi, V, NULL, &r);
             ++k;
             if (trace) trace[o * (msweeps + 1) + e] = r;
             if (rc == ORC_NONFINITE) { bad = 1; break; }
         }
+        if (bad == 2) { st = ORC_INVALID_ARG; break; }
         if (bad) { st = ORC_NONFINITE; ++o; break; }
         double rT;
         int64_t ch;
