@@ -89,6 +89,20 @@ typedef struct {
 #define RMB_DENSE_NO_CLUSTER 0x1000u /* rmb_create_dense: never use the one-cluster solver for tiny batches
                                       (<= 2 MB of P and <= 256 rows per batch: 16 CTAs, DSMEM combine,
                                       hardware cluster barrier); results agree to fp64 rounding        */
+#define RMB_SELECT_REPLACE 0x2000u  /* rmb_vi / rmb_mpi / rmb_apply: SURVEY 8(f) row 4, P:L605 ("sampling the
+                                       states with replacement and/or according to a non-uniform
+                                       distribution") -- every operator application draws n states
+                                       i.i.d. uniformly WITH replacement (DESIGN R28: counter-based,
+                                       s_i = floor(mix64(skey_k + i) * n / 2^64)); batches are
+                                       consecutive blocks of b draws; a state drawn twice in a batch is
+                                       backed up once; undrawn states keep their values.  rmb_vi's stop
+                                       test then confirms r_k <= eps with ||TV - V||_inf <= eps over all
+                                       states (R30; pi = greedy(V) on OK).  Single-GPU handles only;
+                                       excludes RMB_ORDER_IDENTITY and RMB_CHUNKED_T.                   */
+#define RMB_SELECT_WEIGHTED 0x4000u /* as RMB_SELECT_REPLACE, drawing state s with probability w_s / W for
+                                       the handle's integer weights (rmb_set_selection_weights; DESIGN
+                                       R29: inverse CDF on integer prefix sums).  Importance-sampling and
+                                       epsilon-greedy laws are choices of w.                             */
 /* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly
@@ -232,6 +246,18 @@ rmb_status rmb_mpi_group(rmb_problem* handles, int32_t G, int64_t b, int32_t m, 
  * batch t = positions [t*b, min(n,(t+1)*b)).  perm: HOST [n] uint32.
  * flags: RMB_ORDER_IDENTITY gives the identity. */
 rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* perm);
+
+/* State selection with replacement (DESIGN R28-R29).
+ * rmb_set_selection_weights: w = [n] uint32 weights >= 1 (HOST or DEVICE,
+ * copied; NULL clears) for RMB_SELECT_WEIGHTED; a zero weight returns
+ * INVALID_ARG (every state needs a positive probability for convergence).
+ * rmb_select: HOST generator of application `sweep`'s n draws, sel [n] HOST
+ * uint32 (w HOST or NULL = uniform).  rmb_select_device: the same draws from
+ * the device kernel the solvers use (flags RMB_SELECT_REPLACE or
+ * RMB_SELECT_WEIGHTED with the handle's weights), sel: DEVICE [n]. */
+rmb_status rmb_set_selection_weights(rmb_problem h, const uint32_t* w);
+rmb_status rmb_select(int64_t n, uint64_t seed, int64_t sweep, const uint32_t* w, uint32_t* sel);
+rmb_status rmb_select_device(rmb_problem h, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* sel);
 
 /* The same permutation evaluated by the device kernel the solver uses
  * (perm: DEVICE [n] uint32) — exposed for parity tests. */

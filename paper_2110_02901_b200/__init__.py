@@ -29,6 +29,7 @@ F32, F64 = 0, 1
 ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 CHUNKED_T = 0x40
 SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED, DENSE_NO_CLUSTER = 0x80, 0x400, 0x800, 0x1000
+SELECT_REPLACE, SELECT_WEIGHTED = 0x2000, 0x4000
 
 _lib = None
 
@@ -97,6 +98,10 @@ _SIGS = {
                        ctypes.c_uint64, ctypes.c_double, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "rmb_last_phase_times": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_set_selection_weights": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_select": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_select_device": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p],
+                          ctypes.c_int),
     "rmb_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "rmb_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "rmb_last_error": ([], ctypes.c_char_p),
@@ -267,35 +272,39 @@ class Problem:
         return _vec(V, self.n, "f64", "V"), _vec(pi, self.n, "i32", "pi")
 
     def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-           device="cuda", chunked=False, fused=False):
+           device="cuda", chunked=False, fused=False, select=None):
         """MB-VI: V, pi updated in place (torch cuda/cpu or numpy).
         chunked=True: VI* -- every sweep is T computed in chunks of b
-        states against the sweep-start values (RMB_CHUNKED_T)."""
+        states against the sweep-start values (RMB_CHUNKED_T).
+        select="replace" / "weighted": every sweep draws n states with
+        replacement, uniformly / by the weights of set_selection_weights (R28-R30)."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_sweeps)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
-                 | (FUSED if fused else 0))
+                 | (FUSED if fused else 0) | _select_flag(select))
         s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         return Solution(V, pi, tr[: st.sweeps], s, st)
 
     def mpi(self, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
-            v0_zero=False, device="cuda", fused=False):
-        """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start."""
+            v0_zero=False, device="cuda", fused=False, select=None):
+        """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start
+        (select: evaluation sweeps draw with replacement, as vi())."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_outer * (m + 1))
         ch = np.zeros(max_outer, dtype=np.int64)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
-                 | (FUSED if fused else 0))
+                 | (FUSED if fused else 0) | _select_flag(select))
         s = lib().rmb_mpi(self._h, b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi), _ptr(tr), _ptr(ch),
                           ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         o = st.outer_iters
         return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
 
-    def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False, chunked=False):
+    def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False, chunked=False,
+              select=None):
         """One application of B_b (pi None) or B_{pi,b}: returns (V_out, argmin, residual)."""
         import torch
         _vec(V_in, self.n, "f64", "V_in")
@@ -308,7 +317,7 @@ class Problem:
                       if not isinstance(V_out, np.ndarray) else np.empty(self.n, np.int32))
         _vec(argmin, self.n, "i32", "argmin")
         r = ctypes.c_double()
-        flags = (ORDER_IDENTITY if identity else 0) | (CHUNKED_T if chunked else 0)
+        flags = (ORDER_IDENTITY if identity else 0) | (CHUNKED_T if chunked else 0) | _select_flag(select)
         s = lib().rmb_apply(self._h, b, seed, sweep, flags, _ptr(pi), _ptr(V_in),
                             _ptr(V_out), _ptr(argmin), ctypes.byref(r))
         _check(s, (OK, NONFINITE))
@@ -337,6 +346,26 @@ class Problem:
         s = lib().rmb_improve(self._h, _ptr(V), _ptr(pi), ctypes.byref(r), ctypes.byref(ch))
         _check(s, (OK, NONFINITE))
         return pi, r.value, ch.value
+
+    def set_selection_weights(self, w):
+        """Integer weights w_s >= 1 ([n] uint32, host or device; None clears) for
+        select="weighted": state s is drawn with probability w_s / sum(w) (R29)."""
+        if w is not None:
+            import torch
+            if w.dtype not in (np.uint32, torch.int32, np.int32):
+                raise TypeError(f"weights must be uint32 (or int32 >= 1), got {w.dtype}")
+            numel = w.size if isinstance(w, np.ndarray) else w.numel()
+            if numel != self.n:
+                raise ValueError(f"weights must have n = {self.n} entries, got {numel}")
+        _check(lib().rmb_set_selection_weights(self._h, _ptr(w)))
+
+    def select_device(self, seed, sweep, weighted=False):
+        """The draws of application `sweep` from the solvers' device kernel (cuda int32 tensor)."""
+        import torch
+        out = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        _check(lib().rmb_select_device(self._h, seed, sweep, SELECT_WEIGHTED if weighted else SELECT_REPLACE,
+                                       _ptr(out)))
+        return out
 
     def last_launch_count(self):
         return int(lib().rmb_last_launch_count(self._h))
@@ -427,6 +456,27 @@ def partition(n, seed, sweep, identity=False):
     """Host-side partition generator: perm[p] = pi_sweep(p) (numpy uint32)."""
     out = np.empty(n, dtype=np.uint32)
     _check(lib().rmb_partition(n, seed, sweep, ORDER_IDENTITY if identity else 0, _ptr(out)))
+    return out
+
+
+def _select_flag(select):
+    if select is None:
+        return 0
+    if select == "replace":
+        return SELECT_REPLACE
+    if select == "weighted":
+        return SELECT_WEIGHTED
+    raise ValueError(f"select must be None, 'replace' or 'weighted', got {select!r}")
+
+
+def select(n, seed, sweep, weights=None):
+    """Host-side generator of application `sweep`'s n draws with replacement
+    (uniform, or P(s) ~ weights[s] for integer weights >= 1) -- R28-R29."""
+    out = np.empty(n, dtype=np.uint32)
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.uint32)
+    if w is not None and w.shape != (n,):
+        raise ValueError("weights must have n entries")
+    _check(lib().rmb_select(n, seed, sweep, _ptr(w), _ptr(out)))
     return out
 
 

@@ -105,6 +105,7 @@ static void free_problem(Problem* pr)
     pr->pistage.release();
     pr->aux.release();
     pr->rowrec.release();
+    pr->sel_buf.release();
     for (int q = 0; q < 8; ++q)
         if (pr->xpeer_open[q]) cudaIpcCloseMemHandle(pr->xpeer[q]);
     pr->xbuf.release();
@@ -152,6 +153,21 @@ static void apply_create_flags(Problem& pr, uint32_t flags)
 }
 
 static bool is_shard(const Problem& pr) { return pr.nccl_comm || pr.row_begin != 0 || pr.row_end != pr.n; }
+
+// RMB_SELECT_REPLACE / RMB_SELECT_WEIGHTED (readings
+// R28-R29): *sel = 0 (the partition), 1 (uniform draws) or 2 (weighted draws)
+static rmb_status selection_of(const Problem& pr, uint32_t flags, int* sel)
+{
+    *sel = (flags & RMB_SELECT_WEIGHTED) ? 2 : ((flags & RMB_SELECT_REPLACE) ? 1 : 0);
+    if (!*sel) return RMB_OK;
+    if (*sel == 2 && !pr.sel_cum)
+        return fail(RMB_ERR_INVALID_ARG, "RMB_SELECT_WEIGHTED: no weights set (rmb_set_selection_weights)");
+    if (flags & (RMB_ORDER_IDENTITY | RMB_CHUNKED_T))
+        return fail(RMB_ERR_INVALID_ARG, "draws with replacement exclude RMB_ORDER_IDENTITY and RMB_CHUNKED_T");
+    if (is_shard(pr) || (flags & RMB_FUSED))
+        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement are single-GPU (not for row-range handles)");
+    return RMB_OK;
+}
 
 static rmb_status solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t tl, long long* chg_dev,
                         int64_t cl, SolveResult* res)
@@ -227,6 +243,63 @@ static void fill_stats(rmb_stats* st, const SolveResult& r, rmb_status s)
     st->seconds = r.ms * 1e-3;
     st->converged = r.status == RMB_OK;
     st->status = s;
+}
+
+// MB-VI with draws with replacement (reading R30): the sweep residual r_k
+// covers only the drawn states, so r_k <= eps only triggers a confirmation:
+// ||TV - V||_inf over all states (the improvement pass, pi <- greedy(V));
+// the solve stops iff that is <= eps, else it resumes with the next sweep.
+// pi starts at 0 (states never drawn keep it until a confirmation pass).
+static rmb_status vi_with_replacement(Problem& pr, const SolveRequest& rq0, SolveResult* res)
+{
+    cudaError_t e = cudaMemsetAsync(rq0.pi, 0, (size_t)pr.n * 4, pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pi init");
+    double* trace = static_cast<double*>(pr.trace.p);
+    SolveResult tot;
+    tot.status = RMB_ERR_NOT_CONVERGED;
+    int64_t done = 0, launches = 0;
+    while (done < rq0.max_iter) {
+        SolveRequest rq = rq0;
+        rq.k0 = rq0.k0 + done;
+        rq.max_iter = rq0.max_iter - done;
+        SolveResult r;
+        rmb_status s = solve(pr, rq, trace + done, rq.max_iter, nullptr, 0, &r);
+        if (s != RMB_OK) return s;
+        done += r.sweeps;
+        tot.sweeps += r.sweeps;
+        tot.batches += r.batches;
+        tot.ms += r.ms;
+        tot.final_resid = r.final_resid;
+        launches += r.launches;
+        if (r.status != RMB_OK) {  // max_sweeps reached, or a non-finite value
+            tot.status = r.status;
+            break;
+        }
+        SolveRequest iq;
+        iq.mode = MODE_IMPROVE;
+        iq.b = pr.n;
+        iq.identity = true;
+        iq.V = rq0.V;
+        iq.pi = rq0.pi;
+        SolveResult ri;
+        s = solve(pr, iq, nullptr, 0, nullptr, 0, &ri);
+        if (s != RMB_OK) return s;
+        tot.ms += ri.ms;
+        launches += ri.launches;
+        tot.final_resid = ri.final_resid;
+        if (ri.status != RMB_OK) {
+            tot.status = ri.status;
+            break;
+        }
+        if (ri.final_resid <= rq0.eps) {
+            tot.status = RMB_OK;
+            break;
+        }
+    }
+    tot.launches = (int)launches;
+    pr.last_launches = launches;
+    *res = tot;
+    return RMB_OK;
 }
 
 }  // namespace rmb
@@ -371,11 +444,15 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     if (!(eps > 0.0) || !std::isfinite(eps)) return fail(RMB_ERR_INVALID_ARG, "eps must be finite and > 0");
     if (max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "max_sweeps < 1");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    int sel = 0;
+    rmb_status s = selection_of(pr, flags, &sel);
+    if (s != RMB_OK) return s;
     Staged sg;
-    rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, false, sg);
+    s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, false, sg);
     if (s != RMB_OK) return s;
     if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
+    rq.select = sel;
     rq.mode = MODE_VI;
     rq.b = b;
     rq.seed = seed;
@@ -404,13 +481,13 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
         fill_stats(stats, r, ret);
         return ret;
     }
-    s = solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
+    s = sel ? vi_with_replacement(pr, rq, &r) : solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
     if (s != RMB_OK) return s;
     s = stage_out(pr, V, pi, sg);
     if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.sweeps);
     if (s != RMB_OK) return s;
     rmb_status ret = (rmb_status)r.status;
-    if (ret == RMB_ERR_NOT_CONVERGED) g_err = "max_sweeps reached before r_k <= eps";
+    if (ret == RMB_ERR_NOT_CONVERGED) g_err = sel ? "max_sweeps reached before ||TV - V|| <= eps" : "max_sweeps reached before r_k <= eps";
     if (ret == RMB_ERR_NONFINITE) g_err = "a backup produced a non-finite value";
     fill_stats(stats, r, ret);
     return ret;
@@ -428,8 +505,11 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     if (max_outer < 1) return fail(RMB_ERR_INVALID_ARG, "max_outer < 1");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     const bool pi_given = flags & RMB_PI_GIVEN;
+    int sel = 0;
+    rmb_status s = selection_of(pr, flags, &sel);
+    if (s != RMB_OK) return s;
     Staged sg;
-    rmb_status s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
+    s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
     if (s != RMB_OK) return s;
     if (pi_given) {  // the given policy's owned entries must be actions in [0, A)
         s = check_policy(pr, sg.pi, pr.row_begin, pr.row_end);
@@ -440,6 +520,7 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
         return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.mode = MODE_MPI;
+    rq.select = sel;
     rq.b = b;
     rq.msweeps = m;
     rq.seed = seed;
@@ -493,6 +574,8 @@ static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint3
                               double* trace, int64_t tl, int64_t* changed, int64_t cl, rmb_stats* stats)
 {
     if (!hs || G < 1) return fail(RMB_ERR_INVALID_ARG, "handles NULL or G < 1");
+    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED))
+        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement are single-GPU (not for rmb_*_group)");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     std::vector<Problem*> rk((size_t)G);
     for (int g = 0; g < G; ++g) {
@@ -595,6 +678,11 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
     if (b < 1 || b > pr.n) return fail(RMB_ERR_INVALID_ARG, "b not in [1, n]");
     if (sweep < 1) return fail(RMB_ERR_INVALID_ARG, "sweep < 1");
     if (!V_in || !V_out) return fail(RMB_ERR_INVALID_ARG, "V_in or V_out is NULL");
+    int sel = 0;
+    {
+        rmb_status ss = selection_of(pr, flags, &sel);
+        if (ss != RMB_OK) return ss;
+    }
     const size_t vb = (size_t)pr.n * 8, pb = (size_t)pr.n * 4;
     cudaError_t e = cudaSuccess;
     // working V on device: V_out if device, else staging
@@ -628,6 +716,7 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
     if (pr.trace.ensure(64) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.mode = pi_or_null ? MODE_APPLY_PI : MODE_APPLY;
+    rq.select = sel;
     rq.b = b;
     rq.seed = seed;
     rq.k0 = sweep;
@@ -690,6 +779,8 @@ rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_
     if (!(eps > 0.0) || !std::isfinite(eps)) return fail(RMB_ERR_INVALID_ARG, "eps must be finite and > 0");
     if (max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "max_sweeps < 1");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
+    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED))
+        return fail(RMB_ERR_UNSUPPORTED, "rmb_policy_value: draws with replacement are not offered (its stop test is the sweep residual)");
     Staged sg;
     rmb_status s = stage_in(pr, V, const_cast<int32_t*>(pi), flags & RMB_V0_ZERO, true, sg);
     if (s != RMB_OK) return s;
@@ -731,6 +822,70 @@ rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags
     Permutation pm;
     pm.init(n, seed, sweep);
     for (int64_t p = 0; p < n; ++p) perm[p] = (uint32_t)pm((uint64_t)p);
+    return RMB_OK;
+}
+
+rmb_status rmb_set_selection_weights(rmb_problem h, const uint32_t* w)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (!w) {
+        pr.sel_cum = nullptr;
+        pr.sel_W = 0;
+        return RMB_OK;
+    }
+    const int64_t n = pr.n;
+    if (n > 0x7fffffffLL) return fail(RMB_ERR_UNSUPPORTED, "weighted selection needs n < 2^31");
+    std::vector<uint32_t> hw((size_t)n);
+    cudaError_t e = cudaMemcpy(hw.data(), w, (size_t)n * 4, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "read weights");
+    std::vector<uint64_t> cum((size_t)n);
+    uint64_t W = 0;
+    for (int64_t s = 0; s < n; ++s) {
+        if (hw[(size_t)s] == 0) return fail(RMB_ERR_INVALID_ARG, "a selection weight is 0 (every state needs w >= 1)");
+        W += hw[(size_t)s];
+        cum[(size_t)s] = W;
+    }
+    if (pr.sel_buf.ensure((size_t)n * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "weights allocation failed");
+    e = cudaMemcpyAsync(pr.sel_buf.p, cum.data(), (size_t)n * 8, cudaMemcpyHostToDevice, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "upload weights");
+    pr.sel_cum = static_cast<const uint64_t*>(pr.sel_buf.p);
+    pr.sel_W = W;
+    return RMB_OK;
+}
+
+rmb_status rmb_select(int64_t n, uint64_t seed, int64_t sweep, const uint32_t* w, uint32_t* sel)
+{
+    g_err.clear();
+    if (n < 1 || n > 0x7fffffffLL || !sel) return fail(RMB_ERR_INVALID_ARG, "n out of range or sel NULL");
+    std::vector<uint64_t> cum;
+    uint64_t W = 0;
+    if (w) {
+        cum.resize((size_t)n);
+        for (int64_t s = 0; s < n; ++s) {
+            if (w[s] == 0) return fail(RMB_ERR_INVALID_ARG, "a selection weight is 0");
+            W += w[s];
+            cum[(size_t)s] = W;
+        }
+    }
+    fill_order(n, seed, sweep, OrderSpec{w ? 2 : 1, w ? cum.data() : nullptr, W}, sel, 0, 1);
+    return RMB_OK;
+}
+
+rmb_status rmb_select_device(rmb_problem h, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* sel)
+{
+    g_err.clear();
+    if (!h || !sel) return fail(RMB_ERR_INVALID_ARG, "handle or sel is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    int s = 0;
+    rmb_status st = selection_of(pr, flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED), &s);
+    if (st != RMB_OK) return st;
+    if (!s) return fail(RMB_ERR_INVALID_ARG, "flags must hold RMB_SELECT_REPLACE or RMB_SELECT_WEIGHTED");
+    cudaError_t e = launch_select(pr.n, seed, sweep, s, pr.sel_cum, pr.sel_W, sel, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "rmb_select_device");
     return RMB_OK;
 }
 

@@ -57,6 +57,7 @@ struct ClusterArgs {
     double eps;     // < 0: no stopping test (single application)
     int64_t max_iter;
     uint32_t* perm; // 3 * n
+    OrderSpec order;  // permutation, or draws with replacement (R28-R29)
     double* trace;
     int64_t trace_len;
     long long* out;
@@ -125,12 +126,9 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         for (int s = 0; s < a.ring; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the first sweep's order: every CTA draws its share of the positions
-    if (!a.identity) {
-        Permutation pm;
-        pm.init(n, a.seed, a.k0);
-        uint32_t* dst = a.perm + (a.k0 % 3) * n;
-        for (int p = (int)q * kCThreads + t; p < n; p += (int)CS * kCThreads) dst[p] = (uint32_t)pm((uint64_t)p);
-    }
+    if (!a.identity)
+        fill_order(n, a.seed, a.k0, a.order, a.perm + (a.k0 % 3) * n, (int64_t)q * kCThreads + t,
+                   (int64_t)CS * kCThreads);
     cluster_sync();
 
     // ---- the row-job stream (identical on every CTA; each loads its own slab)
@@ -322,13 +320,9 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
                 ++consumed;
             }
             // next sweep's order, off the critical path (batch 0)
-            if (bi == 0 && !a.identity) {
-                Permutation pm2;
-                pm2.init(n, a.seed, k + 1);
-                uint32_t* dst = a.perm + ((k + 1) % 3) * n;
-                for (int p = (int)q * kCThreads + t; p < n; p += (int)CS * kCThreads)
-                    dst[p] = (uint32_t)pm2((uint64_t)p);
-            }
+            if (bi == 0 && !a.identity)
+                fill_order(n, a.seed, k + 1, a.order, a.perm + ((k + 1) % 3) * n, (int64_t)q * kCThreads + t,
+                           (int64_t)CS * kCThreads);
             mark(t_comp);
             cluster_sync();  // the batch's partials of every CTA are complete (and its reads of V done)
             mark(t_bar);
@@ -522,7 +516,8 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     a.b = (int)rq.b;
     a.seed = rq.seed;
     a.k0 = rq.k0;
-    a.identity = rq.identity ? 1 : 0;
+    a.identity = rq.identity && !rq.select ? 1 : 0;
+    a.order = OrderSpec{rq.select, pr.sel_cum, pr.sel_W};
     a.eval = eval ? 1 : 0;
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;

@@ -93,6 +93,7 @@ struct DenseArgs {
     int64_t imp_sub;     // improvement sub-batch (states)
     double* vnext;       // chunked T (VI*): new values of the sweep, applied at its end; null = B_b
     uint32_t* perm;      // 3 * n (triple-buffered by sweep index)
+    OrderSpec order;     // permutation, or draws with replacement (R28-R29)
     double* part;        // 2 * part_stride
     int64_t part_stride;
     double* lval;        // distributed-combine list: value per batch position
@@ -1312,14 +1313,9 @@ __device__ void run_batch(const DenseArgs& a, Ctx& x, double* Vs, int32_t* pis, 
         compute_phase_tma<PT, EVAL, is_vgl(CTA)>(a, Vs, pl, part, x.tm, x.tst, x.tph);
     else
         compute_phase<PT, VE, EVAL, kAG>(a, Vs, pis, perm, lo, cnt, pl, part, a.wctr + (x.phase & 1));
-    if (fill_next_k > 0) {  // next sweep's order, off the critical path
-        Permutation pm;
-        pm.init(a.n, a.seed, fill_next_k);
-        uint32_t* dst = a.perm + (fill_next_k % 3) * a.n;
-        const int64_t stride = (int64_t)a.nctas * kThreads;
-        for (int64_t p = (int64_t)cta_rank(a) * kThreads + threadIdx.x; p < a.n; p += stride)
-            dst[p] = (uint32_t)pm((uint64_t)p);
-    }
+    if (fill_next_k > 0)  // next sweep's order, off the critical path
+        fill_order(a.n, a.seed, fill_next_k, a.order, a.perm + (fill_next_k % 3) * a.n,
+                   (int64_t)cta_rank(a) * kThreads + threadIdx.x, (int64_t)a.nctas * kThreads);
     constexpr bool fused = is_fused(CTA) && KIND <= 1;
     if constexpr (fused) {
         if (cta_rank(a) == 0 && threadIdx.x == 0) a.xcnt[(x.batches + 2) % 3] = 0u;  // slot of batch sb - 1
@@ -1579,13 +1575,9 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
         }
     }
     if (cta_rank(a) == 0 && threadIdx.x == 0) x.t_mark = globaltimer_ns();
-    if (!a.identity && a.mode != MODE_IMPROVE && !shard) {
-        Permutation pm;
-        pm.init(a.n, a.seed, a.k0);
-        uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
-        for (int64_t p = (int64_t)cta_rank(a) * kThreads + threadIdx.x; p < a.n; p += (int64_t)a.nctas * kThreads)
-            dst[p] = (uint32_t)pm((uint64_t)p);
-    }
+    if (!a.identity && a.mode != MODE_IMPROVE && !shard)
+        fill_order(a.n, a.seed, a.k0, a.order, a.perm + (a.k0 % 3) * a.n,
+                   (int64_t)cta_rank(a) * kThreads + threadIdx.x, (int64_t)a.nctas * kThreads);
     timed_sync(x);  // perm of the first sweep visible; also orders the smem loads
     if (is_fused(CTA) && a.mode != MODE_IMPROVE) {  // fused: this rank's states of the first sweep batch
         build_own_list(a, a.identity ? nullptr : a.perm + (a.k0 % 3) * a.n, 0, min(a.b, a.n), 0);
@@ -1828,8 +1820,10 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     a.seed = rq.seed;
     a.k0 = rq.k0;
     // b >= n: one batch per sweep, whose result does not depend on the order
-    // of its states -> no permutation needed
-    a.identity = (rq.identity || rq.b >= n) ? 1 : 0;
+    // of its states -> no permutation needed (draws with replacement are not
+    // a permutation: they always need the order array)
+    a.identity = rq.select ? 0 : ((rq.identity || rq.b >= n) ? 1 : 0);
+    a.order = OrderSpec{rq.select, pr.sel_cum, pr.sel_W};
     a.mode = rq.mode;
     a.pi_given = rq.pi_given ? 1 : 0;
     a.eps = rq.eps;

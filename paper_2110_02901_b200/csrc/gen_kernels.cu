@@ -25,6 +25,20 @@ cudaError_t launch_partition(int64_t n, uint64_t seed, int64_t sweep, bool ident
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- selection
+__global__ void select_kernel(int64_t n, uint64_t seed, int64_t sweep, OrderSpec os, uint32_t* sel)
+{
+    fill_order(n, seed, sweep, os, sel, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+cudaError_t launch_select(int64_t n, uint64_t seed, int64_t sweep, int sel, const uint64_t* cum, uint64_t W,
+                          uint32_t* out, cudaStream_t st)
+{
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    select_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, seed, sweep, OrderSpec{sel, cum, W}, out);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- dense gen
 // one warp per (s, a) row: exact integer row sum, then the normalised row
 template <typename T>

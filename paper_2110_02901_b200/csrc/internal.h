@@ -43,6 +43,7 @@ struct SolveRequest {
     bool identity = false;   // RMB_ORDER_IDENTITY
     bool chunked = false;    // RMB_CHUNKED_T: VI* (T in chunks of b against the sweep-start values)
     bool fused = false;      // RMB_FUSED: multi-rank solve with the in-kernel peer-memory exchange
+    int select = 0;          // 0: partition (R2); 1 / 2: draws with replacement, uniform / weighted (R28-R29)
     double eps = -1.0;       // < 0: no convergence test
     int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
     int msweeps = 1;         // MPI evaluation sweeps per outer iteration
@@ -121,6 +122,11 @@ struct Problem {
     bool no_tma = false;  // dense: RMB_DENSE_NO_TMA (register-streaming warp path)
     bool vglobal = false; // dense: RMB_DENSE_VGLOBAL (V and pi in global memory)
     bool no_cluster = false;  // dense: RMB_DENSE_NO_CLUSTER (tiny batches on the grid solver too)
+    // weighted selection (rmb_set_selection_weights): inclusive prefix sums of
+    // the integer weights (device [n]) and their total; null = none set
+    DevBuf sel_buf;
+    const uint64_t* sel_cum = nullptr;
+    uint64_t sel_W = 0;
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 0;
@@ -164,6 +170,8 @@ rmb_status sparse_shard_step(Problem& pr, const SolveRequest& rq, const uint32_t
 // gen_kernels.cu
 cudaError_t launch_partition(int64_t n, uint64_t seed, int64_t sweep, bool identity, uint32_t* perm,
                              cudaStream_t st);
+cudaError_t launch_select(int64_t n, uint64_t seed, int64_t sweep, int sel, const uint64_t* cum, uint64_t W,
+                          uint32_t* out, cudaStream_t st);
 cudaError_t launch_validate(const Problem& pr, int* bad_dev, cudaStream_t st);
 cudaError_t launch_check_policy(const int32_t* pi, int64_t lo, int64_t hi, int A, int* bad, cudaStream_t st);
 

@@ -93,4 +93,79 @@ struct Permutation {
     }
 };
 
+// State selection WITH replacement (DESIGN
+// readings R28-R29): application k draws n states i.i.d.,
+//   skey_k = mix64(key_k ^ 0x5E1EC7105E1EC710),  u_i = mix64(skey_k + i),
+//   uniform:  s_i = floor(u_i * n / 2^64);
+//   weighted: t_i = floor(u_i * W / 2^64), s_i = first s with cum[s] > t_i
+//             (cum = inclusive prefix sums of integer weights w_s >= 1, W = cum[n-1]).
+// Integer arithmetic only, so every side draws the same states.
+RMB_HD uint64_t mulhi_u64(uint64_t a, uint64_t b)
+{
+#if defined(__CUDA_ARCH__)
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * (unsigned __int128)b) >> 64);
+#endif
+}
+
+struct Selection {
+    uint64_t skey;
+    uint64_t n;
+    const uint64_t* cum;  // null: uniform
+    uint64_t W;
+
+    RMB_HD void init(int64_t n_, uint64_t seed, int64_t sweep, const uint64_t* cum_, uint64_t W_)
+    {
+        n = (uint64_t)n_;
+        const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)sweep);
+        skey = splitmix64(key ^ 0x5E1EC7105E1EC710ULL);
+        cum = cum_;
+        W = W_;
+    }
+
+    // the state of draw i
+    RMB_HD uint32_t operator()(uint64_t i) const
+    {
+        const uint64_t u = splitmix64(skey + i);
+        if (!cum) return (uint32_t)mulhi_u64(u, n);
+        const uint64_t t = mulhi_u64(u, W);
+        uint64_t lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const uint64_t mid = lo + ((hi - lo) >> 1);
+#if defined(__CUDA_ARCH__)
+            const uint64_t cm = __ldg(cum + mid);
+#else
+            const uint64_t cm = cum[mid];
+#endif
+            if (cm > t) hi = mid;
+            else lo = mid + 1;
+        }
+        return (uint32_t)lo;
+    }
+};
+
+// The processing order of operator application k, as the solvers store it
+// (one entry per position): the permutation (sel == 0) or the draws
+// (sel == 1 uniform, 2 weighted).  Threads tid, tid + stride, ... fill dst.
+struct OrderSpec {
+    int sel;
+    const uint64_t* cum;
+    uint64_t W;
+};
+
+RMB_HD void fill_order(int64_t n, uint64_t seed, int64_t k, const OrderSpec& os, uint32_t* dst, int64_t tid,
+                       int64_t stride)
+{
+    if (os.sel) {
+        Selection sl;
+        sl.init(n, seed, k, os.sel == 2 ? os.cum : nullptr, os.W);
+        for (int64_t p = tid; p < n; p += stride) dst[p] = sl((uint64_t)p);
+    } else {
+        Permutation pm;
+        pm.init(n, seed, k);
+        for (int64_t p = tid; p < n; p += stride) dst[p] = (uint32_t)pm((uint64_t)p);
+    }
+}
+
 }  // namespace rmb

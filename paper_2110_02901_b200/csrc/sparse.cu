@@ -74,6 +74,11 @@ struct SparseArgs {
     int msweeps;
     int chunked;     // RMB_CHUNKED_T (VI*): every batch reads the sweep-start values
     uint32_t* perm;  // 3 * n
+    OrderSpec order;  // permutation, or draws with replacement (R28-R29)
+    // draws with replacement: mark[(g & 1) * n + s] == g iff s is drawn in
+    // global batch g (written during batch g - 1) -- decides which carried /
+    // re-copied values a batch's own new values supersede
+    uint32_t* mark;
     unsigned long long* bar;
     int* err;
     unsigned long long* red;  // [4] residual bits ring, [4..8) nonfinite ring, [8..12) changed ring
@@ -444,6 +449,19 @@ __device__ __forceinline__ SweepResult read_slot(const SparseArgs& a, int slot)
     return s;
 }
 
+// Draws with replacement: mark the states of global batch g (= positions
+// [lo, lo + b) of application k's draws), recomputed from the counter-based
+// draw law so the order array need not be visible yet.
+__device__ __forceinline__ void mark_batch(const SparseArgs& a, int64_t k, int64_t lo, int64_t g)
+{
+    Selection sl;
+    sl.init(a.n, a.seed, k, a.order.sel == 2 ? a.order.cum : nullptr, a.order.W);
+    const int64_t cnt = min(a.b, a.n - lo);
+    uint32_t* mk = a.mark + (size_t)(g & 1) * a.n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        mk[sl((uint64_t)(lo + i))] = (uint32_t)g;
+}
+
 // Position of a lane group's item in the batch stream: batch start lo, the
 // warp's position w0 in the batch, and the sweep offset (0 = this sweep,
 // 1 = the next one).
@@ -491,7 +509,10 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
         atomicExch(a.red + 4 + z, 0ull);
         atomicExch(a.red + 8 + z, 0ull);
     }
-    const bool single = b >= n;  // one batch per sweep: every state rewritten each batch
+    // one batch per sweep: every state rewritten each batch (not with draws
+    // with replacement: undrawn states keep their values through the copies)
+    const bool sel = a.order.sel != 0;
+    const bool single = b >= n && !sel;
     // chunked T (VI*): every chunk reads X_cur = the sweep-start
     // values and writes X_next; no re-copies, X flips once per sweep
     const bool chunked = !EVAL && a.chunked && !single;
@@ -553,7 +574,9 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
             // batch of a sweep the state may belong to this batch too: then it
             // gets this batch's new value and the old one is not stored.
             bool skip = false;
-            if (lo == 0) {
+            if (sel) {
+                skip = __ldcg(a.mark + (size_t)(x.gb & 1) * n + x.cs) == (uint32_t)x.gb;
+            } else if (lo == 0) {
                 if (a.identity) {
                     skip = x.cs < cnt;
                 } else {
@@ -599,26 +622,25 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
         // so their copy is skipped (membership through the inverse permutation).
         if (x.prev_valid && !single && !carry) {
             Permutation pk;
-            if (lo == 0 && !a.identity) pk.init(a.n, a.seed, k);
+            if (lo == 0 && !a.identity && !sel) pk.init(a.n, a.seed, k);
             const int stride = (int)(gridDim.x * blockDim.x);
             for (int i = (int)(blockIdx.x * blockDim.x + threadIdx.x); i < x.prev_cnt; i += stride) {
                 const int s = x.prev_perm ? ld_keep(reinterpret_cast<const int*>(x.prev_perm) + x.prev_lo + i, pf)
                                           : x.prev_lo + i;
-                if (lo == 0) {
+                if (sel) {
+                    if (__ldcg(a.mark + (size_t)(x.gb & 1) * n + s) == (uint32_t)x.gb) continue;
+                } else if (lo == 0) {
                     const int64_t pos = a.identity ? s : (int64_t)pk.position((uint64_t)s);
                     if (pos < cnt) continue;
                 }
                 st_keep(Xn + s, ld_keep(Xc + s, pl), pl);
             }
         }
-        if (lo == 0 && !a.identity) {  // next sweep's order, off the critical path
-            Permutation pm;
-            pm.init(a.n, a.seed, k + 1);
-            uint32_t* dst = a.perm + ((k + 1) % 3) * a.n;
-            const int stride = (int)(gridDim.x * blockDim.x);
-            for (int p = (int)(blockIdx.x * blockDim.x + threadIdx.x); p < n; p += stride)
-                dst[p] = (uint32_t)pm((uint64_t)p);
-        }
+        if (lo == 0 && !a.identity)  // next sweep's order, off the critical path
+            fill_order(a.n, a.seed, k + 1, a.order, a.perm + ((k + 1) % 3) * a.n,
+                       (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+        if (sel)  // marks of the next batch (this sweep's next, or the next sweep's first)
+            mark_batch(a, lo + b < n ? k : k + 1, lo + b < n ? lo + b : 0, x.gb + 1);
         const bool last = lo + b >= n;
         if (last) cta_publish(a, slot, rmax, bad, 0);
         s_prof(SP_COMP);
@@ -744,12 +766,8 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
         a.X1[s] = v;
         if (KIND != SK_MIN) a.pw0[s] = a.pi[s];
     }
-    if (!a.identity && KIND != SK_IMPROVE) {
-        Permutation pm;
-        pm.init(a.n, a.seed, a.k0);
-        uint32_t* dst = a.perm + (a.k0 % 3) * a.n;
-        for (int p = tid; p < n; p += stride) dst[p] = (uint32_t)pm((uint64_t)p);
-    }
+    if (!a.identity && KIND != SK_IMPROVE) fill_order(a.n, a.seed, a.k0, a.order, a.perm + (a.k0 % 3) * a.n, tid, stride);
+    if (a.order.sel && KIND != SK_IMPROVE) mark_batch(a, a.k0, 0, 0);
     grid_sync(x.g);
 
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -904,7 +922,8 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.b = rq.b;
     a.seed = rq.seed;
     a.k0 = rq.k0;
-    a.identity = rq.identity ? 1 : 0;
+    a.identity = rq.identity && !rq.select ? 1 : 0;
+    a.order = OrderSpec{rq.select, pr.sel_cum, pr.sel_W};
     a.mode = rq.mode;
     a.pi_given = rq.pi_given ? 1 : 0;
     a.eps = rq.eps;
@@ -917,7 +936,9 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.GSE = GSE;
 
     cudaStream_t st = pr.stream;
-    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.part.ensure((size_t)2 * n * 8 + (size_t)2 * n * 4 + 256) != cudaSuccess ||
+    const size_t xbytes = (size_t)2 * n * 8 + (size_t)2 * n * 4 + 256;
+    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess ||
+        pr.part.ensure(xbytes + (rq.select ? (size_t)2 * n * 4 : 0)) != cudaSuccess ||
         pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("sparse solver: workspace allocation failed");
         return RMB_ERR_OOM;
@@ -927,6 +948,7 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.X1 = a.X0 + n;
     a.pw0 = reinterpret_cast<int32_t*>(a.X1 + n);
     a.pw1 = a.pw0 + n;
+    a.mark = rq.select ? reinterpret_cast<uint32_t*>(static_cast<char*>(pr.part.p) + xbytes) : nullptr;
     unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
     a.bar = ctrl;
     a.err = reinterpret_cast<int*>(ctrl + 64);
@@ -942,6 +964,9 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    // marks are batch numbers of THIS launch: clear the previous launch's
+    // (0xFFFFFFFF never equals a batch number of a launch)
+    if (ce == cudaSuccess && a.mark) ce = cudaMemsetAsync(a.mark, 0xFF, (size_t)2 * n * 4, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
     // row mode: repack the rows into records (inside the timed region: part of the solve)
     a.rec = nullptr;

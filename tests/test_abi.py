@@ -62,3 +62,18 @@ def test_argument_errors_before_device_work():
     assert L.rmb_create_dense(ctypes.byref(d), buf.ctypes.data, buf.ctypes.data, 0, ctypes.byref(h)) == rmb.INVALID_ARG
     assert L.rmb_partition(0, 0, 1, 0, None) == rmb.INVALID_ARG
     assert L.rmb_vi(None, 1, 0, 1e-6, 10, 0, None, None, None, None) == rmb.INVALID_ARG
+
+
+@pytest.mark.parametrize("n,seed,k", [(1, 0, 1), (17, 3, 2), (1000, 9, 5), (65_537, 2**40 + 1, 77)])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_host_select_matches_oracle(n, seed, k, weighted):
+    """The product's host draw generator (partition.cuh Selection, R28-R29) is
+    bitwise the oracle's independent implementation."""
+    import oracle
+    w = np.random.default_rng(n).integers(1, 2**32, size=n, dtype=np.uint64).astype(np.uint32) if weighted else None
+    assert np.array_equal(rmb.select(n, seed, k, w), oracle.select(n, seed, k, w))
+
+
+def test_host_select_rejects_zero_weight():
+    with pytest.raises(rmb.RmbError):
+        rmb.select(3, 1, 1, np.array([1, 0, 2], np.uint32))
