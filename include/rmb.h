@@ -103,6 +103,17 @@ typedef struct {
                                        the handle's integer weights (rmb_set_selection_weights; DESIGN
                                        R29: inverse CDF on integer prefix sums).  Importance-sampling and
                                        epsilon-greedy laws are choices of w.                             */
+#define RMB_ASYNC 0x8000u /* rmb_vi / rmb_mpi / rmb_apply / rmb_policy_value: ASYNCHRONOUS applications
+                             ("asynchronous variants of MB-VI and MB-MPI ...
+                             avoiding synchronization"; DESIGN R31): every application walks the
+                             states in the order of its partition with no batch barrier -- each
+                             state is backed up against V as found in memory (every value read is
+                             one its state held since the application began) and written at once;
+                             one grid barrier per application (residual, stop test).  b is not used
+                             (pass any value in [1, n]).  Results are NOT deterministic: for V0 with
+                             T V0 <= V0 every iterate lies between J* and the Bellman iterate T^k V0.
+                             MB-MPI: asynchronous evaluation sweeps, synchronous improvement.
+                             Single-GPU; excludes RMB_CHUNKED_T and RMB_SELECT_*.                */
 /* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly

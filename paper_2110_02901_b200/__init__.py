@@ -29,7 +29,7 @@ F32, F64 = 0, 1
 ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 CHUNKED_T = 0x40
 SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED, DENSE_NO_CLUSTER = 0x80, 0x400, 0x800, 0x1000
-SELECT_REPLACE, SELECT_WEIGHTED = 0x2000, 0x4000
+SELECT_REPLACE, SELECT_WEIGHTED, ASYNC = 0x2000, 0x4000, 0x8000
 
 _lib = None
 
@@ -272,23 +272,24 @@ class Problem:
         return _vec(V, self.n, "f64", "V"), _vec(pi, self.n, "i32", "pi")
 
     def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-           device="cuda", chunked=False, fused=False, select=None):
+           device="cuda", chunked=False, fused=False, select=None, asynchronous=False):
         """MB-VI: V, pi updated in place (torch cuda/cpu or numpy).
         chunked=True: VI* -- every sweep is T computed in chunks of b
         states against the sweep-start values (RMB_CHUNKED_T).
         select="replace" / "weighted": every sweep draws n states with
-        replacement, uniformly / by the weights of set_selection_weights (R28-R30)."""
+        replacement, uniformly / by the weights of set_selection_weights (R28-R30).
+        asynchronous=True: RMB_ASYNC (R31) -- no batch barrier, b unused."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_sweeps)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
-                 | (FUSED if fused else 0) | _select_flag(select))
+                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0))
         s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         return Solution(V, pi, tr[: st.sweeps], s, st)
 
     def mpi(self, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
-            v0_zero=False, device="cuda", fused=False, select=None):
+            v0_zero=False, device="cuda", fused=False, select=None, asynchronous=False):
         """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start
         (select: evaluation sweeps draw with replacement, as vi())."""
         V, pi = self._vp(V, pi, device)
@@ -296,7 +297,7 @@ class Problem:
         ch = np.zeros(max_outer, dtype=np.int64)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
-                 | (FUSED if fused else 0) | _select_flag(select))
+                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0))
         s = lib().rmb_mpi(self._h, b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi), _ptr(tr), _ptr(ch),
                           ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
@@ -304,7 +305,7 @@ class Problem:
         return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
 
     def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False, chunked=False,
-              select=None):
+              select=None, asynchronous=False):
         """One application of B_b (pi None) or B_{pi,b}: returns (V_out, argmin, residual)."""
         import torch
         _vec(V_in, self.n, "f64", "V_in")
@@ -317,14 +318,15 @@ class Problem:
                       if not isinstance(V_out, np.ndarray) else np.empty(self.n, np.int32))
         _vec(argmin, self.n, "i32", "argmin")
         r = ctypes.c_double()
-        flags = (ORDER_IDENTITY if identity else 0) | (CHUNKED_T if chunked else 0) | _select_flag(select)
+        flags = ((ORDER_IDENTITY if identity else 0) | (CHUNKED_T if chunked else 0) | _select_flag(select)
+                 | (ASYNC if asynchronous else 0))
         s = lib().rmb_apply(self._h, b, seed, sweep, flags, _ptr(pi), _ptr(V_in),
                             _ptr(V_out), _ptr(argmin), ctypes.byref(r))
         _check(s, (OK, NONFINITE))
         return V_out, argmin, r.value
 
     def policy_value(self, pi, b=None, seed=0, eps=1e-10, max_sweeps=1_000_000, V=None, v0_zero=True,
-                     identity=False, device="cuda"):
+                     identity=False, device="cuda", asynchronous=False):
         """J_pi by B_{pi,b} iteration to ||V_k - V_{k-1}|| <= eps (Eq. 4 / Lemma 4)."""
         import torch
         V = torch.zeros(self.n, dtype=torch.float64, device=device) if V is None else V
@@ -332,7 +334,7 @@ class Problem:
         _vec(pi, self.n, "i32", "pi")
         tr = np.zeros(min(max_sweeps, 1 << 20))
         st = Stats()
-        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0)
+        flags = (ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (ASYNC if asynchronous else 0)
         s = lib().rmb_policy_value(self._h, _ptr(pi), self.n if b is None else b, seed, eps, max_sweeps, flags,
                                    _ptr(V), _ptr(tr) if max_sweeps <= len(tr) else None, ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))

@@ -154,6 +154,18 @@ static void apply_create_flags(Problem& pr, uint32_t flags)
 
 static bool is_shard(const Problem& pr) { return pr.nccl_comm || pr.row_begin != 0 || pr.row_end != pr.n; }
 
+// RMB_ASYNC (reading R31): single-GPU, partition order only
+static rmb_status async_of(const Problem& pr, uint32_t flags, bool* as)
+{
+    *as = (flags & RMB_ASYNC) != 0;
+    if (!*as) return RMB_OK;
+    if (flags & (RMB_CHUNKED_T | RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED))
+        return fail(RMB_ERR_INVALID_ARG, "RMB_ASYNC excludes RMB_CHUNKED_T and the RMB_SELECT_* draws");
+    if (is_shard(pr) || (flags & RMB_FUSED))
+        return fail(RMB_ERR_UNSUPPORTED, "RMB_ASYNC is single-GPU (not for row-range handles)");
+    return RMB_OK;
+}
+
 // RMB_SELECT_REPLACE / RMB_SELECT_WEIGHTED (readings
 // R28-R29): *sel = 0 (the partition), 1 (uniform draws) or 2 (weighted draws)
 static rmb_status selection_of(const Problem& pr, uint32_t flags, int* sel)
@@ -175,6 +187,7 @@ static rmb_status solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     if (is_shard(pr))
         return fail(RMB_ERR_INVALID_ARG, "this handle owns a row range: use rmb_vi / rmb_mpi with an NCCL "
                                          "communicator, or rmb_vi_group / rmb_mpi_group");
+    if (rq.async && pr.dense) return dense_async_solve(pr, rq, trace_dev, tl, chg_dev, cl, res);
     return pr.dense ? dense_solve(pr, rq, trace_dev, tl, chg_dev, cl, res)
                     : sparse_solve(pr, rq, trace_dev, tl, chg_dev, cl, res);
 }
@@ -445,7 +458,9 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     if (max_sweeps < 1) return fail(RMB_ERR_INVALID_ARG, "max_sweeps < 1");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     int sel = 0;
+    bool as = false;
     rmb_status s = selection_of(pr, flags, &sel);
+    if (s == RMB_OK) s = async_of(pr, flags, &as);
     if (s != RMB_OK) return s;
     Staged sg;
     s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, false, sg);
@@ -453,6 +468,7 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.select = sel;
+    rq.async = as;
     rq.mode = MODE_VI;
     rq.b = b;
     rq.seed = seed;
@@ -506,7 +522,9 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     const bool pi_given = flags & RMB_PI_GIVEN;
     int sel = 0;
+    bool as = false;
     rmb_status s = selection_of(pr, flags, &sel);
+    if (s == RMB_OK) s = async_of(pr, flags, &as);
     if (s != RMB_OK) return s;
     Staged sg;
     s = stage_in(pr, V, pi, flags & RMB_V0_ZERO, pi_given, sg);
@@ -521,6 +539,7 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     SolveRequest rq;
     rq.mode = MODE_MPI;
     rq.select = sel;
+    rq.async = as;
     rq.b = b;
     rq.msweeps = m;
     rq.seed = seed;
@@ -574,8 +593,8 @@ static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint3
                               double* trace, int64_t tl, int64_t* changed, int64_t cl, rmb_stats* stats)
 {
     if (!hs || G < 1) return fail(RMB_ERR_INVALID_ARG, "handles NULL or G < 1");
-    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED))
-        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement are single-GPU (not for rmb_*_group)");
+    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED | RMB_ASYNC))
+        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement and RMB_ASYNC are single-GPU (not for rmb_*_group)");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     std::vector<Problem*> rk((size_t)G);
     for (int g = 0; g < G; ++g) {
@@ -679,8 +698,10 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
     if (sweep < 1) return fail(RMB_ERR_INVALID_ARG, "sweep < 1");
     if (!V_in || !V_out) return fail(RMB_ERR_INVALID_ARG, "V_in or V_out is NULL");
     int sel = 0;
+    bool as = false;
     {
         rmb_status ss = selection_of(pr, flags, &sel);
+        if (ss == RMB_OK) ss = async_of(pr, flags, &as);
         if (ss != RMB_OK) return ss;
     }
     const size_t vb = (size_t)pr.n * 8, pb = (size_t)pr.n * 4;
@@ -717,6 +738,7 @@ rmb_status rmb_apply(rmb_problem h, int64_t b, uint64_t seed, int64_t sweep, uin
     SolveRequest rq;
     rq.mode = pi_or_null ? MODE_APPLY_PI : MODE_APPLY;
     rq.select = sel;
+    rq.async = as;
     rq.b = b;
     rq.seed = seed;
     rq.k0 = sweep;
@@ -781,14 +803,18 @@ rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED))
         return fail(RMB_ERR_UNSUPPORTED, "rmb_policy_value: draws with replacement are not offered (its stop test is the sweep residual)");
+    bool as = false;
+    rmb_status s = async_of(pr, flags, &as);
+    if (s != RMB_OK) return s;
     Staged sg;
-    rmb_status s = stage_in(pr, V, const_cast<int32_t*>(pi), flags & RMB_V0_ZERO, true, sg);
+    s = stage_in(pr, V, const_cast<int32_t*>(pi), flags & RMB_V0_ZERO, true, sg);
     if (s != RMB_OK) return s;
     s = check_policy(pr, sg.pi, 0, pr.n);
     if (s != RMB_OK) return s;
     if (pr.trace.ensure((size_t)max_sweeps * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "trace allocation failed");
     SolveRequest rq;
     rq.mode = MODE_POLICY_VALUE;
+    rq.async = as;
     rq.b = b;
     rq.seed = seed;
     rq.k0 = 1;

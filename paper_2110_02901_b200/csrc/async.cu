@@ -1,0 +1,430 @@
+// async.cu — asynchronous MB-VI / MB-MPI on DENSE MDPs (SURVEY 8(f) row 4,
+// "asynchronous variants of MB-VI and MB-MPI, which hold the
+// promise of further speedup by avoiding synchronization", citing Tsitsiklis
+// & Bertsekas' asynchronous DP).  DESIGN reading R31:
+//
+//   each operator application k walks the states in the order of its
+//   partition (R2) with NO batch barrier: a CTA takes the next position from
+//   a counter, backs its state up against V as it is in memory at that moment
+//   (values written earlier in this application by any CTA may or may not be
+//   seen -- every value read is one the state held since the application
+//   started) and writes V(s) at once.  One grid barrier per application
+//   (residual, stopping test, the next order).  The result is not
+//   deterministic; it is pinned by properties that hold for every
+//   interleaving (tests/test_gpu_async.py, test_oracle_async.py).
+//
+// One state per CTA: its A rows (all n columns) stream through registers
+// (16-byte loads, L1 bypassed, L2 evict_first), each V vector is loaded once
+// from L2 (.cg: the coherence point, never a stale L1 line) and used for AG
+// rows; the CTA reduces the partial sums in a fixed order (thread columns ->
+// warp butterfly -> warps in order) and takes the min over actions (lowest
+// index on ties, R8).  MPI: evaluation sweeps are asynchronous B_{pi} sweeps,
+// the improvement is an ordinary synchronous pass (no V write).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+#include "partition.cuh"
+
+namespace rmb {
+
+namespace {
+
+constexpr int kAThreads = 512;
+constexpr int kAWarps = kAThreads / 32;
+
+struct AsyncArgs {
+    const void* P;
+    const void* c;
+    int64_t n;
+    int A;
+    double gamma;
+    double* V;
+    int32_t* pi;
+    uint64_t seed;
+    int64_t k0;
+    int identity;
+    int mode;
+    int pi_given;
+    double eps;
+    int64_t max_iter;
+    int msweeps;
+    uint32_t* perm;           // 3 * n
+    unsigned long long* bar;  // grid barrier words
+    int* err;
+    unsigned int* ctr;        // [4] position counters (application parity, improvement)
+    unsigned long long* red;  // [4 slots x 4]: residual bits, bad, changed
+    double* trace;
+    int64_t trace_len;
+    long long* chg;
+    int64_t chg_len;
+    long long* out;
+};
+
+template <typename PT>
+__device__ __forceinline__ double cost_at(const AsyncArgs& a, int64_t r)
+{
+    return (double)__ldg(static_cast<const PT*>(a.c) + r);
+}
+
+// V(j .. j+VE) from L2 (values written by other CTAs during the application)
+template <int VE>
+__device__ __forceinline__ void ld_v(const double* V, int64_t j, double (&v)[VE])
+{
+    if constexpr (VE == 4) {
+        const double2 x = __ldcg(reinterpret_cast<const double2*>(V + j));
+        const double2 y = __ldcg(reinterpret_cast<const double2*>(V + j + 2));
+        v[0] = x.x, v[1] = x.y, v[2] = y.x, v[3] = y.y;
+    } else if constexpr (VE == 2) {
+        const double2 x = __ldcg(reinterpret_cast<const double2*>(V + j));
+        v[0] = x.x, v[1] = x.y;
+    } else {
+        v[0] = __ldcg(V + j);
+    }
+}
+
+// raw P vectors (converted to double inside the FMA loop: fewer registers)
+template <typename PT, int VE>
+struct PVec {
+    PT x[VE];
+};
+template <typename PT, int VE>
+__device__ __forceinline__ PVec<PT, VE> ld_p(const PT* p, uint64_t pol)
+{
+    PVec<PT, VE> r;
+    if constexpr (VE == 4) {
+        const float4 q = ld_first(reinterpret_cast<const float4*>(p), pol);
+        r.x[0] = q.x, r.x[1] = q.y, r.x[2] = q.z, r.x[3] = q.w;
+    } else if constexpr (VE == 2) {
+        const double2 q = ld_first(reinterpret_cast<const double2*>(p), pol);
+        r.x[0] = q.x, r.x[1] = q.y;
+    } else {
+        r.x[0] = ld_first(p, pol);
+    }
+    return r;
+}
+
+// Q(s, a) for the rows rows[0 .. na) of state s (all n columns) into Qs[slot[r]].
+// Every thread of the CTA calls it; ends with the CTA synchronised.
+template <typename PT, int VE, int AG>
+__device__ __forceinline__ void state_rows(const AsyncArgs& a, int64_t s, const int* rows, int na, double* red,
+                                           double* Qs, uint64_t pol)
+{
+    const PT* P = static_cast<const PT*>(a.P);
+    const int64_t n = a.n;
+    double acc[AG];
+#pragma unroll
+    for (int r = 0; r < AG; ++r) acc[r] = 0.0;
+    // the rows of one call are consecutive actions (min) or the single row pi(s)
+    const PT* base = P + ((int64_t)s * a.A + rows[0]) * n;
+    for (int64_t j = (int64_t)threadIdx.x * VE; j < n; j += (int64_t)kAThreads * VE) {
+        PVec<PT, VE> x[AG];
+#pragma unroll
+        for (int r = 0; r < AG; ++r)
+            if (r < na) x[r] = ld_p<PT, VE>(base + (int64_t)r * n + j, pol);
+        double v[VE];
+        ld_v<VE>(a.V, j, v);
+#pragma unroll
+        for (int r = 0; r < AG; ++r)
+            if (r < na) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) acc[r] = fma((double)x[r].x[e], v[e], acc[r]);
+            }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < AG; ++r) {
+        if (r < na) {
+            double t = acc[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) red[warp * AG + r] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < na) {
+        const int r = threadIdx.x;
+        double t = 0.0;
+        for (int w = 0; w < kAWarps; ++w) t += red[w * AG + r];
+        Qs[r] = cost_at<PT>(a, (int64_t)s * a.A + rows[r]) + a.gamma * t;
+    }
+    __syncthreads();
+}
+
+struct AAcc {
+    double rmax;
+    int bad;
+    long long changed;
+};
+
+// publish a CTA's accumulator into reduction slot q (thread 0 only)
+__device__ __forceinline__ void publish(const AsyncArgs& a, int q, const AAcc& acc)
+{
+    unsigned long long* slot = a.red + 4 * (q & 3);
+    atomicMax(slot, (unsigned long long)__double_as_longlong(acc.rmax));
+    if (acc.bad) atomicOr(slot + 1, 1ull);
+    if (acc.changed) atomicAdd(slot + 2, (unsigned long long)acc.changed);
+}
+
+// One pass over the states: KIND 0 = asynchronous B (min), 1 = asynchronous
+// B_pi, 2 = improvement (greedy vs V, pi written, no V write; identity order).
+// Positions are dealt dynamically, one state per CTA at a time.
+template <typename PT, int VE, int AG, int KIND>
+__device__ AAcc run_pass(const AsyncArgs& a, const uint32_t* perm, unsigned int* ctr, double* red, double* Qs,
+                         int* rows, int64_t* sp)
+{
+    const uint64_t pol = l2_evict_first();
+    AAcc acc{0.0, 0, 0};
+    const int64_t n = a.n;
+    if (threadIdx.x == 0) sp[0] = (int64_t)atomicAdd(ctr, 1u);
+    __syncthreads();
+    int64_t pos = sp[0];
+    while (pos < n) {
+        const int64_t s = perm ? (int64_t)__ldcg(perm + pos) : pos;
+        __syncthreads();  // every thread has read sp[0]
+        if (threadIdx.x == 0) sp[0] = (int64_t)atomicAdd(ctr, 1u);  // the next position, in flight
+        double best = 0.0;
+        int barg = 0;
+        if (KIND == 1) {
+            if (threadIdx.x == 0) rows[0] = __ldcg(a.pi + s);
+            __syncthreads();
+            state_rows<PT, VE, AG>(a, s, rows, 1, red, Qs, pol);
+            best = Qs[0];
+            barg = rows[0];
+        } else {
+            for (int a0 = 0; a0 < a.A; a0 += AG) {
+                const int na = min(AG, a.A - a0);
+                if (threadIdx.x < AG) rows[threadIdx.x] = a0 + threadIdx.x;
+                __syncthreads();
+                state_rows<PT, VE, AG>(a, s, rows, na, red, Qs + a0, pol);
+            }
+            if (threadIdx.x == 0) {
+                best = Qs[0];
+                for (int act = 1; act < a.A; ++act)
+                    if (Qs[act] < best) best = Qs[act], barg = act;
+            }
+        }
+        if (threadIdx.x == 0) {
+            const double old = __ldcg(a.V + s);
+            acc.bad |= !isfinite(best);
+            acc.rmax = fmax(acc.rmax, fabs(best - old));
+            if (KIND == 2) {
+                acc.changed += (barg != __ldcg(a.pi + s));
+                __stcg(a.pi + s, barg);
+            } else {
+                __stcg(a.V + s, best);  // visible to every later read of the application
+                if (KIND == 0 && a.pi) __stcg(a.pi + s, barg);
+            }
+        }
+        __syncthreads();
+        pos = sp[0];
+    }
+    return acc;
+}
+
+template <typename PT, int VE, int AG>
+__global__ void __launch_bounds__(kAThreads, 1) dense_async_kernel(const AsyncArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* red = reinterpret_cast<double*>(smem_raw);        // kAWarps * AG
+    double* Qs = red + kAWarps * AG;                           // A (rounded up to AG)
+    __shared__ int rows[AG];
+    __shared__ int64_t sp[1];
+    GridBarrier g{a.bar, a.bar + 32, 0ull, (unsigned long long)gridDim.x, a.err};
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const int64_t n = a.n;
+    const int64_t tid = (int64_t)blockIdx.x * kAThreads + threadIdx.x, stride = (int64_t)gridDim.x * kAThreads;
+    auto fill = [&](int64_t k) {
+        if (!a.identity) fill_order(n, a.seed, k, OrderSpec{0, nullptr, 0}, a.perm + (k % 3) * n, tid, stride);
+    };
+    fill(a.k0);
+    grid_sync(g);
+    int q = 0;  // reduction slot sequence
+    // every pass uses counter q & 3 and slot q & 3; the ones two passes ahead
+    // are re-armed by CTA 0 (their last users finished before the previous barrier)
+    auto pass = [&](int kind, int64_t k) -> AAcc {
+        if (lead) {
+            a.ctr[(q + 2) & 3] = 0u;
+            unsigned long long* z = a.red + 4 * ((q + 2) & 3);
+            z[0] = z[1] = z[2] = 0ull;
+        }
+        const uint32_t* perm = (kind == 2 || a.identity) ? nullptr : a.perm + (k % 3) * n;
+        AAcc acc = kind == 0   ? run_pass<PT, VE, AG, 0>(a, perm, a.ctr + (q & 3), red, Qs, rows, sp)
+                   : kind == 1 ? run_pass<PT, VE, AG, 1>(a, perm, a.ctr + (q & 3), red, Qs, rows, sp)
+                               : run_pass<PT, VE, AG, 2>(a, nullptr, a.ctr + (q & 3), red, Qs, rows, sp);
+        if (threadIdx.x == 0) publish(a, q, acc);
+        if (kind != 2) fill(k + 1);  // the next application's order (read after the barrier)
+        grid_sync(g);
+        unsigned long long* slot = a.red + 4 * (q & 3);
+        AAcc r;
+        r.rmax = __longlong_as_double((long long)ld_acquire_gpu(slot));
+        r.bad = ld_acquire_gpu(slot + 1) != 0;
+        r.changed = (long long)ld_acquire_gpu(slot + 2);
+        ++q;
+        return r;
+    };
+    long long status = RMB_ERR_NOT_CONVERGED, changed = 0;
+    int64_t k = a.k0, it = 0, outer = 0;
+    double last = 0.0;
+    if (a.mode == MODE_MPI) {
+        bool bad = false;
+        if (!a.pi_given) bad = pass(2, 0).bad;
+        while (!bad && outer < a.max_iter) {
+            const int64_t row = outer * (a.msweeps + 1);
+            for (int e = 0; e < a.msweeps && !bad; ++e) {
+                AAcc r = pass(1, k);
+                if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
+                ++k, ++it;
+                bad = r.bad;
+            }
+            if (bad) { ++outer; break; }
+            AAcc r = pass(2, 0);
+            if (lead && row + a.msweeps < a.trace_len) a.trace[row + a.msweeps] = r.rmax;
+            if (lead && outer < a.chg_len) a.chg[outer] = r.changed;
+            ++outer;
+            last = r.rmax;
+            changed = r.changed;
+            if (r.bad) { bad = true; break; }
+            if (r.changed == 0 && r.rmax <= a.eps) { status = RMB_OK; break; }
+        }
+        if (bad) status = RMB_ERR_NONFINITE;
+    } else {
+        const int kind = (a.mode == MODE_APPLY_PI || a.mode == MODE_POLICY_VALUE) ? 1 : 0;
+        const int64_t iters = (a.mode == MODE_VI || a.mode == MODE_POLICY_VALUE) ? a.max_iter : 1;
+        while (it < iters) {
+            AAcc r = pass(kind, k);
+            if (lead && it < a.trace_len) a.trace[it] = r.rmax;
+            ++it, ++k;
+            last = r.rmax;
+            if (r.bad) { status = RMB_ERR_NONFINITE; break; }
+            if (a.eps >= 0.0 && r.rmax <= a.eps) { status = RMB_OK; break; }
+        }
+        if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+    }
+    if (lead) {
+        a.out[OUT_SWEEPS] = it;
+        a.out[OUT_OUTER] = outer;
+        a.out[OUT_STATUS] = status;
+        a.out[OUT_RESID_BITS] = __double_as_longlong(last);
+        a.out[OUT_BATCHES] = it;  // one "batch" (barrier) per application
+        a.out[OUT_CHANGED] = changed;
+    }
+}
+
+template <typename PT, int VE, int AG>
+cudaError_t launch_async(const AsyncArgs& a, size_t smem, int grid, cudaStream_t st)
+{
+    auto kern = dense_async_kernel<PT, VE, AG>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    void* args[] = {const_cast<AsyncArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kAThreads), args, smem, st);
+}
+
+template <typename PT, int VE>
+cudaError_t launch_async_ag(const AsyncArgs& a, size_t smem_base, int grid, cudaStream_t st, int& AG)
+{
+    // rows streamed together per V vector: up to 16 (registers: 16 accumulators
+    // + 16 x VE loads in flight per thread)
+    // + 16 x VE loads in flight per thread); fp64 16-byte rows: up to 8 (spills at 16)
+    constexpr int kAGMax = (sizeof(PT) == 8 && VE == 2) ? 8 : 16;
+    AG = a.A <= 4 ? 4 : (a.A <= 8 || kAGMax == 8 ? 8 : 16);
+    const size_t smem = smem_base + (size_t)kAWarps * AG * 8 + (size_t)((a.A + AG - 1) / AG * AG) * 8;
+    if (AG == 4) return launch_async<PT, VE, 4>(a, smem, grid, st);
+    if constexpr (kAGMax == 8) return launch_async<PT, VE, 8>(a, smem, grid, st);
+    else {
+        if (AG == 8) return launch_async<PT, VE, 8>(a, smem, grid, st);
+        return launch_async<PT, VE, 16>(a, smem, grid, st);
+    }
+}
+
+}  // namespace
+
+rmb_status dense_async_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                             long long* chg_dev, int64_t chg_len, SolveResult* res)
+{
+    const int64_t n = pr.n;
+    const int psz = pr.pdt == RMB_F32 ? 4 : 8;
+    int VE = 16 / psz;
+    if ((n % VE) != 0 || (reinterpret_cast<uintptr_t>(pr.P) & 15u) != 0) VE = 1;
+    AsyncArgs a{};
+    a.P = pr.P;
+    a.c = pr.c;
+    a.n = n;
+    a.A = pr.A;
+    a.gamma = pr.gamma;
+    a.V = rq.V;
+    a.pi = rq.pi;
+    a.seed = rq.seed;
+    a.k0 = rq.k0;
+    a.identity = rq.identity ? 1 : 0;
+    a.mode = rq.mode;
+    a.pi_given = rq.pi_given ? 1 : 0;
+    a.eps = rq.eps;
+    a.max_iter = rq.max_iter;
+    a.msweeps = rq.msweeps;
+    if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.ctrl.ensure(4096) != cudaSuccess) {
+        set_error("async solver: workspace allocation failed");
+        return RMB_ERR_OOM;
+    }
+    a.perm = static_cast<uint32_t*>(pr.perm.p);
+    unsigned long long* ctrl = static_cast<unsigned long long*>(pr.ctrl.p);
+    a.bar = ctrl;                                          // [0], [32]
+    a.err = reinterpret_cast<int*>(ctrl + 64);             // [64]
+    a.out = reinterpret_cast<long long*>(ctrl + 128);      // [128..136)
+    a.ctr = reinterpret_cast<unsigned int*>(ctrl + 256);   // [256..258)
+    a.red = ctrl + 320;                                    // [320..336)
+    a.trace = trace_dev;
+    a.trace_len = trace_len;
+    a.chg = chg_dev;
+    a.chg_len = chg_len;
+    cudaStream_t st = pr.stream;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    int AG = 0;
+    if (ce == cudaSuccess) {
+        const int grid = pr.num_sms;
+        if (pr.pdt == RMB_F32)
+            ce = VE == 4 ? launch_async_ag<float, 4>(a, 0, grid, st, AG) : launch_async_ag<float, 1>(a, 0, grid, st, AG);
+        else
+            ce = VE == 2 ? launch_async_ag<double, 2>(a, 0, grid, st, AG) : launch_async_ag<double, 1>(a, 0, grid, st, AG);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
+    long long out[OUT_N] = {0};
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (ce == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) {
+        set_error(std::string("async solver: ") + cudaGetErrorString(ce));
+        return RMB_ERR_CUDA;
+    }
+    res->sweeps = out[OUT_SWEEPS];
+    res->outer = out[OUT_OUTER];
+    res->status = (int)out[OUT_STATUS];
+    double d;
+    memcpy(&d, &out[OUT_RESID_BITS], 8);
+    res->final_resid = d;
+    res->batches = out[OUT_BATCHES];
+    res->changed = out[OUT_CHANGED];
+    res->ms = ms;
+    res->launches = 1;
+    pr.last_launches = 1;
+    for (int i = 0; i < 4; ++i) pr.prof[i] = 0;
+    return RMB_OK;
+}
+
+}  // namespace rmb

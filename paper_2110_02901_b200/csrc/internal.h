@@ -44,6 +44,7 @@ struct SolveRequest {
     bool chunked = false;    // RMB_CHUNKED_T: VI* (T in chunks of b against the sweep-start values)
     bool fused = false;      // RMB_FUSED: multi-rank solve with the in-kernel peer-memory exchange
     int select = 0;          // 0: partition (R2); 1 / 2: draws with replacement, uniform / weighted (R28-R29)
+    bool async = false;      // RMB_ASYNC: no batch barrier, reads of V as found in memory (R31)
     double eps = -1.0;       // < 0: no convergence test
     int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
     int msweeps = 1;         // MPI evaluation sweeps per outer iteration
@@ -141,6 +142,9 @@ struct Problem {
 // dense.cu
 rmb_status dense_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
                        long long* chg_dev, int64_t chg_len, SolveResult* res);
+// async.cu: asynchronous dense MB-VI / MB-MPI (RMB_ASYNC, reading R31)
+rmb_status dense_async_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, int64_t trace_len,
+                             long long* chg_dev, int64_t chg_len, SolveResult* res);
 // cluster.cu: tiny dense batches on one thread-block cluster (DSMEM combine,
 // hardware cluster barrier); eligible = inside that path's envelope
 bool dense_cluster_eligible(const Problem& pr, const SolveRequest& rq);

@@ -79,6 +79,7 @@ struct SparseArgs {
     // global batch g (written during batch g - 1) -- decides which carried /
     // re-copied values a batch's own new values supersede
     uint32_t* mark;
+    int asyn;  // RMB_ASYNC (R31): one buffer X0, no batch barrier, b = n
     unsigned long long* bar;
     int* err;
     unsigned long long* red;  // [4] residual bits ring, [4..8) nonfinite ring, [8..12) changed ring
@@ -512,7 +513,10 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
     // one batch per sweep: every state rewritten each batch (not with draws
     // with replacement: undrawn states keep their values through the copies)
     const bool sel = a.order.sel != 0;
-    const bool single = b >= n && !sel;
+    // asynchronous applications (R31): one pass over the sweep's order per
+    // application, every state read from and written to X0 at once
+    const bool asy = a.asyn != 0;
+    const bool single = b >= n && !sel && !asy;
     // chunked T (VI*): every chunk reads X_cur = the sweep-start
     // values and writes X_next; no re-copies, X flips once per sweep
     const bool chunked = !EVAL && a.chunked && !single;
@@ -563,11 +567,11 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
     double rmax = 0.0;
     int bad = 0;
     // carry mode: every lane group holds at most one state of a batch
-    const bool carry = !single && !chunked && b <= ngroups;
+    const bool carry = !single && !chunked && !asy && b <= ngroups;
     for (int lo = 0; lo < n; lo += b) {
         const int cnt = cnt_of(lo);
-        const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
-        double* Xn = (x.gb & 1) ? a.X0 : a.X1;
+        const double* Xc = asy ? a.X0 : ((x.gb & 1) ? a.X1 : a.X0);
+        double* Xn = asy ? a.X0 : ((x.gb & 1) ? a.X0 : a.X1);
         if (carry && x.cs >= 0) {
             // the previous batch's new value of this group's state, into X_next
             // (its reads of that buffer ended at the barrier).  In the first
@@ -649,8 +653,8 @@ __device__ __forceinline__ SweepResult run_sweep(const SparseArgs& a, SCtx& x, i
         x.prev_perm = single || a.identity ? nullptr : a.perm + (k % 3) * a.n;
         x.prev_lo = lo;
         x.prev_cnt = cnt;
-        x.prev_valid = !single && !chunked;
-        if (!chunked) ++x.gb;
+        x.prev_valid = !single && !chunked && !asy;
+        if (!chunked && !asy) ++x.gb;
         ++x.batches;
     }
     if (chunked) ++x.gb;
@@ -930,6 +934,8 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
     a.chunked = rq.chunked ? 1 : 0;
+    a.asyn = rq.async ? 1 : 0;
+    if (rq.async) a.b = n;  // one pass per application, no batch barrier
     int mode, GS, GSE;
     sparse_layout(pr, mode, GS, GSE);
     a.GS = GS;
@@ -994,7 +1000,7 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     // are latency-bound: one CTA with CTA barriers beats a 148-CTA grid
     // barrier per batch (measured: FrozenLake b=1 96 vs 125 ms, maze80 b=1
     // 5.96 vs 7.35 s; from ~10^4 nonzeros per batch the full grid wins)
-    const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(rq.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
+    const int64_t nnz_batch = (int64_t)((double)std::min<int64_t>(a.b, n) * (double)pr.nnz / (double)std::max<int64_t>(1, n));
     const int grid = nnz_batch <= kSparseSmallBatchNnz && !pr.sparse_full_grid ? 1 : pr.num_sms;
     if (ce == cudaSuccess) {
         if (pr.pdt == RMB_F32)
