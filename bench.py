@@ -253,6 +253,39 @@ def vi_star_rows(rmb, torch, prob_c2, V, pi):
     return out
 
 
+def f4_rows(rmb, torch, prob_c2, V, pi):
+    """SURVEY 8(f) row 4 (DESIGN R28-R31) on config 2: MB-VI with
+    the paper's partitions vs draws with replacement (uniform, and an
+    epsilon-greedy importance law, R29) vs asynchronous MB-VI (no batch
+    barrier, R31); time-to-eps 1e-6 from V0 = 0."""
+    import numpy as np
+    peak, _ = peaks()
+    bps = algo_bytes_per_sweep(N_STATES, N_ACTIONS, 4, N_STATES)
+    c = rmb.generate_dense(N_STATES, N_ACTIONS, INST_SEED)[1].cpu().numpy()
+    rho = np.abs(c.min(1).astype(np.float64))
+    prob_c2.set_selection_weights(np.maximum(np.ceil(2.0**20 * (0.9 * rho / rho.max() + 0.1)), 1).astype(np.uint32))
+    out = []
+
+    def add(name, sol, note=None):
+        st = sol.stats
+        gbs = st.sweeps * bps / st.seconds / 1e9
+        out.append({"variant": name, "status": int(sol.status), "sweeps": st.sweeps,
+                    "time_to_eps_ms": st.seconds * 1e3, "ms_per_sweep": st.seconds * 1e3 / max(1, st.sweeps),
+                    "GB_per_s": gbs, "frac": gbs / peak, **({"note": note} if note else {})})
+
+    kw = dict(seed=3, eps=EPS, max_sweeps=200_000, V=V, pi=pi, v0_zero=True)
+    prob_c2.vi(1, eps=EPS, max_sweeps=3, V=V, pi=pi, v0_zero=True, asynchronous=True)
+    add("MB-VI, partition (paper), b=1000", prob_c2.vi(1000, **kw))
+    add("MB-VI, with replacement, b=1000", prob_c2.vi(1000, select="replace", **kw),
+        "r_k covers the drawn states only: stop confirmed by ||TV-V|| (R30)")
+    add("MB-VI, eps-greedy importance (w ~ 0.9 |min_a c| / max + 0.1), b=1000", prob_c2.vi(1000, select="weighted", **kw))
+    add("MB-VI, partition, b=n (Bellman)", prob_c2.vi(N_STATES, **kw))
+    add("asynchronous MB-VI (no batch barrier; 4 CTAs x 128 threads per SM, one state per CTA)",
+        prob_c2.vi(1, asynchronous=True, **kw), "dense_async_kernel: not deterministic; pinned by the J* <= V_k <= T^k V0 sandwich")
+    prob_c2.set_selection_weights(None)
+    return out
+
+
 def config5_line(rmb, torch, dist, comm, world, rank, dev):
     """BASELINE config 5 (dense |S|=50 000, |A|=32, fp32, MB-MPI m=10, b=n/8,
     gamma 0.99): P is 320 GB, sharded 8 ways = 40 GB per GPU.  On N GPUs the
@@ -330,6 +363,13 @@ def other_configs(rmb, torch, dev):
                 "frac": st.sweeps * bps / st.seconds / 1e9 / peak,
                 "note": "bound by L1TEX wavefronts of the random 8-byte V gathers (one sector each, 2.56e8 per "
                         "sweep), not HBM: profiles/r02"})
+    sol = prob.vi(1, seed=0, eps=1e-6, max_sweeps=100_000, asynchronous=True)
+    st = sol.stats
+    out.append({"workload": "config 3, asynchronous MB-VI (SURVEY 8(f) row 4, R31: no batch barrier, one V buffer)",
+                "status": int(sol.status), "sweeps": st.sweeps, "time_to_eps_ms": st.seconds * 1e3,
+                "backups_per_s": st.sweeps * n * A / st.seconds,
+                "hbm_algorithmic_GB_per_s": st.sweeps * bps / st.seconds / 1e9,
+                "frac": st.sweeps * bps / st.seconds / 1e9 / peak})
     del prob, rp, col, val, c
     torch.cuda.empty_cache()
     N = 2048
@@ -371,6 +411,9 @@ def paper_envs(rmb, torch):
             st = sol.stats
             rows.append({"b": b, "sweeps": st.sweeps, "time_to_eps_ms": st.seconds * 1e3,
                          "us_per_batch": st.seconds / max(1, st.batches) * 1e6})
+        sol = prob.vi(1, seed=0, eps=1e-6, max_sweeps=100_000, asynchronous=True)  # R31: no batch barrier
+        rows.append({"b": "async", "sweeps": sol.stats.sweeps, "time_to_eps_ms": sol.stats.seconds * 1e3,
+                     "us_per_batch": sol.stats.seconds / max(1, sol.stats.batches) * 1e6})
         out.append({"env": name, "n": n, "A": A, "nnz": int(len(val)), "gamma": 0.95, "vi": rows})
         prob.close()
     return out
@@ -562,6 +605,7 @@ def main():
         result["time_to_eps_vs_b"] = table
     if rank == 0 and world == 1 and not args.no_other:
         result["vi_star_vs_mb_vi"] = vi_star_rows(rmb, torch, prob, V, pi)
+        result["selection_and_async"] = f4_rows(rmb, torch, prob, V, pi)
 
     if rank == 0 and world == 1 and not args.no_e2e:
         # e2e through the C ABI with HOST buffers: H2D of P, c inside the timed region

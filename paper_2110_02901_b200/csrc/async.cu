@@ -13,7 +13,7 @@
 //   deterministic; it is pinned by properties that hold for every
 //   interleaving (tests/test_gpu_async.py, test_oracle_async.py).
 //
-// One state per CTA: its A rows (all n columns) stream through registers
+// One state per CTA (4 CTAs of 128 threads per SM): its A rows (all n columns) stream through registers
 // (16-byte loads, L1 bypassed, L2 evict_first), each V vector is loaded once
 // from L2 (.cg: the coherence point, never a stale L1 line) and used for AG
 // rows; the CTA reduces the partial sums in a fixed order (thread columns ->
@@ -34,8 +34,21 @@ namespace rmb {
 
 namespace {
 
-constexpr int kAThreads = 512;
+// threads per CTA: 4 CTAs of 128 per SM (tools/ab_async.py on config 2: 512 x 1
+// 1.43 ms per application, 256 x 2 1.17, 128 x 4 1.12, 64 x 8 1.08 but more
+// states in flight -> more applications to eps; A/B builds only override it)
+#ifndef RMB_ASYNC_NT
+#define RMB_ASYNC_NT 128
+#endif
+#ifndef RMB_ASYNC_DB  // software-pipelined column loop, rows per pass capped at RMB_ASYNC_AGMAX
+#define RMB_ASYNC_DB 0
+#endif
+#ifndef RMB_ASYNC_AGMAX
+#define RMB_ASYNC_AGMAX 16
+#endif
+constexpr int kAThreads = RMB_ASYNC_NT;
 constexpr int kAWarps = kAThreads / 32;
+constexpr int kACtasPerSm = 512 / kAThreads;
 
 struct AsyncArgs {
     const void* P;
@@ -121,6 +134,36 @@ __device__ __forceinline__ void state_rows(const AsyncArgs& a, int64_t s, const 
     for (int r = 0; r < AG; ++r) acc[r] = 0.0;
     // the rows of one call are consecutive actions (min) or the single row pi(s)
     const PT* base = P + ((int64_t)s * a.A + rows[0]) * n;
+#if RMB_ASYNC_DB
+    // software pipelined: the next column block's rows are in flight while
+    // this block's FMAs run
+    int64_t j = (int64_t)threadIdx.x * VE;
+    PVec<PT, VE> x[AG];
+    if (j < n) {
+#pragma unroll
+        for (int r = 0; r < AG; ++r)
+            if (r < na) x[r] = ld_p<PT, VE>(base + (int64_t)r * n + j, pol);
+    }
+    for (; j < n; j += (int64_t)kAThreads * VE) {
+        const int64_t jn = j + (int64_t)kAThreads * VE;
+        PVec<PT, VE> y[AG];
+        if (jn < n) {
+#pragma unroll
+            for (int r = 0; r < AG; ++r)
+                if (r < na) y[r] = ld_p<PT, VE>(base + (int64_t)r * n + jn, pol);
+        }
+        double v[VE];
+        ld_v<VE>(a.V, j, v);
+#pragma unroll
+        for (int r = 0; r < AG; ++r)
+            if (r < na) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) acc[r] = fma((double)x[r].x[e], v[e], acc[r]);
+            }
+#pragma unroll
+        for (int r = 0; r < AG; ++r) x[r] = y[r];
+    }
+#else
     for (int64_t j = (int64_t)threadIdx.x * VE; j < n; j += (int64_t)kAThreads * VE) {
         PVec<PT, VE> x[AG];
 #pragma unroll
@@ -135,6 +178,7 @@ __device__ __forceinline__ void state_rows(const AsyncArgs& a, int64_t s, const 
                 for (int e = 0; e < VE; ++e) acc[r] = fma((double)x[r].x[e], v[e], acc[r]);
             }
     }
+#endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int r = 0; r < AG; ++r) {
@@ -227,7 +271,7 @@ __device__ AAcc run_pass(const AsyncArgs& a, const uint32_t* perm, unsigned int*
 }
 
 template <typename PT, int VE, int AG>
-__global__ void __launch_bounds__(kAThreads, 1) dense_async_kernel(const AsyncArgs a)
+__global__ void __launch_bounds__(kAThreads, kACtasPerSm) dense_async_kernel(const AsyncArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* red = reinterpret_cast<double*>(smem_raw);        // kAWarps * AG
@@ -324,9 +368,9 @@ cudaError_t launch_async(const AsyncArgs& a, size_t smem, int grid, cudaStream_t
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAThreads, smem);
     if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    if (per_sm < kACtasPerSm) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {const_cast<AsyncArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kAThreads), args, smem, st);
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid * kACtasPerSm), dim3(kAThreads), args, smem, st);
 }
 
 template <typename PT, int VE>
@@ -335,7 +379,7 @@ cudaError_t launch_async_ag(const AsyncArgs& a, size_t smem_base, int grid, cuda
     // rows streamed together per V vector: up to 16 (registers: 16 accumulators
     // + 16 x VE loads in flight per thread)
     // + 16 x VE loads in flight per thread); fp64 16-byte rows: up to 8 (spills at 16)
-    constexpr int kAGMax = (sizeof(PT) == 8 && VE == 2) ? 8 : 16;
+    constexpr int kAGMax = (sizeof(PT) == 8 && VE == 2) ? 8 : RMB_ASYNC_AGMAX;
     AG = a.A <= 4 ? 4 : (a.A <= 8 || kAGMax == 8 ? 8 : 16);
     const size_t smem = smem_base + (size_t)kAWarps * AG * 8 + (size_t)((a.A + AG - 1) / AG * AG) * 8;
     if (AG == 4) return launch_async<PT, VE, 4>(a, smem, grid, st);
