@@ -43,10 +43,17 @@ MUTATIONS = [
      "        for (int64_t p = lo; p < hi; ++p) V[perm[p]] = newv[perm[p]];\n    }"),
     ("last_batch_dropped", "        int64_t hi = lo + b < m->n ? lo + b : m->n;\n        /* every state",
      "        int64_t hi = lo + b < m->n ? lo + b : lo;\n        /* every state"),
+    # draws with replacement (R28-R30)
+    ("select_modulo_not_mulhi", "sel[i] = (uint32_t)mulhi64(u, (uint64_t)n);", "sel[i] = (uint32_t)(u % (uint64_t)n);"),
+    ("select_cdf_off_by_one", "if (cum[mid] > t) hi = mid;", "if (cum[mid] >= t) hi = mid;"),
+    ("select_key_unmixed", "const uint64_t skey = orc_mix64(key ^ ORC_SEL_C);", "const uint64_t skey = key;"),
+    ("select_stop_unconfirmed", "if (rT > eps) continue;", "(void)rT;"),
+    ("select_ignored_by_solvers", "return select ? orc_select(n, seed, k, w, perm) : orc_partition(n, seed, k, identity, perm);",
+     "(void)select; (void)w; return orc_partition(n, seed, k, identity, perm);"),
 ]
 
 TESTS = ["tests/test_oracle_operator.py", "tests/test_oracle_solvers.py", "tests/test_oracle_partition.py",
-         "tests/test_envs.py"]
+         "tests/test_oracle_select.py", "tests/test_oracle_async.py", "tests/test_envs.py"]
 
 
 def main():
@@ -55,7 +62,8 @@ def main():
     args = ap.parse_args()
     src = open(SRC).read()
     bad = []
-    with tempfile.TemporaryDirectory() as td:
+    # a sibling of gen/ so that oracle.c's #include "../gen/rmb_gen.h" resolves
+    with tempfile.TemporaryDirectory(dir=ROOT, prefix=".mutation_") as td:
         for name, old, new in MUTATIONS:
             if args.k not in name:
                 continue
