@@ -280,8 +280,9 @@ def f4_rows(rmb, torch, prob_c2, V, pi):
         "r_k covers the drawn states only: stop confirmed by ||TV-V|| (R30)")
     add("MB-VI, eps-greedy importance (w ~ 0.9 |min_a c| / max + 0.1), b=1000", prob_c2.vi(1000, select="weighted", **kw))
     add("MB-VI, partition, b=n (Bellman)", prob_c2.vi(N_STATES, **kw))
-    add("asynchronous MB-VI (no batch barrier; 4 CTAs x 128 threads per SM, one state per CTA)",
-        prob_c2.vi(1, asynchronous=True, **kw), "dense_async_kernel: not deterministic; pinned by the J* <= V_k <= T^k V0 sandwich")
+    add("asynchronous MB-VI (no batch barrier; one state per CTA, rows by TMA, finisher warp)",
+        prob_c2.vi(1, asynchronous=True, **kw),
+        "dense_async_tma_kernel: not deterministic; pinned by the J* <= V_k <= T^k V0 sandwich")
     prob_c2.set_selection_weights(None)
     return out
 
