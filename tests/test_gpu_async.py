@@ -43,7 +43,9 @@ CASES = {
     "dense_f32": lambda: dense(600, 16, 5),
     "dense_f32_ragged": lambda: dense(257, 5, 6),            # n % 4 != 0: scalar loads
     "dense_f64": lambda: dense(300, 12, 7, dtype=np.float64),
-    "dense_A40": lambda: dense(200, 40, 8),                  # three row groups per state
+    "dense_A40": lambda: dense(200, 40, 8),                  # three row units per state (16 + 16 + 8)
+    "dense_A3": lambda: dense(128, 3, 9),                    # units narrower than a row group of 4
+    "dense_f32_regs": lambda: dense(400, 16, 10, flags=rmb.DENSE_NO_TMA),  # register-streaming kernel
     "sparse_ell": lambda: sparse("ell"),
     "sparse_grid": lambda: sparse("grid"),
 }
