@@ -114,6 +114,12 @@ typedef struct {
                              T V0 <= V0 every iterate lies between J* and the Bellman iterate T^k V0.
                              MB-MPI: asynchronous evaluation sweeps, synchronous improvement.
                              Single-GPU; excludes RMB_CHUNKED_T and RMB_SELECT_*.                */
+#define RMB_TRACE_ERROR_VS_REF 0x10000u /* rmb_vi / rmb_mpi / rmb_policy_value: also record the paper's plotted
+                                          metric -- err[i] = ||V_i - V*||_inf
+                                          after operator application i (VI sweeps, MPI evaluation sweeps),
+                                          V* from rmb_set_reference; read with rmb_error_trace.  Computed
+                                          on the device after each application (asynchronous applications
+                                          add one grid barrier for it).  Single-GPU handles only.         */
 /* A/B and test switches of rmb_create_* (performance choices only: results are bitwise the same) */
 #define RMB_SPARSE_FULL_GRID 0x80u  /* sparse: 148-CTA grid even for tiny batches (default: 1 CTA)  */
 #define RMB_SHARD_NO_GRAPH 0x400u   /* shard handles: launch each sweep's batch sequence eagerly
@@ -267,6 +273,14 @@ rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags
  * the device kernel the solvers use (flags RMB_SELECT_REPLACE or
  * RMB_SELECT_WEIGHTED with the handle's weights), sel: DEVICE [n]. */
 rmb_status rmb_set_selection_weights(rmb_problem h, const uint32_t* w);
+
+/* Error-vs-reference tracing (RMB_TRACE_ERROR_VS_REF).  rmb_set_reference:
+ * Vref = [n] float64 (HOST or DEVICE, copied; NULL clears) -- typically V*
+ * from a tight solve or exact policy iteration.  rmb_error_trace: copies the
+ * last solve's errors (HOST or DEVICE out, up to len) and sets *count (HOST,
+ * may be NULL) to the number recorded (0 when the last solve did not trace). */
+rmb_status rmb_set_reference(rmb_problem h, const void* Vref);
+rmb_status rmb_error_trace(rmb_problem h, double* out, int64_t len, int64_t* count);
 rmb_status rmb_select(int64_t n, uint64_t seed, int64_t sweep, const uint32_t* w, uint32_t* sel);
 rmb_status rmb_select_device(rmb_problem h, uint64_t seed, int64_t sweep, uint32_t flags, uint32_t* sel);
 

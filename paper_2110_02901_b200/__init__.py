@@ -30,6 +30,7 @@ ORDER_IDENTITY, V0_ZERO, PI_GIVEN, VALIDATE, DENSE_NO_TMA, DENSE_VGLOBAL = 0x1, 
 CHUNKED_T = 0x40
 SPARSE_FULL_GRID, SHARD_NO_GRAPH, FUSED, DENSE_NO_CLUSTER = 0x80, 0x400, 0x800, 0x1000
 SELECT_REPLACE, SELECT_WEIGHTED, ASYNC = 0x2000, 0x4000, 0x8000
+TRACE_ERROR_VS_REF = 0x10000
 
 _lib = None
 
@@ -99,6 +100,9 @@ _SIGS = {
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)], ctypes.c_int),
     "rmb_last_phase_times": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "rmb_set_selection_weights": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_set_reference": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "rmb_error_trace": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)],
+                        ctypes.c_int),
     "rmb_select": ([ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "rmb_select_device": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p],
                           ctypes.c_int),
@@ -197,6 +201,7 @@ class Solution:
     status: int
     stats: Stats
     changed: np.ndarray | None = None
+    error: np.ndarray | None = None   # ||V_i - V*||_inf per application (trace_error=True)
 
     @property
     def converged(self):
@@ -272,24 +277,26 @@ class Problem:
         return _vec(V, self.n, "f64", "V"), _vec(pi, self.n, "i32", "pi")
 
     def vi(self, b, seed=0, eps=1e-6, max_sweeps=100_000, V=None, pi=None, identity=False, v0_zero=False,
-           device="cuda", chunked=False, fused=False, select=None, asynchronous=False):
+           device="cuda", chunked=False, fused=False, select=None, asynchronous=False, trace_error=False):
         """MB-VI: V, pi updated in place (torch cuda/cpu or numpy).
         chunked=True: VI* -- every sweep is T computed in chunks of b
         states against the sweep-start values (RMB_CHUNKED_T).
         select="replace" / "weighted": every sweep draws n states with
         replacement, uniformly / by the weights of set_selection_weights (R28-R30).
-        asynchronous=True: RMB_ASYNC (R31) -- no batch barrier, b unused."""
+        asynchronous=True: RMB_ASYNC (R31) -- no batch barrier, b unused.
+        trace_error=True: record ||V_k - V*||_inf per sweep (set_reference first)."""
         V, pi = self._vp(V, pi, device)
         tr = np.zeros(max_sweeps)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (CHUNKED_T if chunked else 0)
-                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0))
+                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0)
+                 | (TRACE_ERROR_VS_REF if trace_error else 0))
         s = lib().rmb_vi(self._h, b, seed, eps, max_sweeps, flags, _ptr(V), _ptr(pi), _ptr(tr), ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
-        return Solution(V, pi, tr[: st.sweeps], s, st)
+        return Solution(V, pi, tr[: st.sweeps], s, st, error=self.error_trace() if trace_error else None)
 
     def mpi(self, b, m, seed=0, eps=1e-6, max_outer=10_000, V=None, pi=None, pi_given=False, identity=False,
-            v0_zero=False, device="cuda", fused=False, select=None, asynchronous=False):
+            v0_zero=False, device="cuda", fused=False, select=None, asynchronous=False, trace_error=False):
         """MB-MPI: Algorithm 1 with B_{pi,b} evaluation, warm start
         (select: evaluation sweeps draw with replacement, as vi())."""
         V, pi = self._vp(V, pi, device)
@@ -297,12 +304,13 @@ class Problem:
         ch = np.zeros(max_outer, dtype=np.int64)
         st = Stats()
         flags = ((ORDER_IDENTITY if identity else 0) | (V0_ZERO if v0_zero else 0) | (PI_GIVEN if pi_given else 0)
-                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0))
+                 | (FUSED if fused else 0) | _select_flag(select) | (ASYNC if asynchronous else 0)
+                 | (TRACE_ERROR_VS_REF if trace_error else 0))
         s = lib().rmb_mpi(self._h, b, m, seed, eps, max_outer, flags, _ptr(V), _ptr(pi), _ptr(tr), _ptr(ch),
                           ctypes.byref(st))
         _check(s, (OK, NOT_CONVERGED, NONFINITE))
         o = st.outer_iters
-        return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o])
+        return Solution(V, pi, tr[: o * (m + 1)], s, st, ch[:o], error=self.error_trace() if trace_error else None)
 
     def apply(self, b, seed, sweep, V_in, V_out=None, pi=None, argmin=None, identity=False, chunked=False,
               select=None, asynchronous=False):
@@ -348,6 +356,21 @@ class Problem:
         s = lib().rmb_improve(self._h, _ptr(V), _ptr(pi), ctypes.byref(r), ctypes.byref(ch))
         _check(s, (OK, NONFINITE))
         return pi, r.value, ch.value
+
+    def set_reference(self, Vref):
+        """V* for trace_error (float64 [n], host or device; None clears)."""
+        if Vref is not None:
+            _vec(Vref, self.n, "f64", "Vref")
+        _check(lib().rmb_set_reference(self._h, _ptr(Vref)))
+
+    def error_trace(self):
+        """||V_i - V*||_inf per application of the last traced solve (numpy)."""
+        cnt = ctypes.c_int64()
+        _check(lib().rmb_error_trace(self._h, None, 0, ctypes.byref(cnt)))
+        out = np.zeros(cnt.value)
+        if cnt.value:
+            _check(lib().rmb_error_trace(self._h, _ptr(out), cnt.value, None))
+        return out
 
     def set_selection_weights(self, w):
         """Integer weights w_s >= 1 ([n] uint32, host or device; None clears) for

@@ -106,6 +106,8 @@ static void free_problem(Problem* pr)
     pr->aux.release();
     pr->rowrec.release();
     pr->sel_buf.release();
+    pr->ref_buf.release();
+    pr->etrace.release();
     for (int q = 0; q < 8; ++q)
         if (pr->xpeer_open[q]) cudaIpcCloseMemHandle(pr->xpeer[q]);
     pr->xbuf.release();
@@ -153,6 +155,26 @@ static void apply_create_flags(Problem& pr, uint32_t flags)
 }
 
 static bool is_shard(const Problem& pr) { return pr.nccl_comm || pr.row_begin != 0 || pr.row_end != pr.n; }
+
+// RMB_TRACE_ERROR_VS_REF (the paper's plotted metric P:L496,
+// L575): etrace[i] = ||V_i - V*||_inf after application i, V* from
+// rmb_set_reference; `apps` = applications the solve may run
+static rmb_status error_trace_of(Problem& pr, uint32_t flags, int64_t apps, SolveRequest& rq)
+{
+    pr.etrace_count = 0;
+    if (!(flags & RMB_TRACE_ERROR_VS_REF)) return RMB_OK;
+    if (!pr.has_ref) return fail(RMB_ERR_INVALID_ARG, "RMB_TRACE_ERROR_VS_REF: no reference set (rmb_set_reference)");
+    if (is_shard(pr) || (flags & RMB_FUSED))
+        return fail(RMB_ERR_UNSUPPORTED, "RMB_TRACE_ERROR_VS_REF is single-GPU (not for row-range handles)");
+    if (pr.etrace.ensure((size_t)std::max<int64_t>(1, apps) * 8) != cudaSuccess)
+        return fail(RMB_ERR_OOM, "error trace allocation failed");
+    cudaError_t e = cudaMemsetAsync(pr.etrace.p, 0, (size_t)std::max<int64_t>(1, apps) * 8, pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "error trace init");
+    rq.vref = static_cast<const double*>(pr.ref_buf.p);
+    rq.etrace = static_cast<double*>(pr.etrace.p);
+    rq.etrace_len = apps;
+    return RMB_OK;
+}
 
 // RMB_ASYNC (reading R31): single-GPU, partition order only
 static rmb_status async_of(const Problem& pr, uint32_t flags, bool* as)
@@ -275,6 +297,10 @@ static rmb_status vi_with_replacement(Problem& pr, const SolveRequest& rq0, Solv
         SolveRequest rq = rq0;
         rq.k0 = rq0.k0 + done;
         rq.max_iter = rq0.max_iter - done;
+        if (rq0.etrace) {
+            rq.etrace = rq0.etrace + done;
+            rq.etrace_len = rq0.etrace_len - done;
+        }
         SolveResult r;
         rmb_status s = solve(pr, rq, trace + done, rq.max_iter, nullptr, 0, &r);
         if (s != RMB_OK) return s;
@@ -469,6 +495,8 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     SolveRequest rq;
     rq.select = sel;
     rq.async = as;
+    s = error_trace_of(pr, flags, max_sweeps, rq);
+    if (s != RMB_OK) return s;
     rq.mode = MODE_VI;
     rq.b = b;
     rq.seed = seed;
@@ -499,6 +527,7 @@ rmb_status rmb_vi(rmb_problem h, int64_t b, uint64_t seed, double eps, int64_t m
     }
     s = sel ? vi_with_replacement(pr, rq, &r) : solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
     if (s != RMB_OK) return s;
+    if (rq.etrace) pr.etrace_count = std::min<int64_t>(r.sweeps, max_sweeps);
     s = stage_out(pr, V, pi, sg);
     if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.sweeps);
     if (s != RMB_OK) return s;
@@ -540,6 +569,8 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     rq.mode = MODE_MPI;
     rq.select = sel;
     rq.async = as;
+    s = error_trace_of(pr, flags, max_outer * (int64_t)m, rq);
+    if (s != RMB_OK) return s;
     rq.b = b;
     rq.msweeps = m;
     rq.seed = seed;
@@ -571,6 +602,7 @@ rmb_status rmb_mpi(rmb_problem h, int64_t b, int32_t m, uint64_t seed, double ep
     }
     s = solve(pr, rq, static_cast<double*>(pr.trace.p), tl, static_cast<long long*>(pr.chg.p), max_outer, &r);
     if (s != RMB_OK) return s;
+    if (rq.etrace) pr.etrace_count = std::min<int64_t>(r.sweeps, max_outer * (int64_t)m);
     s = stage_out(pr, V, pi, sg);
     if (s == RMB_OK) s = copy_trace(pr, trace, static_cast<double*>(pr.trace.p), r.outer * (int64_t)(m + 1));
     if (s == RMB_OK && changed && r.outer > 0) {
@@ -593,8 +625,8 @@ static rmb_status group_solve(rmb_problem* hs, int32_t G, SolveRequest rq, uint3
                               double* trace, int64_t tl, int64_t* changed, int64_t cl, rmb_stats* stats)
 {
     if (!hs || G < 1) return fail(RMB_ERR_INVALID_ARG, "handles NULL or G < 1");
-    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED | RMB_ASYNC))
-        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement and RMB_ASYNC are single-GPU (not for rmb_*_group)");
+    if (flags & (RMB_SELECT_REPLACE | RMB_SELECT_WEIGHTED | RMB_ASYNC | RMB_TRACE_ERROR_VS_REF))
+        return fail(RMB_ERR_UNSUPPORTED, "draws with replacement, RMB_ASYNC and RMB_TRACE_ERROR_VS_REF are single-GPU (not for rmb_*_group)");
     if (!V || !pi) return fail(RMB_ERR_INVALID_ARG, "V or pi is NULL");
     std::vector<Problem*> rk((size_t)G);
     for (int g = 0; g < G; ++g) {
@@ -815,6 +847,8 @@ rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_
     SolveRequest rq;
     rq.mode = MODE_POLICY_VALUE;
     rq.async = as;
+    s = error_trace_of(pr, flags, max_sweeps, rq);
+    if (s != RMB_OK) return s;
     rq.b = b;
     rq.seed = seed;
     rq.k0 = 1;
@@ -826,6 +860,7 @@ rmb_status rmb_policy_value(rmb_problem h, const int32_t* pi, int64_t b, uint64_
     SolveResult r;
     s = solve(pr, rq, static_cast<double*>(pr.trace.p), max_sweeps, nullptr, 0, &r);
     if (s != RMB_OK) return s;
+    if (rq.etrace) pr.etrace_count = std::min<int64_t>(r.sweeps, max_sweeps);
     Staged vo = sg;
     vo.pi_host = false;  // pi is an input here
     s = stage_out(pr, V, nullptr, vo);
@@ -848,6 +883,37 @@ rmb_status rmb_partition(int64_t n, uint64_t seed, int64_t sweep, uint32_t flags
     Permutation pm;
     pm.init(n, seed, sweep);
     for (int64_t p = 0; p < n; ++p) perm[p] = (uint32_t)pm((uint64_t)p);
+    return RMB_OK;
+}
+
+rmb_status rmb_set_reference(rmb_problem h, const void* Vref)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (!Vref) {
+        pr.has_ref = false;
+        return RMB_OK;
+    }
+    if (pr.ref_buf.ensure((size_t)pr.n * 8) != cudaSuccess) return fail(RMB_ERR_OOM, "reference allocation failed");
+    cudaError_t e = cudaMemcpyAsync(pr.ref_buf.p, Vref, (size_t)pr.n * 8, cudaMemcpyDefault, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "copy reference");
+    pr.has_ref = true;
+    return RMB_OK;
+}
+
+rmb_status rmb_error_trace(rmb_problem h, double* out, int64_t len, int64_t* count)
+{
+    g_err.clear();
+    if (!h) return fail(RMB_ERR_INVALID_ARG, "handle is NULL");
+    Problem& pr = *reinterpret_cast<Problem*>(h);
+    if (count) *count = pr.etrace_count;
+    const int64_t m = std::min<int64_t>(len, pr.etrace_count);
+    if (!out || m <= 0) return RMB_OK;
+    cudaError_t e = cudaMemcpyAsync(out, pr.etrace.p, (size_t)m * 8, cudaMemcpyDefault, pr.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "error trace copy");
     return RMB_OK;
 }
 

@@ -71,6 +71,9 @@ struct AsyncArgs {
     int* err;
     unsigned int* ctr;        // [4] position counters (application parity, improvement)
     unsigned long long* red;  // [4 slots x 4]: residual bits, bad, changed
+    const double* vref;       // RMB_TRACE_ERROR_VS_REF (null = off)
+    double* etrace;
+    int64_t etrace_len;
     double* trace;
     int64_t trace_len;
     long long* chg;
@@ -311,6 +314,12 @@ __global__ void __launch_bounds__(kAThreads, kACtasPerSm) dense_async_kernel(con
         ++q;
         return r;
     };
+    // error trace after application it (V is global and written at once by
+    // the next application: a barrier closes the pass)
+    auto etrace_pass = [&](int64_t it_) {
+        trace_error([&](int64_t j) { return __ldcg(a.V + j); }, a.vref, n, tid, stride, a.etrace + it_);
+        grid_sync(g);
+    };
     long long status = RMB_ERR_NOT_CONVERGED, changed = 0;
     int64_t k = a.k0, it = 0, outer = 0;
     double last = 0.0;
@@ -322,6 +331,7 @@ __global__ void __launch_bounds__(kAThreads, kACtasPerSm) dense_async_kernel(con
             for (int e = 0; e < a.msweeps && !bad; ++e) {
                 AAcc r = pass(1, k);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
+                if (a.etrace && it < a.etrace_len) etrace_pass(it);
                 ++k, ++it;
                 bad = r.bad;
             }
@@ -342,6 +352,7 @@ __global__ void __launch_bounds__(kAThreads, kACtasPerSm) dense_async_kernel(con
         while (it < iters) {
             AAcc r = pass(kind, k);
             if (lead && it < a.trace_len) a.trace[it] = r.rmax;
+            if (a.etrace && it < a.etrace_len) etrace_pass(it);
             ++it, ++k;
             last = r.rmax;
             if (r.bad) { status = RMB_ERR_NONFINITE; break; }
@@ -795,6 +806,11 @@ __global__ void __launch_bounds__(kTThreads, 1) dense_async_tma_kernel(const Tma
         ++q;
         return r;
     };
+    auto etrace_pass = [&](int64_t it_) {
+        trace_error([&](int64_t j) { return __ldcg(a.V + j); }, a.vref, n, (int64_t)blockIdx.x * kTBar + threadIdx.x,
+                    (int64_t)gridDim.x * kTBar, a.etrace + it_);
+        grid_sync<kTBar>(g);
+    };
     long long status = RMB_ERR_NOT_CONVERGED, changed = 0;
     int64_t k = a.k0, it = 0, outer = 0;
     double last = 0.0;
@@ -806,6 +822,7 @@ __global__ void __launch_bounds__(kTThreads, 1) dense_async_tma_kernel(const Tma
             for (int e = 0; e < a.msweeps && !bad; ++e) {
                 AAcc r = pass(1, k);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
+                if (a.etrace && it < a.etrace_len) etrace_pass(it);
                 ++k, ++it;
                 bad = r.bad;
             }
@@ -826,6 +843,7 @@ __global__ void __launch_bounds__(kTThreads, 1) dense_async_tma_kernel(const Tma
         while (it < iters) {
             AAcc r = pass(kind, k);
             if (lead && it < a.trace_len) a.trace[it] = r.rmax;
+            if (a.etrace && it < a.etrace_len) etrace_pass(it);
             ++it, ++k;
             last = r.rmax;
             if (r.bad) { status = RMB_ERR_NONFINITE; break; }
@@ -903,6 +921,9 @@ rmb_status dense_async_solve(Problem& pr, const SolveRequest& rq, double* trace_
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;
     a.msweeps = rq.msweeps;
+    a.vref = rq.vref;
+    a.etrace = rq.etrace;
+    a.etrace_len = rq.etrace_len;
     if (pr.perm.ensure((size_t)3 * n * 4) != cudaSuccess || pr.ctrl.ensure(4096) != cudaSuccess) {
         set_error("async solver: workspace allocation failed");
         return RMB_ERR_OOM;

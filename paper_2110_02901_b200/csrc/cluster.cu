@@ -58,6 +58,9 @@ struct ClusterArgs {
     int64_t max_iter;
     uint32_t* perm; // 3 * n
     OrderSpec order;  // permutation, or draws with replacement (R28-R29)
+    const double* vref;  // RMB_TRACE_ERROR_VS_REF (null = off)
+    double* etrace;
+    int64_t etrace_len;
     double* trace;
     int64_t trace_len;
     long long* out;
@@ -397,6 +400,9 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         for (int w = 0; w < kCWarps; ++w) r = fmax(r, red[w]), bb |= redb[w];
         __syncthreads();
         if (q == 0 && t == 0 && it < a.trace_len) a.trace[it] = r;
+        if (a.etrace && it < a.etrace_len)  // every CTA holds all of V: CTA q folds its share
+            trace_error([&](int64_t j) { return Vs[vidx((int)j)]; }, a.vref, n, (int64_t)q * kCThreads + t,
+                        (int64_t)CS * kCThreads, a.etrace + it);
         ++it;
         ++ck;
         last = r;
@@ -518,6 +524,9 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     a.k0 = rq.k0;
     a.identity = rq.identity && !rq.select ? 1 : 0;
     a.order = OrderSpec{rq.select, pr.sel_cum, pr.sel_W};
+    a.vref = rq.vref;
+    a.etrace = rq.etrace;
+    a.etrace_len = rq.etrace_len;
     a.eval = eval ? 1 : 0;
     a.eps = rq.eps;
     a.max_iter = rq.max_iter;

@@ -317,6 +317,22 @@ __device__ __forceinline__ void st_release_cta(long long* p, long long v)
 }
 
 
+// ------------------------------------------------------------- error trace
+// RMB_TRACE_ERROR_VS_REF: ||V - Vref||_inf over the entries j0, j0 + stride,
+// ... < n (V read through get(j)), folded into *slot (>= 0 doubles order like
+// their bits).  Every lane of every calling warp must call it (warp max).
+template <typename Get>
+__device__ __forceinline__ void trace_error(Get get, const double* vref, int64_t n, int64_t j0, int64_t stride,
+                                            double* slot)
+{
+    double e = 0.0;
+    for (int64_t j = j0; j < n; j += stride) e = fmax(e, fabs(get(j) - __ldg(vref + j)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if ((threadIdx.x & 31) == 0 && e > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)__double_as_longlong(e));
+}
+
 // ------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v)
 {

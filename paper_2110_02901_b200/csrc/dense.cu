@@ -94,6 +94,9 @@ struct DenseArgs {
     double* vnext;       // chunked T (VI*): new values of the sweep, applied at its end; null = B_b
     uint32_t* perm;      // 3 * n (triple-buffered by sweep index)
     OrderSpec order;     // permutation, or draws with replacement (R28-R29)
+    const double* vref;  // RMB_TRACE_ERROR_VS_REF: reference V*, etrace[i] = ||V_i - V*|| (null = off)
+    double* etrace;
+    int64_t etrace_len;
     double* part;        // 2 * part_stride
     int64_t part_stride;
     double* lval;        // distributed-combine list: value per batch position
@@ -1529,6 +1532,34 @@ __device__ PhaseAcc run_improve(const DenseArgs& a, Ctx& x, double* Vs, int32_t*
     return r;
 }
 
+// error trace after application `it`: each CTA folds its share of the states
+// (its shared-memory copy of V is complete after the application's last
+// patch; global V after the grid reduction).  A non-inlined call with scalar
+// arguments: the solver loop keeps the register allocation of the untraced
+// kernel (inlined, or passing DenseArgs by reference, made it spill).
+__device__ __noinline__ void trace_error_dense(const double* V, int smem, int64_t vs_half, const double* vref,
+                                               int64_t n, int64_t j0, int64_t stride, double* slot)
+{
+    if (smem)
+        trace_error([&](int64_t j) { return V[vs_index(j, vs_half)]; }, vref, n, j0, stride, slot);
+    else
+        trace_error([&](int64_t j) { return __ldcg(V + j); }, vref, n, j0, stride, slot);
+}
+
+#ifndef RMB_AB_NO_ETRACE
+#define RMB_ETRACE_DENSE()                                                                                       \
+    do {                                                                                                          \
+        if (a.etrace && it < a.etrace_len)                                                                        \
+            trace_error_dense(is_vgl(CTA) ? a.V : Vs, !is_vgl(CTA), a.vs_half, a.vref, a.n,                       \
+                              (int64_t)cta_rank(a) * kThreads + threadIdx.x, (int64_t)a.nctas * kThreads,          \
+                              a.etrace + it);                                                                     \
+    } while (0)
+#else  // A/B builds: the solver without the trace call
+#define RMB_ETRACE_DENSE() \
+    do {                   \
+    } while (0)
+#endif
+
 template <typename PT, int VE, int CTA>
 __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
 {
@@ -1614,6 +1645,7 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
             PhaseAcc r = eval ? run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs)
                                                  : run_sweep<PT, VE, false, CTA>(a, x, Vs, pis, k, Qs);
             if (lead && it < a.trace_len) a.trace[it] = r.rmax;
+            RMB_ETRACE_DENSE();
             ++it;
             ++k;
             last = r.rmax;
@@ -1637,6 +1669,7 @@ __device__ __forceinline__ void dense_solver_body(const DenseArgs& a)
             for (int e = 0; e < a.msweeps && !bad; ++e) {
                 PhaseAcc r = run_sweep<PT, VE, true, CTA>(a, x, Vs, pis, k, Qs);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.rmax;
+                RMB_ETRACE_DENSE();
                 ++k;
                 ++it;
                 bad = r.bad;
@@ -1824,6 +1857,9 @@ static rmb_status dense_prepare(Problem& pr, const SolveRequest& rq, double* tra
     // a permutation: they always need the order array)
     a.identity = rq.select ? 0 : ((rq.identity || rq.b >= n) ? 1 : 0);
     a.order = OrderSpec{rq.select, pr.sel_cum, pr.sel_W};
+    a.vref = rq.vref;
+    a.etrace = rq.etrace;
+    a.etrace_len = rq.etrace_len;
     a.mode = rq.mode;
     a.pi_given = rq.pi_given ? 1 : 0;
     a.eps = rq.eps;

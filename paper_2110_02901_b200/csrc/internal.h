@@ -45,6 +45,11 @@ struct SolveRequest {
     bool fused = false;      // RMB_FUSED: multi-rank solve with the in-kernel peer-memory exchange
     int select = 0;          // 0: partition (R2); 1 / 2: draws with replacement, uniform / weighted (R28-R29)
     bool async = false;      // RMB_ASYNC: no batch barrier, reads of V as found in memory (R31)
+    // RMB_TRACE_ERROR_VS_REF: etrace[i] = ||V_i - vref||_inf after operator
+    // application i of the launch (device, zeroed by the caller); null = off
+    const double* vref = nullptr;
+    double* etrace = nullptr;
+    int64_t etrace_len = 0;
     double eps = -1.0;       // < 0: no convergence test
     int64_t max_iter = 1;    // VI: sweeps; MPI: outer iterations
     int msweeps = 1;         // MPI evaluation sweeps per outer iteration
@@ -128,6 +133,11 @@ struct Problem {
     DevBuf sel_buf;
     const uint64_t* sel_cum = nullptr;
     uint64_t sel_W = 0;
+    // reference V* for RMB_TRACE_ERROR_VS_REF (rmb_set_reference) and the
+    // last solve's error trace (rmb_error_trace)
+    DevBuf ref_buf, etrace;
+    bool has_ref = false;
+    int64_t etrace_count = 0;
     cudaStream_t stream = nullptr;
     int device = 0;
     int num_sms = 0;

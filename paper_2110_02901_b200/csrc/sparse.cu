@@ -80,6 +80,9 @@ struct SparseArgs {
     // re-copied values a batch's own new values supersede
     uint32_t* mark;
     int asyn;  // RMB_ASYNC (R31): one buffer X0, no batch barrier, b = n
+    const double* vref;  // RMB_TRACE_ERROR_VS_REF (null = off)
+    double* etrace;
+    int64_t etrace_len;
     unsigned long long* bar;
     int* err;
     unsigned long long* red;  // [4] residual bits ring, [4..8) nonfinite ring, [8..12) changed ring
@@ -751,6 +754,18 @@ enum SKind : int {
     SK_IMPROVE = 3,  // one policy improvement
 };
 
+// error trace after application `it`: X[gb & 1] is the interim V after the
+// application's last barrier; the next batch writes only the other buffer --
+// except asynchronous applications (one buffer): a barrier then keeps the next
+// application's writes out of the pass
+__device__ __forceinline__ void sparse_trace_error(const SparseArgs& a, SCtx& x, int64_t it)
+{
+    const double* Xc = (x.gb & 1) ? a.X1 : a.X0;
+    trace_error([&](int64_t j) { return __ldcg(Xc + j); }, a.vref, a.n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                (int64_t)gridDim.x * blockDim.x, a.etrace + it);
+    if (a.asyn) grid_sync(x.g);
+}
+
 template <typename PT, int MODE, int KIND>
 __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(const SparseArgs a)
 {
@@ -789,6 +804,7 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
             SweepResult r = run_sweep<PT, MODE, KIND == SK_EVAL>(a, x, k, KIND == SK_EVAL ? a.pw0 : nullptr, pre,
                                                                   have, chain);
             if (lead && it < a.trace_len) a.trace[it] = r.r;
+            if (a.etrace && it < a.etrace_len) sparse_trace_error(a, x, it);
             ++it;
             ++k;
             last = r.r;
@@ -817,6 +833,7 @@ __global__ void __launch_bounds__(SThreads<MODE>::v, 1) sparse_solver_kernel(con
             for (int e = 0; e < a.msweeps && !bad; ++e) {
                 SweepResult r = run_sweep<PT, MODE, true>(a, x, k, pol, pre, have, e + 1 < a.msweeps);
                 if (lead && row + e < a.trace_len) a.trace[row + e] = r.r;
+                if (a.etrace && it < a.etrace_len) sparse_trace_error(a, x, it);
                 ++k;
                 ++it;
                 bad = r.bad;
@@ -935,6 +952,9 @@ rmb_status sparse_solve(Problem& pr, const SolveRequest& rq, double* trace_dev, 
     a.msweeps = rq.msweeps;
     a.chunked = rq.chunked ? 1 : 0;
     a.asyn = rq.async ? 1 : 0;
+    a.vref = rq.vref;
+    a.etrace = rq.etrace;
+    a.etrace_len = rq.etrace_len;
     if (rq.async) a.b = n;  // one pass per application, no batch barrier
     int mode, GS, GSE;
     sparse_layout(pr, mode, GS, GSE);
