@@ -389,6 +389,15 @@ def other_configs(rmb, torch, dev):
                 "hbm_algorithmic_GB_per_s": algo / st.seconds / 1e9, "frac": algo / st.seconds / 1e9 / peak,
                 "note": "64 batches per evaluation sweep: per-batch latency (grid barrier ~2.5 us + one V-gather "
                         "round trip) and L2 capacity (two 33.5 MB copies of V) bound it: profiles/r02"})
+    sol = prob.mpi(65536, 10, seed=0, eps=1e-6, max_outer=100_000, asynchronous=True)
+    st = sol.stats
+    backups = st.sweeps * n + (st.outer_iters + 1) * n * 4
+    algo = st.sweeps * (n * 48 + 16 * n) + (st.outer_iters + 1) * (n * 4 * 40 + n * 4 * 4 + 8 * n)
+    out.append({"workload": "config 4, asynchronous MB-MPI m=10 (SURVEY 8(f) row 4, R31: evaluation sweeps with no "
+                            "batch barrier, one V buffer)",
+                "status": int(sol.status), "outer_iterations": st.outer_iters, "eval_sweeps": st.sweeps,
+                "time_to_eps_ms": st.seconds * 1e3, "backups_per_s": backups / st.seconds,
+                "hbm_algorithmic_GB_per_s": algo / st.seconds / 1e9, "frac": algo / st.seconds / 1e9 / peak})
     del prob, rp, col, val, c
     torch.cuda.empty_cache()
     return out
