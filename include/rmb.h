@@ -138,7 +138,10 @@ typedef struct {
  *   P: [n][A][n] row-major, P[(s*A + a)*n + j] = p(j | s, a), dtype desc->p_dtype.
  *   c: [n][A], c[s*A + a] = stage cost, same dtype.
  * Device pointers are BORROWED (must outlive the handle; never copied).
- * Host pointers are copied once into owned device memory.
+ * Host pointers are copied once into owned device memory, allocated
+ * stream-ordered from the device's default memory pool; rmb_destroy returns
+ * it to that pool, which keeps it reserved for the next handle (release
+ * threshold raised on first use; cudaMemPoolTrimTo gives it back).
  * The library allocates its workspace here and in the first solve.
  * Errors: INVALID_ARG (sizes, gamma, dtype, NULL pointers), INVALID_MDP
  * (with RMB_VALIDATE), OOM, CUDA. */

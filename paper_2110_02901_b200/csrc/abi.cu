@@ -46,8 +46,21 @@ static rmb_status device_view(Problem& pr, const void* p, size_t bytes, const vo
         *out = p;
         return RMB_OK;
     }
+    // stream-ordered allocation from the device's pool, which keeps freed
+    // memory reserved: a handle created right after another one's destroy
+    // (a new host problem per solve -- the e2e path) reuses it without a
+    // fresh cudaMalloc / cudaFree of gigabytes
+    static bool pool_set = false;
+    if (!pool_set) {
+        cudaMemPool_t mp;
+        if (cudaDeviceGetDefaultMemPool(&mp, pr.device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_set = true;
+    }
     void* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, bytes);
+    cudaError_t e = cudaMallocAsync(&d, bytes, pr.stream);
     if (e != cudaSuccess) return cuda_fail(e, what);
     pr.owned.push_back(d);
     e = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, pr.stream);
@@ -95,7 +108,8 @@ static rmb_status init_problem(Problem& pr, const rmb_desc* d)
 static void free_problem(Problem* pr)
 {
     if (!pr) return;
-    for (void* p : pr->owned) cudaFree(p);
+    for (void* p : pr->owned) cudaFreeAsync(p, pr->stream);
+    if (!pr->owned.empty()) cudaStreamSynchronize(pr->stream);
     pr->perm.release();
     pr->part.release();
     pr->ctrl.release();
