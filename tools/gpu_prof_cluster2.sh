@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+python tools/prof_cluster.py > gpurun_out/prof_cluster_plain.log 2>&1; cat gpurun_out/prof_cluster_plain.log
+ncu --set full --import-source on --clock-control none -k regex:dense_cluster_kernel -c 1 -o gpurun_out/prof_cluster_b1 -f \
+    python tools/prof_cluster.py > gpurun_out/prof_cluster_ncu.log 2>&1
+echo "ncu rc=$?"
+ncu -i gpurun_out/prof_cluster_b1.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_cluster_b1_sass.csv 2>&1
+echo "src rc=$?"; wc -l gpurun_out/prof_cluster_b1_sass.csv
