@@ -412,8 +412,9 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
             while (issued < consumed + a.ring && may_issue(ck, 0)) issue_one(ck, 0);
     }
     if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
-    // drain: bulk copies in flight must land before the CTA exits
-    if (t == 0) {
+    // drain: bulk copies in flight must land before the CTA exits (the
+    // issuing warp's lane 0 holds the issue count)
+    if (warp == kCDot && lane == 0) {
         for (int64_t d = consumed; d < issued; ++d) {
             const int slot = (int)(d % a.ring);
             const unsigned ph = (unsigned)((d / a.ring) & 1);
@@ -434,6 +435,323 @@ __global__ void __launch_bounds__(kCThreads, 1) dense_cluster_kernel(const Clust
         a.prof[2] = (long long)t_comb;
         a.prof[3] = batches + 2;  // cluster barriers (one per batch, one at each end)
         a.out[7] = (long long)t_wait;  // of prof[0]: waiting for the ring
+    }
+}
+
+
+// ------------------------------------------------------------------ b = 1
+// Gauss-Seidel batches (b = 1, <= 16 rows per state) with the dot of the
+// next batch taken OFF the per-batch chain.  Batch u's rows are dotted
+// against V with batch u-1's column left out (its value is not final yet),
+// the owner CTA keeps P(row, s_{u-1}); once batch u-1 is combined, a combine
+// warp adds P(row, s_{u-1}) V(s_{u-1}) to its partial -- the same sum in a
+// different (fixed) order, R26.  Warps 0-7 dot, warp 8 issues the ring, warp
+// 9 corrects, signals every CTA (remote mbarrier arrive, release.cluster),
+// waits for the cluster's partials of the batch, combines them through DSMEM
+// and patches V; the dot warps meanwhile dot batch u+1 (they wait only for
+// batch u-1's patch).  Per batch the chain is correction + cluster signal +
+// combine, not stream + dot + barrier + combine.
+constexpr int kLThreads = 320;  // 8 dot warps + the issuing warp + the combine warp
+constexpr int kLGroup = 288;    // dot + issuing warps (named barrier 1)
+constexpr int kLComb = 9;       // the combine warp
+
+__device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, unsigned rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_cluster(unsigned long long* b, unsigned parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, "
+        "0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+template <typename PT>
+__global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const ClusterArgs a)
+{
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* Vs = reinterpret_cast<double*>(sm + a.v_off);
+    int32_t* pis = reinterpret_cast<int32_t*>(sm + a.pi_off);
+    unsigned char* ring = sm + a.ring_off;
+    double* prt = reinterpret_cast<double*>(sm + a.part_off);  // [3][16] row partials of batch u (slot u % 3)
+    double* pcol = prt + 48;                                      // [3][16] P(row, s_{u-1}) (owner CTA)
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + a.bar_off);  // [ring]
+    unsigned long long* cbar = full + a.ring;  // the cluster's partials of a batch are in (count CS)
+    long long* flg = reinterpret_cast<long long*>(cbar + 1);  // [0] dotted, [1] patched, [2] stop
+    const unsigned q = cluster_rank();
+    const unsigned CS = gridDim.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = a.n;
+    const int Ae = a.eval ? 1 : a.A;  // <= 16
+    const int c0 = min(n, (int)q * a.slab), c1 = min(n, c0 + a.slab);
+    constexpr int E = 16 / (int)sizeof(PT);
+    using VT = typename std::conditional<sizeof(PT) == 4, float4, double2>::type;
+    const int vhalf = sizeof(PT) == 4 ? ((n + 3) & ~3) / 2 : 0;
+    auto vidx = [&](int j) { return vhalf ? ((j & 2) ? vhalf : 0) + ((j >> 2) << 1) + (j & 1) : j; };
+    for (int j = t; j < n; j += kLThreads) {
+        Vs[vidx(j)] = a.V[j];
+        if (a.eval) pis[j] = a.pi[j];
+    }
+    if (t == 0) {
+        for (int s = 0; s < a.ring; ++s) mbar_init(full + s, 1);
+        mbar_init(cbar, CS);
+        flg[0] = flg[1] = -1;
+        flg[2] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (!a.identity)
+        fill_order(n, a.seed, a.k0, a.order, a.perm + (a.k0 % 3) * n, (int64_t)q * kLThreads + t,
+                   (int64_t)CS * kLThreads);
+    cluster_sync();
+
+    const int64_t total = a.max_iter * (int64_t)n;  // batches of the launch
+    auto state_at = [&](int64_t u) -> int {
+        const int64_t k = a.k0 + u / n;
+        const int bi = (int)(u % n);
+        return a.identity ? bi : (int)__ldcg(a.perm + (k % 3) * n + bi);
+    };
+    const PT* P = static_cast<const PT*>(a.P);
+    long long status = RMB_ERR_NOT_CONVERGED;
+    int64_t it = 0, batches = 0;
+    double last = 0.0;
+    int64_t consumed = 0, issued = 0;
+
+    if (warp < kLComb) {
+        // ---------------------------------------------- dot + issuing warps
+        const int64_t last_sweep = a.k0 + a.max_iter - 1;
+        int64_t pk = a.k0;
+        int pb = 0;
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        // the next sweep's order is filled in its predecessor's batch 0, visible
+        // here once batch 0's patch is (acquired with patched >= batch 0, i.e.
+        // from the sweep's batch 2 on)
+        auto may_issue = [&](int64_t cons_k, int cons_b) {
+            return pk <= last_sweep && (pk == cons_k || (pk == cons_k + 1 && cons_b >= 2));
+        };
+        int pre_s = 0;
+        bool pre_ok = false;
+        auto issue_one = [&](int64_t cons_k, int cons_b) {
+            if (pk > last_sweep) return;
+            const int s = pre_ok ? pre_s : (lane < Ae ? state_at((pk - a.k0) * n + pb) : 0);
+            const int act = lane < Ae ? (a.eval ? __ldcg(a.pi + s) : lane) : 0;
+            const int slot = (int)(issued % a.ring);
+            unsigned char* dst = ring + (size_t)slot * a.rows * a.row_bytes;
+            const unsigned bytes = (unsigned)((c1 - c0) * (int)sizeof(PT));
+            if (lane == 0) mbar_arrive_tx(full + slot, bytes * (unsigned)Ae);
+            __syncwarp();
+            if (lane < Ae && bytes > 0)
+                bulk_g2s(dst + (size_t)lane * a.row_bytes, P + ((int64_t)s * a.A + act) * n + c0, bytes, full + slot, pol);
+            ++issued;
+            if (++pb == n) pb = 0, ++pk;
+            pre_ok = may_issue(cons_k, cons_b) && pk <= last_sweep;
+            if (pre_ok) pre_s = lane < Ae ? state_at((pk - a.k0) * n + pb) : 0;
+        };
+        if (warp == kCDot)
+            for (int s = 0; s < a.ring && may_issue(a.k0, 0); ++s) issue_one(a.k0, 0);
+        int s_prev = -1;
+        int s_this = state_at(0);
+        for (int64_t u = 0; u < total; ++u) {
+            const int64_t k = a.k0 + u / n;
+            const int bi = (int)(u % n);
+            // V must hold batch u-2's value (batch u-1's column is left out)
+            if (lane == 0) {
+                SpinGuard sg;
+                while (ld_acquire_cta(flg + 1) < u - 2 && ld_acquire_cta(flg + 2) == 0) sg.tick();
+            }
+            __syncwarp();
+            if (ld_acquire_cta(flg + 2) != 0) break;
+            const int s_next = u + 1 < total ? state_at(u + 1) : 0;  // in flight during this batch
+            if (warp == kCDot)
+                while (issued < consumed + a.ring && may_issue(k, bi)) issue_one(k, bi);
+            const int slot = (int)(consumed % a.ring);
+            const unsigned ph = (unsigned)((consumed / a.ring) & 1);
+            {
+                SpinGuard sg;
+                while (!mbar_try(full + slot, ph)) sg.tick();
+            }
+            const unsigned char* stg = ring + (size_t)slot * a.rows * a.row_bytes;
+            const int nv = (c1 - c0) / E;
+            const int jx = (s_prev >= c0 && s_prev < c1) ? s_prev - c0 : -1;  // column left out (this CTA's)
+            double* pr = prt + (u % 3) * 16;
+            if (warp < kCDot && warp < Ae) {
+                const bool two = warp + kCDot < Ae;
+                const VT* row0 = reinterpret_cast<const VT*>(stg + (size_t)warp * a.row_bytes);
+                const VT* row1 = reinterpret_cast<const VT*>(stg + (size_t)(warp + kCDot) * a.row_bytes);
+                double acc0 = 0.0, acc1 = 0.0;
+                for (int v = lane; v < nv; v += kWarp) {
+                    const int j = c0 + v * E;
+                    double vs[E];
+                    if constexpr (sizeof(PT) == 4) {
+                        const double2 lo = *reinterpret_cast<const double2*>(Vs + (j >> 1));
+                        const double2 hi = *reinterpret_cast<const double2*>(Vs + vhalf + (j >> 1));
+                        vs[0] = lo.x, vs[1] = lo.y, vs[2] = hi.x, vs[3] = hi.y;
+                    } else {
+                        const double2 x = *reinterpret_cast<const double2*>(Vs + j);
+                        vs[0] = x.x, vs[1] = x.y;
+                    }
+                    if (jx >= v * E && jx < v * E + E) vs[jx - v * E] = 0.0;
+                    const VT x0 = row0[v];
+                    const double p0[4] = {(double)x0.x, (double)x0.y, sizeof(PT) == 4 ? (double)((const float*)&x0)[2] : 0.0,
+                                          sizeof(PT) == 4 ? (double)((const float*)&x0)[3] : 0.0};
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc0 = fma(p0[e], vs[e], acc0);
+                    if (two) {
+                        const VT x1 = row1[v];
+                        const double p1[4] = {(double)x1.x, (double)x1.y,
+                                              sizeof(PT) == 4 ? (double)((const float*)&x1)[2] : 0.0,
+                                              sizeof(PT) == 4 ? (double)((const float*)&x1)[3] : 0.0};
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc1 = fma(p1[e], vs[e], acc1);
+                    }
+                }
+                acc0 = warp_sum(acc0);
+                acc1 = warp_sum(acc1);
+                if (lane == 0) {
+                    pr[warp] = acc0;
+                    if (two) pr[warp + kCDot] = acc1;
+                }
+            }
+            if (jx >= 0 && t < Ae)  // the left-out column's P, for the correction
+                pcol[(u % 3) * 16 + t] = (double)reinterpret_cast<const PT*>(stg + (size_t)t * a.row_bytes)[jx];
+            if (bi == 0 && !a.identity)  // the next sweep's order (covered by this batch's signal)
+                fill_order(n, a.seed, k + 1, a.order, a.perm + ((k + 1) % 3) * n, (int64_t)q * kLGroup + t,
+                           (int64_t)CS * kLGroup);
+            bar_sync_n<kLGroup>();  // the ring slot is free; partials and pcol written
+            if (t == 0) st_release_cta(flg, u);
+            ++consumed;
+            s_prev = s_this;
+            s_this = s_next;
+        }
+    } else {
+        // ---------------------------------------------------- combine warp
+        int L = 1;  // lanes per state in the argmin (pow2 >= Ae)
+        while (L < Ae) L <<= 1;
+        int s_cur = state_at(0), s_prev = -1;
+        int s_nx = total > 1 ? state_at(1) : 0;
+        auto cost = [&](int s) -> double {
+            return lane < Ae ? (double)__ldg(static_cast<const PT*>(a.c) + (int64_t)s * a.A + (a.eval ? pis[s] : lane))
+                             : 0.0;
+        };
+        double cc = cost(s_cur);
+        double rmax = 0.0;
+        int bad = 0;
+        bool stop = false;
+        // phase profile of CTA 0's combine warp: waiting for the dot warps,
+        // correction + cluster exchange, combine + patch
+        const bool prof = q == 0 && lane == 0;
+        unsigned long long tm = prof ? globaltimer_ns() : 0, t_dot = 0, t_x = 0, t_cb = 0;
+        auto mark = [&](unsigned long long& acc) {
+            if (prof) {
+                const unsigned long long now = globaltimer_ns();
+                acc += now - tm;
+                tm = now;
+            }
+        };
+        for (int64_t u = 0; u < total && !stop; ++u) {
+            const int bi = (int)(u % n);
+            if (lane == 0) {
+                SpinGuard sg;
+                while (ld_acquire_cta(flg) < u) sg.tick();
+            }
+            __syncwarp();
+            mark(t_dot);
+            double* pr = prt + (u % 3) * 16;
+            if (s_prev >= c0 && s_prev < c1 && lane < Ae)  // the left-out column, now final
+                pr[lane] = fma(pcol[(u % 3) * 16 + lane], Vs[vidx(s_prev)], pr[lane]);
+            __syncwarp();
+            if ((unsigned)lane < CS) mbar_arrive_remote(cbar, (unsigned)lane);
+            {
+                SpinGuard sg;
+                while (!mbar_try_cluster(cbar, (unsigned)(u & 1))) sg.tick();
+            }
+            mark(t_x);
+            double Q = INFINITY;
+            int arg = 0x7fffffff;
+            if (lane < Ae) {
+                double pv[16];
+#pragma unroll
+                for (unsigned cq = 0; cq < 16; ++cq) pv[cq] = cq < CS ? *dsmem(pr + lane, cq) : 0.0;
+                double sum = 0.0;
+#pragma unroll
+                for (unsigned cq = 0; cq < 16; ++cq)
+                    if (cq < CS) sum += pv[cq];
+                Q = cc + a.gamma * sum;
+                arg = a.eval ? pis[s_cur] : lane;
+            }
+            for (int o = 1; o < L; o <<= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, Q, o);
+                const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                if (ov < Q || (ov == Q && oa < arg)) Q = ov, arg = oa;
+            }
+            if (lane == 0) {
+                rmax = fmax(rmax, fabs(Q - Vs[vidx(s_cur)]));
+                bad |= !isfinite(Q);
+                Vs[vidx(s_cur)] = Q;
+                if (q == 0) {
+                    a.V[s_cur] = Q;
+                    if (!a.eval && a.pi) a.pi[s_cur] = arg;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) st_release_cta(flg + 1, u);
+            mark(t_cb);
+            ++batches;
+            s_prev = s_cur;
+            s_cur = s_nx;
+            s_nx = u + 2 < total ? state_at(u + 2) : 0;
+            cc = u + 1 < total ? cost(s_cur) : 0.0;
+            if (bi == n - 1) {  // end of a sweep: every CTA holds the same residual
+                const double r = __shfl_sync(0xffffffffu, rmax, 0);
+                const int bb = __shfl_sync(0xffffffffu, bad, 0);
+                if (q == 0 && lane == 0 && it < a.trace_len) a.trace[it] = r;
+                if (a.etrace && it < a.etrace_len)
+                    trace_error([&](int64_t j) { return Vs[vidx((int)j)]; }, a.vref, n, (int64_t)q * kWarp + lane,
+                                (int64_t)CS * kWarp, a.etrace + it);
+                ++it;
+                last = r;
+                rmax = 0.0;
+                bad = 0;
+                if (bb) status = RMB_ERR_NONFINITE, stop = true;
+                else if (a.eps >= 0.0 && r <= a.eps) status = RMB_OK, stop = true;
+            }
+        }
+        if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
+        if (lane == 0) st_release_cta(flg + 2, 1);  // the dot warps stop
+        if (prof) {
+            a.prof[0] = (long long)t_dot;  // waiting for the dot warps
+            a.prof[1] = (long long)t_x;    // correction + the cluster exchange of the partials
+            a.prof[2] = (long long)t_cb;   // DSMEM combine + patch
+        }
+    }
+    __syncthreads();
+    // drain: bulk copies in flight must land before the CTA exits (the
+    // issuing warp's lane 0 holds the issue count)
+    if (warp == kCDot && lane == 0) {
+        for (int64_t d = consumed; d < issued; ++d) {
+            const int slot = (int)(d % a.ring);
+            const unsigned ph = (unsigned)((d / a.ring) & 1);
+            SpinGuard sg;
+            while (!mbar_try(full + slot, ph)) sg.tick();
+        }
+    }
+    cluster_sync();  // no CTA exits while another may still read its shared memory
+    if (q == 0 && warp == kLComb && lane == 0) {
+        a.out[OUT_SWEEPS] = it;
+        a.out[OUT_OUTER] = 0;
+        a.out[OUT_STATUS] = status;
+        a.out[OUT_RESID_BITS] = __double_as_longlong(last);
+        a.out[OUT_BATCHES] = batches;
+        a.out[OUT_CHANGED] = 0;
+        a.prof[3] = batches + 2;  // one cluster-wide exchange per batch + the barriers at both ends
+        a.out[7] = 0;
     }
 }
 
@@ -458,15 +776,15 @@ bool dense_cluster_eligible(const Problem& pr, const SolveRequest& rq)
 }
 
 template <typename PT>
-static cudaError_t launch_cluster(const ClusterArgs& a, int CS, size_t smem, cudaStream_t st)
+static cudaError_t launch_cluster(const ClusterArgs& a, int CS, size_t smem, cudaStream_t st, bool la)
 {
-    auto kern = dense_cluster_kernel<PT>;
+    auto kern = la ? dense_cluster_la_kernel<PT> : dense_cluster_kernel<PT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(kCThreads);
+    cfg.blockDim = dim3(la ? kLThreads : kCThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -545,7 +863,7 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
         a.v_off = take((size_t)n * 8);
         a.pi_off = take(eval ? (size_t)n * 4 : 16);
         a.part_off = take((size_t)2 * kCBatchRows * 8);
-        a.bar_off = take(8 * 8);
+        a.bar_off = take(32 * 8);  // ring mbarriers (<= 8), the b = 1 kernel's cluster mbarrier and flags
         const int64_t room = (int64_t)pr.smem_optin - (int64_t)off - 1024;
         const int Ae = eval ? 1 : pr.A;
         a.rows = (int)std::min<int64_t>(kCRowsMax, std::min<int64_t>(rq.b * Ae, room / (2 * a.row_bytes)));
@@ -576,8 +894,14 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     cudaEventCreate(&e1);
     cudaError_t ce = cudaMemsetAsync(ctrl, 0, 4096, st);
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
+    // Gauss-Seidel batches (b = 1, <= 16 rows): the look-ahead kernel
+#ifndef RMB_AB_NO_CLUSTER_LA
+    const bool la = rq.b == 1 && (eval ? 1 : pr.A) <= 16 && n >= 4;
+#else
+    const bool la = false;
+#endif
     if (ce == cudaSuccess)
-        ce = pr.pdt == RMB_F32 ? launch_cluster<float>(a, CS, smem, st) : launch_cluster<double>(a, CS, smem, st);
+        ce = pr.pdt == RMB_F32 ? launch_cluster<float>(a, CS, smem, st, la) : launch_cluster<double>(a, CS, smem, st, la);
     if (ce == cudaSuccess) ce = cudaEventRecord(e1, st);
     long long out[OUT_N + 4] = {0};
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, a.out, sizeof(long long) * OUT_N, cudaMemcpyDeviceToHost, st);
