@@ -461,6 +461,17 @@ __device__ __forceinline__ void mbar_arrive_remote(unsigned long long* bar, unsi
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(bar)), "r"(rank));
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
 }
+// 8-byte store into CTA `rank`'s shared memory, completing 8 bytes of its
+// mbarrier `bar` (same offsets in every CTA of the cluster)
+__device__ __forceinline__ void st_async_remote(double* dst, double v, unsigned long long* bar, unsigned rank)
+{
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_addr(bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra),
+                 "l"(__double_as_longlong(v)), "r"(rb)
+                 : "memory");
+}
 __device__ __forceinline__ bool mbar_try_cluster(unsigned long long* b, unsigned parity)
 {
     uint32_t ok;
@@ -480,11 +491,13 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
     double* Vs = reinterpret_cast<double*>(sm + a.v_off);
     int32_t* pis = reinterpret_cast<int32_t*>(sm + a.pi_off);
     unsigned char* ring = sm + a.ring_off;
-    double* prt = reinterpret_cast<double*>(sm + a.part_off);  // [3][16] row partials of batch u (slot u % 3)
-    double* pcol = prt + 48;                                      // [3][16] P(row, s_{u-1}) (owner CTA)
+    // batch u's slot u % 4 (received from every CTA by st.async): [16 CTAs][16 rows]
+    // row partials, then [16] coefficients P(row, s_{u-1}) from the column's owner
+    double* xb = reinterpret_cast<double*>(sm + a.part_off);
+    constexpr int kXSlot = 16 * 16 + 16;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + a.bar_off);  // [ring]
-    unsigned long long* cbar = full + a.ring;  // the cluster's partials of a batch are in (count CS)
-    long long* flg = reinterpret_cast<long long*>(cbar + 1);  // [0] dotted, [1] patched, [2] stop
+    unsigned long long* xbar = full + a.ring;  // [4] batch u's data has arrived (slot u % 4)
+    long long* flg = reinterpret_cast<long long*>(xbar + 4);  // [1] patched, [2] stop
     const unsigned q = cluster_rank();
     const unsigned CS = gridDim.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -499,19 +512,24 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         Vs[vidx(j)] = a.V[j];
         if (a.eval) pis[j] = a.pi[j];
     }
+    const int64_t total = a.max_iter * (int64_t)n;  // batches of the launch
+    // bytes batch u brings into every CTA: CS x Ae partials, plus Ae coefficients
+    // from the owner of column s_{u-1} (none for the launch's first batch)
+    auto xbytes = [&](int64_t u) { return (unsigned)((CS * Ae + (u > 0 ? Ae : 0)) * 8); };
     if (t == 0) {
         for (int s = 0; s < a.ring; ++s) mbar_init(full + s, 1);
-        mbar_init(cbar, CS);
-        flg[0] = flg[1] = -1;
+        for (int s = 0; s < 4; ++s) mbar_init(xbar + s, 1);
+        flg[1] = -1;
         flg[2] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (t == 0)  // slots armed for batches 0..3 (re-armed after each batch's combine)
+        for (int s = 0; s < 4 && s < total; ++s) mbar_arrive_tx(xbar + s, xbytes(s));
     if (!a.identity)
         fill_order(n, a.seed, a.k0, a.order, a.perm + (a.k0 % 3) * n, (int64_t)q * kLThreads + t,
                    (int64_t)CS * kLThreads);
     cluster_sync();
 
-    const int64_t total = a.max_iter * (int64_t)n;  // batches of the launch
     auto state_at = [&](int64_t u) -> int {
         const int64_t k = a.k0 + u / n;
         const int bi = (int)(u % n);
@@ -580,7 +598,8 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
             const unsigned char* stg = ring + (size_t)slot * a.rows * a.row_bytes;
             const int nv = (c1 - c0) / E;
             const int jx = (s_prev >= c0 && s_prev < c1) ? s_prev - c0 : -1;  // column left out (this CTA's)
-            double* pr = prt + (u % 3) * 16;
+            double* xs = xb + (u % 4) * kXSlot;
+            unsigned long long* xu = xbar + (u % 4);
             if (warp < kCDot && warp < Ae) {
                 const bool two = warp + kCDot < Ae;
                 const VT* row0 = reinterpret_cast<const VT*>(stg + (size_t)warp * a.row_bytes);
@@ -614,18 +633,22 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
                 }
                 acc0 = warp_sum(acc0);
                 acc1 = warp_sum(acc1);
-                if (lane == 0) {
-                    pr[warp] = acc0;
-                    if (two) pr[warp + kCDot] = acc1;
-                }
+                // to every CTA: lane l < CS row `warp`, lane 16 + l row `warp + 8`
+                const unsigned dst = lane & 15;
+                if (dst < CS && (lane < 16 || two))
+                    st_async_remote(xs + q * 16 + warp + (lane < 16 ? 0 : kCDot), lane < 16 ? acc0 : acc1, xu, dst);
             }
-            if (jx >= 0 && t < Ae)  // the left-out column's P, for the correction
-                pcol[(u % 3) * 16 + t] = (double)reinterpret_cast<const PT*>(stg + (size_t)t * a.row_bytes)[jx];
+            if (jx >= 0 && t < 16 * 16) {  // the left-out column's P (owner): thread r + 16 d -> row r, CTA d
+                const int r = t & 15, d = t >> 4;
+                if (r < Ae && (unsigned)d < CS)
+                    st_async_remote(xs + 16 * 16 + r,
+                                    (double)reinterpret_cast<const PT*>(stg + (size_t)r * a.row_bytes)[jx], xu,
+                                    (unsigned)d);
+            }
             if (bi == 0 && !a.identity)  // the next sweep's order (covered by this batch's signal)
                 fill_order(n, a.seed, k + 1, a.order, a.perm + ((k + 1) % 3) * n, (int64_t)q * kLGroup + t,
                            (int64_t)CS * kLGroup);
-            bar_sync_n<kLGroup>();  // the ring slot is free; partials and pcol written
-            if (t == 0) st_release_cta(flg, u);
+            bar_sync_n<kLGroup>();  // every warp is done with the ring slot
             ++consumed;
             s_prev = s_this;
             s_this = s_next;
@@ -647,7 +670,7 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         // phase profile of CTA 0's combine warp: waiting for the dot warps,
         // correction + cluster exchange, combine + patch
         const bool prof = q == 0 && lane == 0;
-        unsigned long long tm = prof ? globaltimer_ns() : 0, t_dot = 0, t_x = 0, t_cb = 0;
+        unsigned long long tm = prof ? globaltimer_ns() : 0, t_x = 0, t_cb = 0;
         auto mark = [&](unsigned long long& acc) {
             if (prof) {
                 const unsigned long long now = globaltimer_ns();
@@ -657,32 +680,18 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         };
         for (int64_t u = 0; u < total && !stop; ++u) {
             const int bi = (int)(u % n);
-            if (lane == 0) {
-                SpinGuard sg;
-                while (ld_acquire_cta(flg) < u) sg.tick();
-            }
-            __syncwarp();
-            mark(t_dot);
-            double* pr = prt + (u % 3) * 16;
-            if (s_prev >= c0 && s_prev < c1 && lane < Ae)  // the left-out column, now final
-                pr[lane] = fma(pcol[(u % 3) * 16 + lane], Vs[vidx(s_prev)], pr[lane]);
-            __syncwarp();
-            if ((unsigned)lane < CS) mbar_arrive_remote(cbar, (unsigned)lane);
+            const double* xs = xb + (u % 4) * kXSlot;
             {
                 SpinGuard sg;
-                while (!mbar_try_cluster(cbar, (unsigned)(u & 1))) sg.tick();
+                while (!mbar_try_cluster(xbar + (u % 4), (unsigned)((u / 4) & 1))) sg.tick();
             }
             mark(t_x);
             double Q = INFINITY;
             int arg = 0x7fffffff;
             if (lane < Ae) {
-                double pv[16];
-#pragma unroll
-                for (unsigned cq = 0; cq < 16; ++cq) pv[cq] = cq < CS ? *dsmem(pr + lane, cq) : 0.0;
                 double sum = 0.0;
-#pragma unroll
-                for (unsigned cq = 0; cq < 16; ++cq)
-                    if (cq < CS) sum += pv[cq];
+                for (unsigned cq = 0; cq < CS; ++cq) sum += xs[cq * 16 + lane];  // CTA order
+                if (u > 0) sum = fma(xs[16 * 16 + lane], Vs[vidx(s_prev)], sum);  // the left-out column
                 Q = cc + a.gamma * sum;
                 arg = a.eval ? pis[s_cur] : lane;
             }
@@ -701,7 +710,10 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
                 }
             }
             __syncwarp();
-            if (lane == 0) st_release_cta(flg + 1, u);
+            if (lane == 0) {
+                if (u + 4 < total) mbar_arrive_tx(xbar + (u % 4), xbytes(u + 4));  // the slot, for batch u + 4
+                st_release_cta(flg + 1, u);
+            }
             mark(t_cb);
             ++batches;
             s_prev = s_cur;
@@ -726,9 +738,9 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
         if (lane == 0) st_release_cta(flg + 2, 1);  // the dot warps stop
         if (prof) {
-            a.prof[0] = (long long)t_dot;  // waiting for the dot warps
-            a.prof[1] = (long long)t_x;    // correction + the cluster exchange of the partials
-            a.prof[2] = (long long)t_cb;   // DSMEM combine + patch
+            a.prof[0] = 0;
+            a.prof[1] = (long long)t_x;    // waiting for the batch's partials from every CTA
+            a.prof[2] = (long long)t_cb;   // combine + patch
         }
     }
     __syncthreads();
@@ -862,7 +874,7 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
         };
         a.v_off = take((size_t)n * 8);
         a.pi_off = take(eval ? (size_t)n * 4 : 16);
-        a.part_off = take((size_t)2 * kCBatchRows * 8);
+        a.part_off = take(std::max<size_t>((size_t)2 * kCBatchRows * 8, (size_t)4 * (16 * 16 + 16) * 8));
         a.bar_off = take(32 * 8);  // ring mbarriers (<= 8), the b = 1 kernel's cluster mbarrier and flags
         const int64_t room = (int64_t)pr.smem_optin - (int64_t)off - 1024;
         const int Ae = eval ? 1 : pr.A;
