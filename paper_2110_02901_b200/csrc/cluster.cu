@@ -549,10 +549,10 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         // the next sweep's order is filled in its predecessor's batch 0, visible
-        // here once batch 0's patch is (acquired with patched >= batch 0, i.e.
-        // from the sweep's batch 2 on)
+        // here once batch 0's patch is (acquired with patched >= batch 0 in the
+        // sweep's batch 2; the refill at the top of batch 3 comes after it)
         auto may_issue = [&](int64_t cons_k, int cons_b) {
-            return pk <= last_sweep && (pk == cons_k || (pk == cons_k + 1 && cons_b >= 2));
+            return pk <= last_sweep && (pk == cons_k || (pk == cons_k + 1 && cons_b >= 3));
         };
         int pre_s = 0;
         bool pre_ok = false;
@@ -579,16 +579,28 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
         for (int64_t u = 0; u < total; ++u) {
             const int64_t k = a.k0 + u / n;
             const int bi = (int)(u % n);
-            // V must hold batch u-2's value (batch u-1's column is left out)
-            if (lane == 0) {
-                SpinGuard sg;
-                while (ld_acquire_cta(flg + 1) < u - 2 && ld_acquire_cta(flg + 2) == 0) sg.tick();
-            }
-            __syncwarp();
-            if (ld_acquire_cta(flg + 2) != 0) break;
-            const int s_next = u + 1 < total ? state_at(u + 1) : 0;  // in flight during this batch
+            // refill the ring first (the slot of batch u-1 is free): the copies
+            // must not wait for the patch below
             if (warp == kCDot)
                 while (issued < consumed + a.ring && may_issue(k, bi)) issue_one(k, bi);
+            if (bi == 0 && u > 0) {
+                // a new sweep: the combine warp's verdict on the previous one first
+                // (published with the patch of its last batch).  One thread reads
+                // it and the group follows: per-warp reads could split the group
+                // across the named barrier at the end of the batch
+                if (t == 0) {
+                    SpinGuard sg;
+                    while (ld_acquire_cta(flg + 1) < u - 1) sg.tick();
+                    flg[3] = ld_acquire_cta(flg + 2);
+                }
+                bar_sync_n<kLGroup>();
+                if (flg[3] != 0) break;
+            } else if (lane == 0) {  // V must hold batch u-2's value (batch u-1's column is left out)
+                SpinGuard sg;
+                while (ld_acquire_cta(flg + 1) < u - 2) sg.tick();
+            }
+            __syncwarp();
+            const int s_next = u + 1 < total ? state_at(u + 1) : 0;  // in flight during this batch
             const int slot = (int)(consumed % a.ring);
             const unsigned ph = (unsigned)((consumed / a.ring) & 1);
             {
@@ -710,16 +722,6 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
                 }
             }
             __syncwarp();
-            if (lane == 0) {
-                if (u + 4 < total) mbar_arrive_tx(xbar + (u % 4), xbytes(u + 4));  // the slot, for batch u + 4
-                st_release_cta(flg + 1, u);
-            }
-            mark(t_cb);
-            ++batches;
-            s_prev = s_cur;
-            s_cur = s_nx;
-            s_nx = u + 2 < total ? state_at(u + 2) : 0;
-            cc = u + 1 < total ? cost(s_cur) : 0.0;
             if (bi == n - 1) {  // end of a sweep: every CTA holds the same residual
                 const double r = __shfl_sync(0xffffffffu, rmax, 0);
                 const int bb = __shfl_sync(0xffffffffu, bad, 0);
@@ -733,7 +735,18 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
                 bad = 0;
                 if (bb) status = RMB_ERR_NONFINITE, stop = true;
                 else if (a.eps >= 0.0 && r <= a.eps) status = RMB_OK, stop = true;
+                if (stop && lane == 0) flg[2] = 1;  // published by the release of this batch's patch
             }
+            if (lane == 0) {
+                if (u + 4 < total) mbar_arrive_tx(xbar + (u % 4), xbytes(u + 4));  // the slot, for batch u + 4
+                st_release_cta(flg + 1, u);
+            }
+            mark(t_cb);
+            ++batches;
+            s_prev = s_cur;
+            s_cur = s_nx;
+            s_nx = u + 2 < total ? state_at(u + 2) : 0;
+            cc = u + 1 < total ? cost(s_cur) : 0.0;
         }
         if (a.eps < 0.0 && status == RMB_ERR_NOT_CONVERGED) status = RMB_OK;
         if (lane == 0) st_release_cta(flg + 2, 1);  // the dot warps stop
@@ -908,7 +921,7 @@ rmb_status dense_cluster_solve(Problem& pr, const SolveRequest& rq, double* trac
     if (ce == cudaSuccess) ce = cudaEventRecord(e0, st);
     // Gauss-Seidel batches (b = 1, <= 16 rows): the look-ahead kernel
 #ifndef RMB_AB_NO_CLUSTER_LA
-    const bool la = rq.b == 1 && (eval ? 1 : pr.A) <= 16 && n >= 4;
+    const bool la = rq.b == 1 && (eval ? 1 : pr.A) <= 16 && n >= 5;
 #else
     const bool la = false;
 #endif
