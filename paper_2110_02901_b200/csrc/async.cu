@@ -36,12 +36,10 @@ namespace {
 
 // threads per CTA: 4 CTAs of 128 per SM (tools/ab_async.py on config 2: 512 x 1
 // 1.43 ms per application, 256 x 2 1.17, 128 x 4 1.12, 64 x 8 1.08 but more
-// states in flight -> more applications to eps; A/B builds only override it)
+// states in flight -> more applications to eps; a software-pipelined column
+// loop measured 1.10, not kept; A/B builds only override these)
 #ifndef RMB_ASYNC_NT
 #define RMB_ASYNC_NT 128
-#endif
-#ifndef RMB_ASYNC_DB  // software-pipelined column loop, rows per pass capped at RMB_ASYNC_AGMAX
-#define RMB_ASYNC_DB 0
 #endif
 #ifndef RMB_ASYNC_AGMAX
 #define RMB_ASYNC_AGMAX 16
@@ -137,36 +135,6 @@ __device__ __forceinline__ void state_rows(const AsyncArgs& a, int64_t s, const 
     for (int r = 0; r < AG; ++r) acc[r] = 0.0;
     // the rows of one call are consecutive actions (min) or the single row pi(s)
     const PT* base = P + ((int64_t)s * a.A + rows[0]) * n;
-#if RMB_ASYNC_DB
-    // software pipelined: the next column block's rows are in flight while
-    // this block's FMAs run
-    int64_t j = (int64_t)threadIdx.x * VE;
-    PVec<PT, VE> x[AG];
-    if (j < n) {
-#pragma unroll
-        for (int r = 0; r < AG; ++r)
-            if (r < na) x[r] = ld_p<PT, VE>(base + (int64_t)r * n + j, pol);
-    }
-    for (; j < n; j += (int64_t)kAThreads * VE) {
-        const int64_t jn = j + (int64_t)kAThreads * VE;
-        PVec<PT, VE> y[AG];
-        if (jn < n) {
-#pragma unroll
-            for (int r = 0; r < AG; ++r)
-                if (r < na) y[r] = ld_p<PT, VE>(base + (int64_t)r * n + jn, pol);
-        }
-        double v[VE];
-        ld_v<VE>(a.V, j, v);
-#pragma unroll
-        for (int r = 0; r < AG; ++r)
-            if (r < na) {
-#pragma unroll
-                for (int e = 0; e < VE; ++e) acc[r] = fma((double)x[r].x[e], v[e], acc[r]);
-            }
-#pragma unroll
-        for (int r = 0; r < AG; ++r) x[r] = y[r];
-    }
-#else
     for (int64_t j = (int64_t)threadIdx.x * VE; j < n; j += (int64_t)kAThreads * VE) {
         PVec<PT, VE> x[AG];
 #pragma unroll
@@ -181,7 +149,7 @@ __device__ __forceinline__ void state_rows(const AsyncArgs& a, int64_t s, const 
                 for (int e = 0; e < VE; ++e) acc[r] = fma((double)x[r].x[e], v[e], acc[r]);
             }
     }
-#endif
+
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int r = 0; r < AG; ++r) {
