@@ -88,7 +88,9 @@ typedef struct {
                                    and chunking (DESIGN reading R21).  Not for sharded handles.        */
 #define RMB_DENSE_NO_CLUSTER 0x1000u /* rmb_create_dense: never use the one-cluster solver for tiny batches
                                       (<= 2 MB of P and <= 256 rows per batch: 16 CTAs, DSMEM combine,
-                                      hardware cluster barrier); results agree to fp64 rounding        */
+                                      hardware cluster barrier; b = 1 with <= 16 rows: a look-ahead
+                                      kernel exchanging partials by st.async); results agree to fp64
+                                      rounding                                                          */
 #define RMB_SELECT_REPLACE 0x2000u  /* rmb_vi / rmb_mpi / rmb_apply: SURVEY 8(f) row 4, P:L605 ("sampling the
                                        states with replacement and/or according to a non-uniform
                                        distribution") -- every operator application draws n states
