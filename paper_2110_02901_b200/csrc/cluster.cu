@@ -628,7 +628,10 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
                         const double2 x = *reinterpret_cast<const double2*>(Vs + j);
                         vs[0] = x.x, vs[1] = x.y;
                     }
-                    if (jx >= v * E && jx < v * E + E) vs[jx - v * E] = 0.0;
+                    // the left-out column: a select per element (a dynamic index
+                    // would put vs[] in local memory)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) vs[e] = (jx == v * E + e) ? 0.0 : vs[e];
                     const VT x0 = row0[v];
                     const double p0[4] = {(double)x0.x, (double)x0.y, sizeof(PT) == 4 ? (double)((const float*)&x0)[2] : 0.0,
                                           sizeof(PT) == 4 ? (double)((const float*)&x0)[3] : 0.0};
@@ -695,7 +698,8 @@ __global__ void __launch_bounds__(kLThreads, 1) dense_cluster_la_kernel(const Cl
             const double* xs = xb + (u % 4) * kXSlot;
             {
                 SpinGuard sg;
-                while (!mbar_try_cluster(xbar + (u % 4), (unsigned)((u / 4) & 1))) sg.tick();
+                // st.async data is visible to the CTA once the mbarrier phase completes
+                while (!mbar_try(xbar + (u % 4), (unsigned)((u / 4) & 1))) sg.tick();
             }
             mark(t_x);
             double Q = INFINITY;
