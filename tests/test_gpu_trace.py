@@ -47,7 +47,7 @@ def oracle_errors(m, b, seed, sweeps, Vref):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("b", [3, 37])
+@pytest.mark.parametrize("b", [1, 3, 37])   # b = 1 on the cluster path: the look-ahead kernel
 def test_error_trace_matches_oracle(name, b):
     m, prob = CASES[name]()
     Vref = oracle.vi(m, m.n, eps=1e-13, max_sweeps=100000, identity=True).V
