@@ -11,9 +11,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANTS = {"nt128": ["RMB_ASYNC_NT=128"], "nt64": ["RMB_ASYNC_NT=64"],
-            "nt128_db8": ["RMB_ASYNC_NT=128", "RMB_ASYNC_DB=1", "RMB_ASYNC_AGMAX=8"],
-            "nt256_db8": ["RMB_ASYNC_NT=256", "RMB_ASYNC_DB=1", "RMB_ASYNC_AGMAX=8"]}
+VARIANTS = {"nt512": ["RMB_ASYNC_NT=512"], "nt256": ["RMB_ASYNC_NT=256"], "nt128": ["RMB_ASYNC_NT=128"],
+            "nt64": ["RMB_ASYNC_NT=64"]}
 if len(sys.argv) > 2:
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in sys.argv[2].split(",")}
 
