@@ -48,7 +48,7 @@ def one():
     import paper_2110_02901_b200 as rmb
     n, A = 10_000, 16
     P, c = rmb.generate_dense(n, A, 1)
-    prob = rmb.Problem.dense(P, c, 0.99)
+    prob = rmb.Problem.dense(P, c, 0.99, flags=rmb.DENSE_NO_TMA if os.environ.get("AB_ASYNC_REGS") else 0)
     prob.vi(1, eps=1e-6, max_sweeps=3, asynchronous=True)
     best = 1e9
     for rep in range(3):
@@ -67,5 +67,5 @@ if __name__ == "__main__":
         one()
     else:
         for name in VARIANTS:
-            env = dict(os.environ, RMB_LIB_PATH=lib_of(name))
+            env = dict(os.environ, RMB_LIB_PATH=lib_of(name), AB_ASYNC_REGS="1")
             subprocess.run([sys.executable, __file__, "one"], env=env, check=False)
